@@ -1,0 +1,308 @@
+// Migration engine: each switch's working-set transition as one coalesced
+// batch between pinned host DRAM and the HBM frame arena.
+//
+// The planner leaves a list of (page, frame) pairs: evictions first (head
+// order), then installs (populate order).  This file
+//   1. cuts the list into maximal segments that are contiguous in both the
+//      host backing (slot = dense page mod pool pages) and the frame arena;
+//   2. moves large segments with the copy engines (cudaMemcpyBatchAsync, one
+//      stream per direction so D2H and H2D overlap, full duplex), gating each
+//      install chunk on the eviction chunk that frees its frames — the real
+//      counterpart of the pipelined-swap model (engine.py:139-166);
+//   3. moves fragmented batches with SM gather/scatter kernels reading and
+//      writing mapped pinned memory with 16-byte accesses.
+#include "msched_internal.cuh"
+
+#include <algorithm>
+
+namespace msg {
+
+constexpr int64_t kTagMagic = 0x5a17c0de00000000ll;
+constexpr int64_t kSegCeMax = 1 << 16;   // CE path limit on segments per batch
+constexpr int64_t kMinCePages = 8;       // average segment size for the CE path (pages)
+
+__device__ __forceinline__ int64_t tag_of(int64_t page) { return kTagMagic ^ page; }
+
+__global__ void k_seg_mark(const int64_t* list, int64_t n, int64_t n_d2h, int64_t pool_pages, int32_t* flag) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    bool b = (i == 0 || i == n_d2h);
+    if (!b) {
+      int64_t x = list[i], y = list[i - 1];
+      int64_t p = x >> 32, q = y >> 32;
+      int32_t f = (int32_t)(uint32_t)(x & 0xffffffff), g = (int32_t)(uint32_t)(y & 0xffffffff);
+      b = (p != q + 1) || (f != g + 1) || (p % pool_pages == 0);
+    }
+    flag[i] = b ? 1 : 0;
+  }
+}
+
+__global__ void k_seg_write(const int64_t* list, int64_t n, const int32_t* flag, const int64_t* off, int64_t* segs) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    if (flag[i]) {
+      int64_t k = off[i];
+      segs[2 * k] = i;
+      segs[2 * k + 1] = list[i];
+    }
+  }
+}
+
+// SM path: one warp per page, 16-byte accesses (page size multiple of 512 B)
+__global__ void k_sm_copy(const int64_t* list, int64_t n, char* arena, char* pool, int64_t P, int64_t pool_pages,
+                          int to_host) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  int64_t v16 = P / 16;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    int64_t x = list[i];
+    int64_t page = x >> 32;
+    int64_t frame = (int64_t)(uint32_t)(x & 0xffffffff);
+    int4* a = reinterpret_cast<int4*>(arena + frame * P);
+    int4* h = reinterpret_cast<int4*>(pool + (page % pool_pages) * P);
+    if (to_host) {
+      for (int64_t k = lane; k < v16; k += 32) h[k] = a[k];
+    } else {
+      for (int64_t k = lane; k < v16; k += 32) a[k] = h[k];
+    }
+  }
+}
+
+__global__ void k_write_tags(const int64_t* list, int64_t n, char* arena, int64_t P) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t x = list[i];
+    int64_t page = x >> 32, frame = (int64_t)(uint32_t)(x & 0xffffffff);
+    *reinterpret_cast<int64_t*>(arena + frame * P) = tag_of(page);
+  }
+}
+
+__global__ void k_verify(const uint32_t* bits, const int32_t* frame, int64_t D, const char* arena, int64_t P,
+                         unsigned long long* bad) {
+  unsigned long long nb = 0;
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < D; p += (int64_t)gridDim.x * blockDim.x) {
+    bool res = (bits[p >> 5] >> (p & 31)) & 1u;
+    int32_t f = frame[p];
+    if (res != (f >= 0)) { ++nb; continue; }
+    if (res && *reinterpret_cast<const int64_t*>(arena + (int64_t)f * P) != tag_of(p)) ++nb;
+  }
+  if (nb) atomicAdd(bad, nb);
+}
+
+void migration_init(Ctx& c) {
+  MSG_CUDA(cudaStreamCreateWithFlags(&c.st_d2h, cudaStreamNonBlocking));
+  MSG_CUDA(cudaStreamCreateWithFlags(&c.st_h2d, cudaStreamNonBlocking));
+  MSG_CUDA(cudaEventCreateWithFlags(&c.ev_mig[0], cudaEventDisableTiming));
+  MSG_CUDA(cudaEventCreateWithFlags(&c.ev_mig[1], cudaEventDisableTiming));
+  MSG_CUDA(cudaEventCreateWithFlags(&c.ev_h2d_done, cudaEventDisableTiming));
+  MSG_CUDA(cudaEventCreateWithFlags(&c.ev_plan_done, cudaEventDisableTiming));
+  MSG_CUDA(cudaEventCreateWithFlags(&c.ev_d2h_prev, cudaEventDisableTiming));
+  MSG_CUDA(cudaEventRecord(c.ev_d2h_prev, c.st));
+  MSG_CUDA(cudaEventRecord(c.ev_mig[0], c.st));
+  MSG_CUDA(cudaEventRecord(c.ev_mig[1], c.st));
+  MSG_CUDA(cudaEventRecord(c.ev_h2d_done, c.st));
+  MSG_CUDA(cudaEventRecord(c.ev_plan_done, c.st));
+  if (!(c.cfg.flags & (MSG_F_MIGRATE | MSG_F_VERIFY_TAGS))) return;
+  if (c.P % 512 != 0) throw Error(MSG_E_INVAL, "migration needs page_size to be a multiple of 512 bytes");
+  size_t abytes = (size_t)c.C * (size_t)c.P;
+  if (cudaMalloc(&c.arena, abytes) != cudaSuccess) {
+    cudaGetLastError();
+    throw Error(MSG_E_OOM, "HBM frame arena of " + std::to_string(abytes) + " bytes does not fit");
+  }
+  c.pool_pages = c.cfg.host_pool_pages > 0 ? std::min<int64_t>(c.cfg.host_pool_pages, c.D) : c.D;
+  if (c.pool_pages < 1) c.pool_pages = 1;
+  size_t pbytes = (size_t)c.pool_pages * (size_t)c.P;
+  if (cudaHostAlloc(reinterpret_cast<void**>(&c.pool), pbytes, cudaHostAllocMapped | cudaHostAllocPortable) !=
+      cudaSuccess) {
+    cudaGetLastError();
+    throw Error(MSG_E_OOM, "pinned host pool of " + std::to_string(pbytes) + " bytes failed");
+  }
+  MSG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.pool_dev), c.pool, 0));
+  if (c.cfg.flags & MSG_F_VERIFY_TAGS) {
+    for (int64_t s = 0; s < c.pool_pages; ++s) *reinterpret_cast<int64_t*>(c.pool + s * c.P) = kTagMagic ^ s;
+  }
+}
+
+static cudaEvent_t new_event(Ctx& c, bool timing) {
+  cudaEvent_t e;
+  MSG_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
+  c.ev_pool.push_back(e);
+  return e;
+}
+
+static void ce_batch(std::vector<void*>& d, std::vector<void*>& s, std::vector<size_t>& z, cudaStream_t st) {
+  if (d.empty()) return;
+  cudaMemcpyAttributes attr = {};
+  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  size_t idx0 = 0, fail = 0;
+  MSG_CUDA(cudaMemcpyBatchAsync(d.data(), s.data(), z.data(), d.size(), &attr, &idx0, 1, &fail, st));
+  d.clear(); s.clear(); z.clear();
+}
+
+void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bool copy_h2d) {
+  int par = c.mig_par;
+  int64_t n = n_d2h + n_h2d;
+  const int64_t* list = c.mig_list[par].p;
+  bool real = c.cfg.flags & MSG_F_MIGRATE;
+  if (n == 0) return;
+  if (!real) {
+    // bookkeeping only: frames receive their page's tag as if the copy happened
+    if (n_h2d) {
+      k_write_tags<<<std::min<int64_t>((n_h2d + 255) / 256, 1184), 256, 0, c.st>>>(list + n_d2h, n_h2d, c.arena, c.P);
+      MSG_CHECK_LAUNCH();
+      add_launches(1);
+    }
+    MSG_CUDA(cudaEventRecord(c.ev_mig[par], c.st));
+    c.mig_par ^= 1;
+    return;
+  }
+  // 1. segments
+  c.s.mflag.resize(n, c.st);
+  c.s.moff.resize(n, c.st);
+  c.s.msegs.resize(2 * n + 2, c.st);
+  int grid = (int)std::min<int64_t>((n + 255) / 256, 1184);
+  k_seg_mark<<<grid, 256, 0, c.st>>>(list, n, n_d2h, c.pool_pages, c.s.mflag.p);
+  MSG_CHECK_LAUNCH();
+  scan_flags(c, c.s.mflag.p, n, c.s.moff.p);
+  k_seg_write<<<grid, 256, 0, c.st>>>(list, n, c.s.mflag.p, c.s.moff.p, c.s.msegs.p);
+  MSG_CHECK_LAUNCH();
+  add_launches(2);
+  int64_t* hb = c.hbuf.p;
+  MSG_CUDA(cudaMemcpyAsync(hb, c.s.moff.p + n - 1, 8, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaMemcpyAsync(hb + 1, c.s.mflag.p + n - 1, 4, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  int64_t nseg = hb[0] + (int64_t)(*reinterpret_cast<int32_t*>(hb + 1));
+  bool use_ce = nseg <= kSegCeMax && n >= kMinCePages * nseg;
+  cudaEvent_t planned = new_event(c, false);
+  MSG_CUDA(cudaEventRecord(planned, c.st));
+  // frames written by earlier installs must land before they are read back
+  MSG_CUDA(cudaStreamWaitEvent(c.st_d2h, c.ev_h2d_done, 0));
+  cudaEvent_t d2h_start = new_event(c, true), d2h_end = new_event(c, true);
+  cudaEvent_t h2d_start = new_event(c, true), h2d_end = new_event(c, true);
+  if (!use_ce) {
+    c.stats.sm_batches++;
+    MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, planned, 0));
+    MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_d2h_prev, 0));
+    MSG_CUDA(cudaEventRecord(d2h_start, c.st_h2d));
+    if (n_d2h) k_sm_copy<<<296, 256, 0, c.st_h2d>>>(list, n_d2h, c.arena, c.pool_dev, c.P, c.pool_pages, 1);
+    MSG_CUDA(cudaEventRecord(d2h_end, c.st_h2d));
+    MSG_CUDA(cudaEventRecord(h2d_start, c.st_h2d));
+    if (n_h2d) {
+      if (copy_h2d) k_sm_copy<<<296, 256, 0, c.st_h2d>>>(list + n_d2h, n_h2d, c.arena, c.pool_dev, c.P, c.pool_pages, 0);
+      else if (c.cfg.flags & MSG_F_VERIFY_TAGS)
+        k_write_tags<<<std::min<int64_t>((n_h2d + 255) / 256, 1184), 256, 0, c.st_h2d>>>(list + n_d2h, n_h2d, c.arena, c.P);
+    }
+    MSG_CHECK_LAUNCH();
+    add_launches(2);
+    MSG_CUDA(cudaEventRecord(h2d_end, c.st_h2d));
+    MSG_CUDA(cudaEventRecord(c.ev_h2d_done, c.st_h2d));
+    MSG_CUDA(cudaEventRecord(c.ev_d2h_prev, c.st_h2d));
+    MSG_CUDA(cudaEventRecord(c.ev_mig[par], c.st_h2d));
+    if (copy_h2d) c.stats.h2d_bytes += n_h2d * c.P;
+    c.stats.d2h_bytes += n_d2h * c.P;
+  } else {
+    c.stats.ce_batches++;
+    std::vector<int64_t> segs(2 * nseg);
+    MSG_CUDA(cudaMemcpyAsync(segs.data(), c.s.msegs.p, 2 * nseg * 8, cudaMemcpyDeviceToHost, c.st));
+    MSG_CUDA(cudaStreamSynchronize(c.st));
+    MSG_CUDA(cudaEventRecord(c.ev_mig[par], c.st));  // the device list is no longer needed
+    auto seg_at = [&](int64_t k, int64_t* i0, int64_t* len, int64_t* page, int64_t* frame) {
+      *i0 = segs[2 * k];
+      int64_t nxt = k + 1 < nseg ? segs[2 * (k + 1)] : n;
+      *len = nxt - *i0;
+      *page = segs[2 * k + 1] >> 32;
+      *frame = (int64_t)(uint32_t)(segs[2 * k + 1] & 0xffffffff);
+    };
+    // evictions, in chunks; each chunk's completion is an event that gates
+    // the installs reusing its frames
+    const int kChunks = 8;
+    int64_t chunk = std::max<int64_t>((n_d2h + kChunks - 1) / kChunks, 1);
+    std::vector<std::pair<int64_t, cudaEvent_t>> done;   // (evictions complete up to, event)
+    std::vector<void*> dd, ss;
+    std::vector<size_t> zz;
+    MSG_CUDA(cudaEventRecord(d2h_start, c.st_d2h));
+    int64_t k = 0, next_cut = chunk;
+    for (; k < nseg; ++k) {
+      int64_t i0, len, page, frame;
+      seg_at(k, &i0, &len, &page, &frame);
+      if (i0 >= n_d2h) break;
+      dd.push_back(c.pool + (page % c.pool_pages) * c.P);
+      ss.push_back(c.arena + frame * c.P);
+      zz.push_back((size_t)(len * c.P));
+      c.stats.d2h_bytes += len * c.P;
+      c.stats.d2h_segments++;
+      if (i0 + len >= next_cut && i0 + len < n_d2h) {
+        ce_batch(dd, ss, zz, c.st_d2h);
+        cudaEvent_t e = new_event(c, false);
+        MSG_CUDA(cudaEventRecord(e, c.st_d2h));
+        done.push_back({i0 + len, e});
+        next_cut = ((i0 + len) / chunk + 1) * chunk;
+      }
+    }
+    ce_batch(dd, ss, zz, c.st_d2h);
+    MSG_CUDA(cudaEventRecord(d2h_end, c.st_d2h));
+    done.push_back({n_d2h, d2h_end});
+    // installs: frames that were free before this batch may still be draining
+    // from earlier evictions; frames freed by this batch wait for their chunk
+    MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_d2h_prev, 0));
+    MSG_CUDA(cudaEventRecord(h2d_start, c.st_h2d));
+    size_t waited = 0;
+    bool any_wait = false;
+    for (; k < nseg; ++k) {
+      int64_t i0, len, page, frame;
+      seg_at(k, &i0, &len, &page, &frame);
+      int64_t e_idx = (i0 - n_d2h) + len - 1 - free_before;   // last eviction this segment depends on
+      if (e_idx >= 0) {
+        size_t need = 0;
+        while (need + 1 < done.size() && done[need].first <= e_idx) ++need;
+        if (!any_wait || need > waited) {
+          ce_batch(dd, ss, zz, c.st_h2d);
+          MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, done[need].second, 0));
+          waited = need;
+          any_wait = true;
+        }
+      }
+      if (copy_h2d) {
+        dd.push_back(c.arena + frame * c.P);
+        ss.push_back(c.pool + (page % c.pool_pages) * c.P);
+        zz.push_back((size_t)(len * c.P));
+        c.stats.h2d_bytes += len * c.P;
+        c.stats.h2d_segments++;
+      }
+    }
+    ce_batch(dd, ss, zz, c.st_h2d);
+    if (!copy_h2d && (c.cfg.flags & MSG_F_VERIFY_TAGS) && n_h2d) {
+      // installs that carry their own data (memcpy): stamp the frames instead
+      MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, d2h_end, 0));
+      MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, planned, 0));
+      k_write_tags<<<std::min<int64_t>((n_h2d + 255) / 256, 1184), 256, 0, c.st_h2d>>>(list + n_d2h, n_h2d, c.arena, c.P);
+      MSG_CHECK_LAUNCH();
+      add_launches(1);
+      MSG_CUDA(cudaEventRecord(c.ev_mig[par], c.st_h2d));
+    }
+    MSG_CUDA(cudaEventRecord(h2d_end, c.st_h2d));
+    MSG_CUDA(cudaEventRecord(c.ev_h2d_done, c.st_h2d));
+    MSG_CUDA(cudaEventRecord(c.ev_d2h_prev, c.st_d2h));
+  }
+  c.busy_d2h.push_back({d2h_start, d2h_end});
+  c.busy_h2d.push_back({h2d_start, h2d_end});
+  c.mig_par ^= 1;
+}
+
+void verify_tags(Ctx& c, int64_t* bad) {
+  if (!(c.cfg.flags & MSG_F_VERIFY_TAGS)) throw Error(MSG_E_INVAL, "context created without MSG_F_VERIFY_TAGS");
+  if (c.pool_pages < c.D) throw Error(MSG_E_INVAL, "tag verification needs an unaliased host pool");
+  MSG_CUDA(cudaDeviceSynchronize());
+  unsigned long long* d = nullptr;
+  MSG_CUDA(cudaMalloc(&d, 8));
+  MSG_CUDA(cudaMemset(d, 0, 8));
+  k_verify<<<1184, 256, 0, c.st>>>(c.bits.p, c.frame.p, c.D, c.arena, c.P, d);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  unsigned long long h = 0;
+  MSG_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  cudaFree(d);
+  *bad = (int64_t)h;
+}
+
+}  // namespace msg

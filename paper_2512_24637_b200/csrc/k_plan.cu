@@ -1,0 +1,1602 @@
+// K3-K6, K8, K9 — the placement planner on the device.
+//
+// Data layout in HBM (per context):
+//   bits[]    resident bitmap over the dense page space (1 bit / page)
+//   order[2]  the eviction list as a dense array of page ids, head -> tail
+//             (ping-pong buffers; live region order[cur][head, head+len))
+//   frame[]   HBM frame of every resident dense page (-1 otherwise)
+//   fifo[]    free-frame ring: populate j takes the j-th free frame, frames
+//             released by eviction are appended in eviction order, so the
+//             frame reuse order matches the pipelined-swap model
+//             (engine.py:139-158).
+//
+// reorder_for_opt (memman.py:218-241) is restated exactly as ONE stable
+// multisplit of the eviction list: every resident page gets a class equal to
+// the dense rank of its tuple (class in window 0, ..., class in window W-1),
+// where a page's class in window w is (K_w - r) for the r-th first-access run
+// of that window (0 if absent).  Stable partition by that class reproduces the
+// reference's sequence of per-run madvise calls (windows last to first, runs
+// last to first) — see DESIGN.md §3 for the proof sketch.  Victims are then
+// the list head (plan_migration reads evlist._runs head-first,
+// memman.py:292-301), so victim selection is a prefix, not a search.
+#include "msched_internal.cuh"
+
+#include <algorithm>
+
+namespace msg {
+
+static int64_t g_launches = 0;
+int64_t kernel_launches() { return g_launches; }
+void add_launches(int64_t n) { g_launches += n; }
+
+// ---------------------------------------------------------------------------
+// block-level helpers
+
+template <class T>
+__device__ T block_excl_scan(T v, T* smem_warp, T* total) {
+  // blockDim.x multiple of 32, <= 1024
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  T x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    T y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    T s = lane < nw ? smem_warp[lane] : T(0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      T y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) smem_warp[lane] = s;
+  }
+  __syncthreads();
+  T before = (wid ? smem_warp[wid - 1] : T(0)) + x - v;
+  if (total) *total = smem_warp[nw - 1];
+  __syncthreads();
+  return before;
+}
+
+// Block-wide exclusive scan of a[0..n) in place (any n); returns the total.
+template <class T>
+__device__ T block_scan_array(T* a, int64_t n) {
+  __shared__ T warp_s[32];
+  __shared__ T carry_s;
+  if (threadIdx.x == 0) carry_s = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < n; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    T v = i < n ? a[i] : T(0);
+    T tot;
+    T ex = block_excl_scan<T>(v, warp_s, &tot);
+    T carry = carry_s;
+    if (i < n) a[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry_s = carry + tot;
+    __syncthreads();
+  }
+  return carry_s;
+}
+
+// Bitonic sort of uint64 keys with int64 payload, n padded to a power of two.
+__device__ void bitonic_kv(uint64_t* key, int64_t* val, int64_t npow2) {
+  for (int64_t k = 2; k <= npow2; k <<= 1) {
+    for (int64_t j = k >> 1; j > 0; j >>= 1) {
+      for (int64_t i = threadIdx.x; i < npow2; i += blockDim.x) {
+        int64_t l = i ^ j;
+        if (l > i) {
+          bool up = (i & k) == 0;
+          if ((key[i] > key[l]) == up) {
+            uint64_t tk = key[i]; key[i] = key[l]; key[l] = tk;
+            int64_t tv = val[i]; val[i] = val[l]; val[l] = tv;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ __forceinline__ int64_t lower_bound_i64(const int64_t* a, int64_t n, int64_t x) {
+  int64_t lo = 0, hi = n;
+  while (lo < hi) {
+    int64_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+
+__host__ __device__ inline int64_t pow2_at_least(int64_t n) {
+  int64_t p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+// ---------------------------------------------------------------------------
+// K3: per-window first-access runs (memman.py:174-196).  One CTA per window.
+
+struct WinDesc {
+  const Iv* pool;               // the task's predicted intervals
+  int64_t pool_lo, pool_hi;    // predicted intervals of commands [c0, c1)
+  int32_t c0, c1, w, pad;
+  const int64_t* cmd_off;      // task CSR offsets (pool indices), ncmd+1
+  const uint8_t* selfpop;
+  int64_t scratch;             // offset of this window's scratch region (elements)
+};
+
+struct WinOut {
+  // per window: runs in first-access order (label asc, start asc)
+  int64_t* run_a;   // abs start
+  int64_t* run_b;   // abs end
+  int64_t* run_d;   // dense start
+  int32_t* run_lab; // command index
+  int64_t* run_base;// per-window offset into the run arrays (= scratch base)
+  int64_t* nruns;   // per window
+  int64_t* pages;   // per window |w.pages|
+};
+
+__global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, int64_t* gkey_u, int64_t* gval,
+                              int32_t* glab, WinOut out) {
+  const WinDesc W = wins[blockIdx.x];
+  const Iv* pool = W.pool;
+  int64_t n = W.pool_hi - W.pool_lo;
+  int64_t base = W.scratch;           // scratch: 4n slots of key/val, 2n labels
+  uint64_t* key = reinterpret_cast<uint64_t*>(gkey_u) + base;
+  int64_t* val = gval + base;
+  __shared__ int64_t tot_s;
+  if (n == 0) {
+    if (threadIdx.x == 0) { out.nruns[W.w] = 0; out.pages[W.w] = 0; out.run_base[W.w] = base; }
+    return;
+  }
+  // 1. endpoints, sorted
+  int64_t m = 2 * n, mp = pow2_at_least(m);
+  for (int64_t i = threadIdx.x; i < mp; i += blockDim.x) {
+    if (i < m) {
+      const Iv& v = pool[W.pool_lo + (i >> 1)];
+      key[i] = (uint64_t)((i & 1) ? v.b : v.a) ^ 0x8000000000000000ull;  // order-preserving
+    } else {
+      key[i] = ~0ull;
+    }
+    val[i] = 0;
+  }
+  __syncthreads();
+  bitonic_kv(key, val, mp);
+  // 2. unique: flag first occurrences, scan to positions (val holds flags)
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) val[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
+  __syncthreads();
+  int64_t* pos = val;
+  int64_t nu = block_scan_array<int64_t>(pos, m);
+  // compact unique endpoints into E (reuse key region after m: use val2 area)
+  int64_t* E = reinterpret_cast<int64_t*>(key) + mp;  // scratch has room: 4n >= mp + m
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+    bool first = (i == 0 || key[i] != key[i - 1]);
+    if (first) E[pos[i]] = (int64_t)(key[i] ^ 0x8000000000000000ull);
+  }
+  __syncthreads();
+  int64_t nseg = nu - 1;
+  int32_t* L = glab + base;   // 2n labels available
+  for (int64_t k = threadIdx.x; k < nseg; k += blockDim.x) L[k] = kNone;
+  __syncthreads();
+  // 3. label = min covering command (first access)
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+    const Iv& v = pool[W.pool_lo + i];
+    // command of interval i: largest c with cmd_off[c] <= pool_lo + i
+    int64_t gi = W.pool_lo + i;
+    int32_t lo = W.c0, hi = W.c1;
+    while (lo < hi) {
+      int32_t mid = (lo + hi) >> 1;
+      if (W.cmd_off[mid + 1] <= gi) lo = mid + 1; else hi = mid;
+    }
+    int32_t cmd = lo;
+    int64_t s0 = lower_bound_i64(E, nu, v.a), s1 = lower_bound_i64(E, nu, v.b);
+    for (int64_t k = s0; k < s1; ++k) atomicMin(&L[k], cmd);
+  }
+  __syncthreads();
+  // 4. runs: maximal segment groups with one label (segments abut by construction)
+  int64_t* rflag = val;  // reuse: run-start flags -> run ids
+  for (int64_t k = threadIdx.x; k < nseg; k += blockDim.x)
+    rflag[k] = (L[k] != kNone && (k == 0 || L[k - 1] != L[k])) ? 1 : 0;
+  __syncthreads();
+  int64_t nr = block_scan_array<int64_t>(rflag, nseg);
+  // run r: start segment = the k with flag; end = first k' > k with L[k'] != L[k]
+  int64_t* ra = out.run_a + base;
+  int64_t* rb = out.run_b + base;
+  int32_t* rl = out.run_lab + base;
+  for (int64_t k = threadIdx.x; k < nseg; k += blockDim.x) {
+    if (L[k] == kNone) continue;
+    bool start = (k == 0 || L[k - 1] != L[k]);
+    bool end = (k + 1 == nseg || L[k + 1] != L[k]);
+    int64_t r = rflag[k] - (start ? 0 : 0);
+    // rflag is an exclusive scan of start flags: for a start segment it is its run id;
+    // for non-start segments it equals (id of its run) + 1.
+    int64_t id = start ? r : r - 1;
+    if (start) { ra[id] = E[k]; rl[id] = L[k]; }
+    if (end) rb[id] = E[k + 1];
+  }
+  __syncthreads();
+  // 5. order runs by (label, start): key = label << 32 | run id (ids are in start order)
+  int64_t rp = pow2_at_least(nr);
+  uint64_t* k2 = key;       // reuse sort buffers (E no longer needed after this)
+  int64_t* v2 = val;
+  // E lives at key + mp; make sure we do not overwrite it before use: copy runs first
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < rp; i += blockDim.x) {
+    k2[i] = i < nr ? (((uint64_t)(uint32_t)rl[i] << 32) | (uint64_t)i) : ~0ull;
+    v2[i] = i;
+  }
+  __syncthreads();
+  bitonic_kv(k2, v2, rp);
+  // gather into final order (use the label area beyond nr as temp for permuted copy)
+  int64_t* ta = reinterpret_cast<int64_t*>(key) + rp;   // temp arrays
+  int64_t* tb = ta + nr;
+  int32_t* tl = reinterpret_cast<int32_t*>(tb + nr);
+  for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) {
+    int64_t src = v2[i];
+    ta[i] = ra[src]; tb[i] = rb[src]; tl[i] = rl[src];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) tot_s = 0;
+  __syncthreads();
+  int64_t mine = 0;
+  for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) {
+    ra[i] = ta[i]; rb[i] = tb[i]; rl[i] = tl[i];
+    mine += tb[i] - ta[i];
+  }
+  atomicAdd(reinterpret_cast<unsigned long long*>(&tot_s), (unsigned long long)mine);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out.nruns[W.w] = nr;
+    out.pages[W.w] = tot_s;
+    out.run_base[W.w] = base;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Cross-window class table: elementary segments of all windows' runs, each
+// with its tuple of per-window classes, ranked lexicographically.
+
+struct CombineParams {
+  int32_t nwin;
+  const int64_t* run_a; const int64_t* run_b; const int32_t* run_lab;
+  const int64_t* run_base; const int64_t* nruns;
+  const int32_t* run_cls;   // optional explicit class per run (facade); else K_w - rank
+  // dense map
+  const int64_t* span_first; const int64_t* span_n; const int64_t* span_dense; int32_t nspans;
+  // scratch (sized by host)
+  uint64_t* key; int64_t* val; int64_t* E; int32_t* T; int64_t* idx;
+  // outputs: covered segments sorted by dense start
+  int64_t* seg_lo; int64_t* seg_hi; int32_t* seg_cls; int64_t* nseg_out; int64_t* ncls_out;
+};
+
+__device__ int64_t dense_at(const CombineParams& P, int64_t a) {
+  int lo = 0, hi = P.nspans;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (P.span_first[mid] <= a) lo = mid + 1; else hi = mid;
+  }
+  int s = lo - 1;
+  return P.span_dense[s] + (a - P.span_first[s]);
+}
+
+__device__ __forceinline__ int tuple_cmp(const int32_t* T, int64_t i, int64_t j, int W) {
+  for (int w = 0; w < W; ++w) {
+    int32_t a = T[i * W + w], b = T[j * W + w];
+    if (a != b) return a < b ? -1 : 1;
+  }
+  return 0;
+}
+
+__global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P) {
+  __shared__ int64_t tot_runs_s;
+  int W = P.nwin;
+  // gather all runs' endpoints
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < W; ++w) t += P.nruns[w];
+    tot_runs_s = t;
+  }
+  __syncthreads();
+  int64_t M = tot_runs_s;
+  if (M == 0) {
+    if (threadIdx.x == 0) { *P.nseg_out = 0; *P.ncls_out = 0; }
+    return;
+  }
+  int64_t m = 2 * M, mp = pow2_at_least(m);
+  // flatten (w, r) -> global run index g via per-window prefix (small W: linear walk)
+  for (int64_t i = threadIdx.x; i < mp; i += blockDim.x) {
+    if (i < m) {
+      int64_t g = i >> 1, w = 0;
+      while (g >= P.nruns[w]) { g -= P.nruns[w]; ++w; }
+      int64_t r = P.run_base[w] + g;
+      P.key[i] = (uint64_t)((i & 1) ? P.run_b[r] : P.run_a[r]) ^ 0x8000000000000000ull;
+    } else {
+      P.key[i] = ~0ull;
+    }
+    P.val[i] = 0;
+  }
+  __syncthreads();
+  bitonic_kv(P.key, P.val, mp);
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) P.val[i] = (i == 0 || P.key[i] != P.key[i - 1]) ? 1 : 0;
+  __syncthreads();
+  int64_t nu = block_scan_array<int64_t>(P.val, m);
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x)
+    if (i == 0 || P.key[i] != P.key[i - 1]) P.E[P.val[i]] = (int64_t)(P.key[i] ^ 0x8000000000000000ull);
+  __syncthreads();
+  int64_t ns = nu - 1;
+  for (int64_t i = threadIdx.x; i < ns * W; i += blockDim.x) P.T[i] = 0;
+  __syncthreads();
+  // paint each run's class (K_w - rank) over its segments
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    int64_t g = i, w = 0;
+    while (g >= P.nruns[w]) { g -= P.nruns[w]; ++w; }
+    int64_t r = P.run_base[w] + g;
+    int32_t cls = P.run_cls ? P.run_cls[r] : (int32_t)(P.nruns[w] - g);
+    int64_t s0 = lower_bound_i64(P.E, nu, P.run_a[r]), s1 = lower_bound_i64(P.E, nu, P.run_b[r]);
+    for (int64_t k = s0; k < s1; ++k) P.T[k * W + w] = cls;
+  }
+  __syncthreads();
+  // covered segments -> compact indices
+  for (int64_t k = threadIdx.x; k < ns; k += blockDim.x) {
+    bool cov = false;
+    for (int w = 0; w < W; ++w) cov |= P.T[k * W + w] != 0;
+    P.val[k] = cov ? 1 : 0;
+  }
+  __syncthreads();
+  int64_t nc = block_scan_array<int64_t>(P.val, ns);
+  for (int64_t k = threadIdx.x; k < ns; k += blockDim.x) {
+    bool cov = (k + 1 < ns ? P.val[k + 1] : nc) != P.val[k];
+    if (cov) P.idx[P.val[k]] = k;
+  }
+  __syncthreads();
+  // sort covered segments by tuple (comparison bitonic over indices)
+  int64_t cp = pow2_at_least(nc);
+  int64_t* perm = P.val;  // reuse
+  for (int64_t i = threadIdx.x; i < cp; i += blockDim.x) perm[i] = i < nc ? P.idx[i] : -1;
+  __syncthreads();
+  for (int64_t k = 2; k <= cp; k <<= 1) {
+    for (int64_t j = k >> 1; j > 0; j >>= 1) {
+      for (int64_t i = threadIdx.x; i < cp; i += blockDim.x) {
+        int64_t l = i ^ j;
+        if (l > i) {
+          bool up = (i & k) == 0;
+          int64_t a = perm[i], b = perm[l];
+          int c;
+          if (a < 0 && b < 0) c = 0;
+          else if (a < 0) c = 1;
+          else if (b < 0) c = -1;
+          else { c = tuple_cmp(P.T, a, b, W); if (c == 0) c = a < b ? -1 : (a > b ? 1 : 0); }
+          if ((c > 0) == up) { perm[i] = b; perm[l] = a; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // dense rank of distinct tuples (1-based); write class per segment via key scratch
+  int64_t* rk = reinterpret_cast<int64_t*>(P.key);
+  for (int64_t i = threadIdx.x; i < nc; i += blockDim.x)
+    rk[i] = (i == 0 || tuple_cmp(P.T, perm[i - 1], perm[i], W) != 0) ? 1 : 0;
+  __syncthreads();
+  int64_t ndist = block_scan_array<int64_t>(rk, nc);
+  // rk[i] = (#distinct before i); class = rk + (first? 1 : 0) ... recompute inclusive
+  for (int64_t i = threadIdx.x; i < nc; i += blockDim.x) {
+    bool first = (i == 0 || tuple_cmp(P.T, perm[i - 1], perm[i], W) != 0);
+    int64_t cls = rk[i] + (first ? 1 : 0);
+    // store into T's first column slot of that segment is unsafe (needed by neighbours);
+    // write to the output by covered position instead: segments in E order
+    P.E[nu + perm[i]] = cls;      // scratch after E: class per segment index
+  }
+  __syncthreads();
+  for (int64_t ci = threadIdx.x; ci < nc; ci += blockDim.x) {
+    int64_t k = P.idx[ci];
+    P.seg_lo[ci] = dense_at(P, P.E[k]);
+    P.seg_hi[ci] = P.seg_lo[ci] + (P.E[k + 1] - P.E[k]);
+    P.seg_cls[ci] = (int32_t)P.E[nu + k];
+  }
+  if (threadIdx.x == 0) { *P.nseg_out = nc; *P.ncls_out = ndist; }
+}
+
+// ---------------------------------------------------------------------------
+// Demand runs of window 0 vs the resident bitmap (engine.py:310-313,
+// memman.py:284-291, engine.py:350-355).
+
+__device__ __forceinline__ bool is_res(const uint32_t* bits, int64_t p) {
+  return (bits[p >> 5] >> (p & 31)) & 1u;
+}
+
+// count non-resident pages of dense ranges [lo, lo+len): one warp per range
+__device__ int64_t warp_count_nonres(const uint32_t* bits, int64_t lo, int64_t len) {
+  int lane = threadIdx.x & 31;
+  int64_t hi = lo + len, acc = 0;
+  int64_t w0 = lo >> 5, w1 = (hi + 31) >> 5;
+  for (int64_t w = w0 + lane; w < w1; w += 32) {
+    uint32_t word = ~bits[w];
+    int64_t p0 = w << 5;
+    if (p0 < lo) word &= ~0u << (lo - p0);
+    if (p0 + 32 > hi) word &= (hi - p0) >= 32 ? ~0u : ((1u << (hi - p0)) - 1u);
+    acc += __popc(word);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  return acc;
+}
+
+struct DemandParams {
+  const int64_t* run_a; const int64_t* run_b; const int32_t* run_lab; int64_t run_base; const int64_t* nruns;
+  const uint8_t* selfpop; int32_t c0;
+  const int64_t* span_first; const int64_t* span_n; const int64_t* span_dense; int32_t nspans;
+  const uint32_t* bits;
+  int64_t* dlo; int64_t* dlen; int64_t* dmiss; int64_t* dlab;  // compacted demand runs
+  int64_t* ndemand;
+  int64_t* prefix;   // per command of window 0
+};
+
+__global__ void __launch_bounds__(1024, 1) k_demand_collect(DemandParams P) {
+  // single block: compact window-0 runs whose first-access command is not self-populating
+  int64_t nr = P.nruns[0];
+  __shared__ int64_t ws[32];
+  __shared__ int64_t carry;
+  if (threadIdx.x == 0) carry = 0;
+  __syncthreads();
+  for (int64_t base = 0; base < nr; base += blockDim.x) {
+    int64_t i = base + threadIdx.x;
+    bool keep = false;
+    int64_t r = P.run_base + i;
+    if (i < nr) keep = !P.selfpop[P.run_lab[r]];
+    int64_t tot;
+    int64_t ex = block_excl_scan<int64_t>(keep ? 1 : 0, ws, &tot);
+    if (keep) {
+      int64_t o = carry + ex;
+      int64_t a = P.run_a[r];
+      int lo = 0, hi = P.nspans;
+      while (lo < hi) { int mid = (lo + hi) >> 1; if (P.span_first[mid] <= a) lo = mid + 1; else hi = mid; }
+      int s = lo - 1;
+      P.dlo[o] = P.span_dense[s] + (a - P.span_first[s]);
+      P.dlen[o] = P.run_b[r] - a;
+      P.dlab[o] = P.run_lab[r] - P.c0;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *P.ndemand = carry;
+}
+
+__global__ void k_demand_count(DemandParams P) {
+  int64_t nd = *P.ndemand;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < nd; r += nwarps) {
+    int64_t c = warp_count_nonres(P.bits, P.dlo[r], P.dlen[r]);
+    if ((threadIdx.x & 31) == 0) {
+      P.dmiss[r] = c;
+      atomicAdd(reinterpret_cast<unsigned long long*>(&P.prefix[P.dlab[r]]), (unsigned long long)c);
+    }
+  }
+}
+
+// exclusive scan of dmiss (single block) and the plan scalars
+__global__ void __launch_bounds__(1024, 1) k_demand_scan(DemandParams P, DevState* S, int64_t capacity, int64_t len) {
+  int64_t nd = *P.ndemand;
+  int64_t total = block_scan_array<int64_t>(P.dmiss, nd);
+  if (threadIdx.x == 0) {
+    S->missing = total;
+    int64_t pop = total < capacity ? total : capacity;
+    S->populate = pop;
+    S->truncated = total - pop;
+    S->free_before = capacity - len;
+    int64_t ev = pop - (capacity - len);
+    S->evict = ev > 0 ? ev : 0;
+    S->skip = total == 0;
+  }
+}
+
+// write the populate list: non-resident pages of each demand run, in order,
+// truncated at `populate` (memman.py:284-291).  One warp per run.
+__global__ void k_demand_fill(DemandParams P, const DevState* S, int32_t* out) {
+  int64_t nd = *P.ndemand, cap = S->populate;
+  int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < nd; r += nwarps) {
+    int64_t o = P.dmiss[r];
+    if (o >= cap) continue;
+    int64_t lo = P.dlo[r], hi = lo + P.dlen[r];
+    for (int64_t p0 = lo; p0 < hi && o < cap; p0 += 32) {
+      int64_t p = p0 + lane;
+      bool want = p < hi && !is_res(P.bits, p);
+      uint32_t m = __ballot_sync(0xffffffffu, want);
+      int64_t at = o + __popc(m & ((1u << lane) - 1u));
+      if (want && at < cap) out[at] = (int32_t)p;
+      o += __popc(m);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Multisplit of the eviction list (the reorder / madvise / remove kernel).
+
+constexpr int MS_THREADS = 256;
+constexpr int MS_ITEMS = 16;
+constexpr int MS_TILE = MS_THREADS * MS_ITEMS;
+constexpr int MS_SMEM_SEGS = 1536;
+
+struct SegTab {
+  const int64_t* lo; const int64_t* hi; const int32_t* cls; const int64_t* n;
+};
+
+struct MsSmem {
+  int64_t lo[MS_SMEM_SEGS];
+  int64_t hi[MS_SMEM_SEGS];
+  int32_t cls[MS_SMEM_SEGS];
+  int32_t cnt[MS_THREADS / 32][256];
+};
+
+__device__ __forceinline__ int32_t class_lookup(int64_t p, const int64_t* lo, const int64_t* hi,
+                                                const int32_t* cls, int64_t n) {
+  int64_t a = 0, b = n;
+  while (a < b) {
+    int64_t mid = (a + b) >> 1;
+    if (lo[mid] <= p) a = mid + 1; else b = mid;
+  }
+  --a;
+  return (a >= 0 && p < hi[a]) ? cls[a] : 0;
+}
+
+__device__ void ms_load_table(const SegTab& T, MsSmem& sm, const int64_t** lo, const int64_t** hi,
+                              const int32_t** cls, int64_t* n) {
+  int64_t nn = *T.n;
+  *n = nn;
+  if (nn <= MS_SMEM_SEGS) {
+    for (int64_t i = threadIdx.x; i < nn; i += blockDim.x) { sm.lo[i] = T.lo[i]; sm.hi[i] = T.hi[i]; sm.cls[i] = T.cls[i]; }
+    *lo = sm.lo; *hi = sm.hi; *cls = sm.cls;
+  } else {
+    *lo = T.lo; *hi = T.hi; *cls = T.cls;
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(MS_THREADS) k_ms_count(const int32_t* __restrict__ src, int64_t n, SegTab T,
+                                                         int shift, int32_t* __restrict__ hist, int64_t ntiles) {
+  __shared__ MsSmem sm;
+  const int64_t *lo, *hi; const int32_t* cls; int64_t nt;
+  ms_load_table(T, sm, &lo, &hi, &cls, &nt);
+  int32_t* h = sm.cnt[0];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * MS_TILE;
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#pragma unroll 4
+  for (int it = 0; it < MS_ITEMS; ++it) {
+    int64_t i = base + warp * (MS_ITEMS * 32) + it * 32 + lane;
+    if (i < n) {
+      int32_t c = class_lookup(src[i], lo, hi, cls, nt);
+      atomicAdd(&h[(c >> shift) & 255], 1);
+    }
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[(int64_t)d * ntiles + blockIdx.x] = h[d];
+}
+
+__global__ void __launch_bounds__(MS_THREADS) k_ms_scatter(const int32_t* __restrict__ src, int64_t n, SegTab T,
+                                                           int shift, const int64_t* __restrict__ goff, int64_t ntiles,
+                                                           int32_t* __restrict__ dst) {
+  __shared__ MsSmem sm;
+  const int64_t *lo, *hi; const int32_t* cls; int64_t nt;
+  ms_load_table(T, sm, &lo, &hi, &cls, &nt);
+  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = lane; i < 256; i += 32) sm.cnt[warp][i] = 0;
+  __syncwarp();
+  int64_t base = (int64_t)blockIdx.x * MS_TILE;
+  int32_t v[MS_ITEMS];
+  int32_t dg[MS_ITEMS];
+  int32_t rk[MS_ITEMS];
+  const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+  for (int it = 0; it < MS_ITEMS; ++it) {
+    int64_t i = base + warp * (MS_ITEMS * 32) + it * 32 + lane;
+    int d = 256;
+    if (i < n) {
+      v[it] = src[i];
+      d = (class_lookup(v[it], lo, hi, cls, nt) >> shift) & 255;
+    }
+    dg[it] = d;
+    uint32_t peers = __match_any_sync(0xffffffffu, d);
+    int leader = __ffs(peers) - 1;
+    int32_t before = d < 256 ? sm.cnt[warp][d] : 0;
+    __syncwarp();
+    if (lane == leader && d < 256) sm.cnt[warp][d] = before + __popc(peers);
+    __syncwarp();
+    rk[it] = before + __popc(peers & lt);
+  }
+  __syncthreads();
+  // exclusive prefix over warps per digit
+  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
+    int32_t s = 0;
+    for (int w = 0; w < MS_THREADS / 32; ++w) { int32_t t = sm.cnt[w][d]; sm.cnt[w][d] = s; s += t; }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int it = 0; it < MS_ITEMS; ++it) {
+    int d = dg[it];
+    if (d < 256) {
+      int64_t at = goff[(int64_t)d * ntiles + blockIdx.x] + sm.cnt[warp][d] + rk[it];
+      dst[at] = v[it];
+    }
+  }
+}
+
+// generic exclusive scan (int32 in -> int64 out), 3 phases
+constexpr int SCAN_BLOCK = 1024, SCAN_ITEMS = 4, SCAN_CHUNK = SCAN_BLOCK * SCAN_ITEMS;
+
+__global__ void __launch_bounds__(1024, 1) k_scan_reduce(const int32_t* in, int64_t n, int64_t* sums) {
+  __shared__ int64_t ws[32];
+  int64_t base = (int64_t)blockIdx.x * SCAN_CHUNK;
+  int64_t acc = 0;
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    int64_t i = base + k * SCAN_BLOCK + threadIdx.x;
+    if (i < n) acc += in[i];
+  }
+  int64_t tot;
+  block_excl_scan<int64_t>(acc, ws, &tot);
+  if (threadIdx.x == 0) sums[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(1024, 1) k_scan_sums(int64_t* sums, int64_t nb) { block_scan_array<int64_t>(sums, nb); }
+
+__global__ void __launch_bounds__(1024, 1) k_scan_down(const int32_t* in, int64_t n, const int64_t* sums, int64_t* out) {
+  __shared__ int64_t ws[32];
+  __shared__ int64_t carry;
+  int64_t base = (int64_t)blockIdx.x * SCAN_CHUNK;
+  if (threadIdx.x == 0) carry = sums[blockIdx.x];
+  __syncthreads();
+  for (int k = 0; k < SCAN_ITEMS; ++k) {
+    int64_t i = base + k * SCAN_BLOCK + threadIdx.x;
+    int64_t v = i < n ? in[i] : 0;
+    int64_t tot;
+    int64_t ex = block_excl_scan<int64_t>(v, ws, &tot);
+    if (i < n) out[i] = carry + ex;
+    __syncthreads();
+    if (threadIdx.x == 0) carry += tot;
+    __syncthreads();
+  }
+}
+
+static void scan_i32_to_i64(Ctx& c, const int32_t* in, int64_t n, int64_t* out) {
+  int64_t nb = (n + SCAN_CHUNK - 1) / SCAN_CHUNK;
+  c.s.i64e.resize(std::max<int64_t>(nb, 1), c.st);
+  k_scan_reduce<<<nb, SCAN_BLOCK, 0, c.st>>>(in, n, c.s.i64e.p);
+  k_scan_sums<<<1, SCAN_BLOCK, 0, c.st>>>(c.s.i64e.p, nb);
+  k_scan_down<<<nb, SCAN_BLOCK, 0, c.st>>>(in, n, c.s.i64e.p, out);
+  MSG_CHECK_LAUNCH();
+  add_launches(3);
+}
+
+void scan_flags(Ctx& c, const int32_t* in, int64_t n, int64_t* out) { scan_i32_to_i64(c, in, n, out); }
+
+// Stable multisplit of order[cur][head, head+len) by class digits; result
+// at order[cur^1][0, len) (one buffer swap per pass).  `passes` LSD passes.
+static void multisplit(Ctx& c, const SegTab& T, int passes) {
+  int64_t n = c.len;
+  if (n == 0 || passes <= 0) return;
+  int64_t ntiles = (n + MS_TILE - 1) / MS_TILE;
+  c.s.i32a.resize(256 * ntiles, c.st);
+  c.s.i64a.resize(256 * ntiles, c.st);
+  for (int pass = 0; pass < passes; ++pass) {
+    const int32_t* src = c.order[c.cur].p + c.head;
+    int32_t* dst = c.order[c.cur ^ 1].p;
+    k_ms_count<<<ntiles, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, c.s.i32a.p, ntiles);
+    MSG_CHECK_LAUNCH();
+    scan_i32_to_i64(c, c.s.i32a.p, 256 * ntiles, c.s.i64a.p);
+    k_ms_scatter<<<ntiles, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, c.s.i64a.p, ntiles, dst);
+    MSG_CHECK_LAUNCH();
+    add_launches(2);
+    c.cur ^= 1;
+    c.head = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// apply: evict the list head, install pages at the tail (memman.py:43-56, 93-112)
+
+__global__ void k_evict_head(const int32_t* order, int64_t n, uint32_t* bits, int32_t* frame, int32_t* fifo,
+                             int64_t fifo_tail, int64_t C, int64_t* mig) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t p = order[e];
+    atomicAnd(&bits[p >> 5], ~(1u << (p & 31)));
+    int32_t f = frame[p];
+    frame[p] = -1;
+    fifo[(fifo_tail + e) % C] = f;
+    if (mig) mig[e] = ((int64_t)p << 32) | (uint32_t)f;
+  }
+}
+
+__global__ void k_install(const int32_t* pages, const int64_t* np_dev, int64_t np_host, uint32_t* bits,
+                          int32_t* frame, const int32_t* fifo, int64_t fifo_head, int64_t C, int32_t* order_tail,
+                          int64_t* mig) {
+  int64_t n = np_dev ? *np_dev : np_host;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
+    int32_t p = pages[j];
+    atomicOr(&bits[p >> 5], 1u << (p & 31));
+    int32_t f = fifo[(fifo_head + j) % C];
+    frame[p] = f;
+    order_tail[j] = p;
+    if (mig) mig[j] = ((int64_t)p << 32) | (uint32_t)f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K8 touch scan: missing pages of each command's actual set (engine.py:396-397)
+
+__global__ void k_touch_scan(const Iv* act, const int64_t* act_off, int32_t c_lo, int32_t c_hi,
+                             const uint32_t* bits, int64_t* cnt) {
+  int64_t i0 = act_off[c_lo], i1 = act_off[c_hi];
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = i0 + warp; i < i1; i += nwarps) {
+    const Iv v = act[i];
+    int64_t m = warp_count_nonres(bits, v.d, v.b - v.a);
+    if ((threadIdx.x & 31) == 0 && m) {
+      int32_t lo = c_lo, hi = c_hi;  // command of interval i
+      while (lo < hi) {
+        int32_t mid = (lo + hi) >> 1;
+        if (act_off[mid + 1] <= i) lo = mid + 1; else hi = mid;
+      }
+      atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[lo - c_lo]), (unsigned long long)m);
+    }
+  }
+}
+
+// missing pages of one command in page order (for installs): one warp per interval
+__global__ void k_missing_count(const Iv* act, int64_t i0, int64_t i1, const uint32_t* bits, int64_t* cnt) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = i0 + warp; i < i1; i += nwarps) {
+    const Iv v = act[i];
+    int64_t m = warp_count_nonres(bits, v.d, v.b - v.a);
+    if ((threadIdx.x & 31) == 0) cnt[i - i0] = m;
+  }
+}
+
+__global__ void __launch_bounds__(1024, 1) k_scan_small(int64_t* a, int64_t n, int64_t* total) {
+  int64_t t = block_scan_array<int64_t>(a, n);
+  if (threadIdx.x == 0 && total) *total = t;
+}
+
+__global__ void k_missing_fill(const Iv* act, int64_t i0, int64_t i1, const uint32_t* bits, const int64_t* off,
+                               int32_t* out) {
+  int lane = threadIdx.x & 31;
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = i0 + warp; i < i1; i += nwarps) {
+    const Iv v = act[i];
+    int64_t o = off[i - i0];
+    int64_t lo = v.d, hi = v.d + (v.b - v.a);
+    for (int64_t p0 = lo; p0 < hi; p0 += 32) {
+      int64_t p = p0 + lane;
+      bool want = p < hi && !is_res(bits, p);
+      uint32_t m = __ballot_sync(0xffffffffu, want);
+      if (want) out[o + __popc(m & ((1u << lane) - 1u))] = (int32_t)p;
+      o += __popc(m);
+    }
+  }
+}
+
+// class table from explicit dense ranges (madvise / remove / release)
+__global__ void k_table_from_ranges(const int64_t* lo, const int64_t* len, int64_t n, int64_t* tlo, int64_t* thi,
+                                    int32_t* tcls, int64_t* tn) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    tlo[i] = lo[i];
+    thi[i] = lo[i] + len[i];
+    tcls[i] = 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *tn = n;
+}
+
+// ---------------------------------------------------------------------------
+// host orchestration
+
+static DevState& hs(Ctx& c) { return *c.hstate; }
+
+void pull_state(Ctx& c) {
+  MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+}
+
+static inline int grid_for(int64_t n, int threads, int max_blocks = 148 * 8) {
+  int64_t b = (n + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return (int)b;
+}
+
+// Build the class table for windows `win` into c.s (seg arrays) and return
+// (#segments upper bound, passes).  Also fills per-window page counts and the
+// window-0 run arrays (used by the demand path).
+struct WinBuild {
+  int64_t total_iv = 0;
+  int64_t scratch_total = 0;
+  std::vector<int64_t> win_base;
+};
+
+static void build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild& wb) {
+  std::vector<WinDesc> wd(nwin);
+  int64_t off = 0;
+  for (int w = 0; w < nwin; ++w) {
+    if (win[w].task < 0 || win[w].task >= (int32_t)c.tasks.size() || !c.tasks[win[w].task])
+      throw Error(MSG_E_INVAL, "unknown task in window");
+    TaskTab& t = *c.tasks[win[w].task];
+    if (win[w].c0 < 0 || win[w].c1 < win[w].c0 || win[w].c1 > t.ncmd) throw Error(MSG_E_INVAL, "bad window range");
+    wd[w].pool = t.pred_pool.p;
+    wd[w].pool_lo = t.pred_off[win[w].c0];
+    wd[w].pool_hi = t.pred_off[win[w].c1];
+    wd[w].c0 = win[w].c0; wd[w].c1 = win[w].c1; wd[w].w = w;
+    wd[w].cmd_off = t.d_pred_off.p;
+    wd[w].selfpop = t.d_selfpop.p;
+    wd[w].scratch = off;
+    int64_t n = wd[w].pool_hi - wd[w].pool_lo;
+    wb.total_iv += n;
+    off += 4 * pow2_at_least(2 * std::max<int64_t>(n, 1)) + 16;
+  }
+  wb.scratch_total = off;
+  cudaStream_t st = c.st;
+  // scratch: keys/vals/labels per window + run arrays; combine scratch
+  c.s.i64a.resize(off, st);                 // keys
+  c.s.i64b.resize(off, st);                 // vals
+  c.s.i32a.resize(off, st);                 // labels / run labels
+  c.s.i64c.resize(3 * off + 4 * nwin + 8, st);   // run_a | run_b | run_d | run_base | nruns | pages
+  DVec<WinDesc>& dwd = *reinterpret_cast<DVec<WinDesc>*>(&c.s.iv);  // reuse Iv buffer as raw bytes
+  size_t need_iv = (nwin * sizeof(WinDesc) + sizeof(Iv) - 1) / sizeof(Iv);
+  c.s.iv.resize(need_iv, st);
+  MSG_CUDA(cudaMemcpyAsync(c.s.iv.p, wd.data(), nwin * sizeof(WinDesc), cudaMemcpyHostToDevice, st));
+  (void)dwd;
+  int64_t* rbuf = c.s.i64c.p;
+  WinOut o;
+  o.run_a = rbuf; o.run_b = rbuf + off; o.run_d = rbuf + 2 * off;
+  o.run_base = rbuf + 3 * off; o.nruns = o.run_base + nwin; o.pages = o.nruns + nwin;
+  c.s.i32b.resize(off, st);
+  o.run_lab = c.s.i32b.p;
+  k_window_runs<<<nwin, 1024, 0, st>>>(reinterpret_cast<const WinDesc*>(c.s.iv.p),
+                                       c.s.i64a.p, c.s.i64b.p, c.s.i32a.p, o);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  // combine scratch: key[mp] | val[mp] | E[2mp] | idx[2M] | seg_lo[2M] | seg_hi[2M] | nseg | ncls
+  int64_t M = 2 * wb.total_iv + 2;    // >= total runs
+  int64_t mp = pow2_at_least(2 * M);
+  c.s.i64d.resize(4 * mp + 6 * M + 4, st);
+  c.s.u32a.resize(2 * M * (int64_t)nwin + 16, st);
+  c.s.i32c.resize(2 * M + 16, st);
+  CombineParams P{};
+  P.nwin = nwin;
+  P.run_a = o.run_a; P.run_b = o.run_b; P.run_lab = o.run_lab; P.run_base = o.run_base; P.nruns = o.nruns;
+  P.run_cls = nullptr;
+  P.span_first = c.d_span_first.p; P.span_n = c.d_span_n.p; P.span_dense = c.d_span_dense.p;
+  P.nspans = (int32_t)c.span_first.size();
+  int64_t* d = c.s.i64d.p;
+  P.key = reinterpret_cast<uint64_t*>(d);
+  P.val = d + mp;
+  P.E = d + 2 * mp;
+  P.idx = d + 4 * mp;
+  P.T = reinterpret_cast<int32_t*>(c.s.u32a.p);
+  P.seg_lo = d + 4 * mp + 2 * M;
+  P.seg_hi = P.seg_lo + 2 * M;
+  P.seg_cls = c.s.i32c.p;
+  P.nseg_out = P.seg_hi + 2 * M;
+  P.ncls_out = P.nseg_out + 1;
+  k_window_combine<<<1, 1024, 0, st>>>(P);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+}
+
+// pointers into the build outputs (must mirror build_windows)
+struct WinPtrs {
+  int64_t *run_a, *run_b, *run_base, *nruns, *pages;
+  int32_t* run_lab;
+  SegTab tab;
+  int64_t* ncls;
+};
+
+static WinPtrs win_ptrs(Ctx& c, int32_t nwin, const WinBuild& wb) {
+  WinPtrs p{};
+  int64_t off = wb.scratch_total;
+  int64_t* rbuf = c.s.i64c.p;
+  p.run_a = rbuf; p.run_b = rbuf + off; p.run_base = rbuf + 3 * off; p.nruns = p.run_base + nwin;
+  p.pages = p.nruns + nwin; p.run_lab = c.s.i32b.p;
+  int64_t M = 2 * wb.total_iv + 2;
+  int64_t mp = pow2_at_least(2 * M);
+  int64_t* d = c.s.i64d.p;
+  int64_t* seg_lo = d + 4 * mp + 2 * M;
+  int64_t* seg_hi = seg_lo + 2 * M;
+  p.tab.lo = seg_lo; p.tab.hi = seg_hi; p.tab.cls = c.s.i32c.p;
+  p.tab.n = seg_hi + 2 * M;
+  p.ncls = seg_hi + 2 * M + 1;
+  return p;
+}
+
+static int passes_for(int64_t ncls) {
+  int p = 0;
+  while (ncls > 0) { ++p; ncls >>= 8; }
+  return p;
+}
+
+static void compact_if_needed(Ctx& c) {
+  // invariant for appends without a preceding multisplit: head <= C
+  if (c.head > c.C) {
+    MSG_CUDA(cudaMemcpyAsync(c.order[c.cur ^ 1].p, c.order[c.cur].p + c.head, c.len * sizeof(int32_t),
+                             cudaMemcpyDeviceToDevice, c.st));
+    c.cur ^= 1;
+    c.head = 0;
+  }
+}
+
+static int64_t* mig_buf(Ctx& c, int64_t n) {
+  if (!(c.cfg.flags & MSG_F_MIGRATE) && !(c.cfg.flags & MSG_F_VERIFY_TAGS)) return nullptr;
+  int par = c.mig_par;
+  // the copy work that last used this buffer must be finished
+  MSG_CUDA(cudaStreamWaitEvent(c.st, c.ev_mig[par], 0));
+  c.mig_list[par].resize(std::max<int64_t>(n, 1), c.st);
+  return c.mig_list[par].p;
+}
+
+// evict `n` pages from the head; pushes frames; fills mig[0..n)
+static void evict_head_n(Ctx& c, int64_t n, int64_t* mig) {
+  if (n <= 0) return;
+  k_evict_head<<<grid_for(n, 256), 256, 0, c.st>>>(c.order[c.cur].p + c.head, n, c.bits.p, c.frame.p, c.fifo.p,
+                                                  c.fifo_head + c.fifo_len, c.C, mig);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  c.head += n;
+  c.len -= n;
+  c.fifo_len += n;
+}
+
+// install `n` pages (device list) at the tail
+static void install_pages(Ctx& c, const int32_t* pages, int64_t n, int64_t* mig) {
+  if (n <= 0) return;
+  k_install<<<grid_for(n, 256), 256, 0, c.st>>>(pages, nullptr, n, c.bits.p, c.frame.p, c.fifo.p, c.fifo_head, c.C,
+                                               c.order[c.cur].p + c.head + c.len, mig);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  c.fifo_head = (c.fifo_head + n) % c.C;
+  c.fifo_len -= n;
+  c.len += n;
+}
+
+static void reorder_with_windows(Ctx& c, const msg_window* win, int32_t nwin, int64_t* win_pages) {
+  WinBuild wb;
+  build_windows(c, win, nwin, wb);
+  WinPtrs wp = win_ptrs(c, nwin, wb);
+  int64_t* hb = c.hbuf.p;
+  MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaMemcpyAsync(hb + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  for (int w = 0; w < nwin; ++w) win_pages[w] = hb[w];
+  multisplit(c, wp.tab, passes_for(hb[nwin]));
+}
+
+static int64_t abs_of(const Ctx& c, int64_t d) {
+  auto it = std::upper_bound(c.span_dense.begin(), c.span_dense.end(), d);
+  int64_t s = (it - c.span_dense.begin()) - 1;
+  return c.span_first[s] + (d - c.span_dense[s]);
+}
+
+static void dump_dense(Ctx& c, const int32_t* dev, int64_t n, std::vector<int64_t>& out) {
+  std::vector<int32_t> h(n);
+  if (n) MSG_CUDA(cudaMemcpyAsync(h.data(), dev, n * 4, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  out.resize(n);
+  for (int64_t i = 0; i < n; ++i) out[i] = abs_of(c, h[i]);
+}
+
+void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_t* win, int32_t n, int32_t nwin,
+                  int64_t* win_pages) {
+  if (nwin <= 0) return;
+  // per-window runs in the given (first-access) order; class = K_w - rank
+  std::vector<std::vector<std::pair<int64_t, int64_t>>> per(nwin);
+  for (int i = 0; i < n; ++i) {
+    if (win[i] < 0 || win[i] >= nwin) throw Error(MSG_E_INVAL, "bad window index");
+    if (end[i] > first[i]) per[win[i]].push_back({first[i], end[i]});
+  }
+  std::vector<int64_t> ra, rb, nr(nwin), base(nwin);
+  std::vector<int32_t> rc;
+  for (int w = 0; w < nwin; ++w) {
+    base[w] = (int64_t)ra.size();
+    int64_t K = (int64_t)per[w].size();
+    win_pages[w] = 0;
+    for (int64_t r = 0; r < K; ++r) {
+      int64_t a = per[w][r].first, b = per[w][r].second;
+      win_pages[w] += b - a;
+      // clip to the domain (pages outside it are never resident)
+      while (a < b) {
+        auto it = std::upper_bound(c.span_first.begin(), c.span_first.end(), a);
+        int64_t s = (it - c.span_first.begin()) - 1;
+        if (s < 0 || a >= c.span_first[s] + c.span_n[s]) {
+          if ((size_t)(s + 1) >= c.span_first.size() || c.span_first[s + 1] >= b) break;
+          a = c.span_first[s + 1];
+          continue;
+        }
+        int64_t e = std::min(b, c.span_first[s] + c.span_n[s]);
+        ra.push_back(a); rb.push_back(e); rc.push_back((int32_t)(K - r));
+        a = e;
+      }
+    }
+    nr[w] = (int64_t)ra.size() - base[w];
+  }
+  int64_t M = std::max<int64_t>((int64_t)ra.size(), 1);
+  cudaStream_t st = c.st;
+  c.s.i64c.resize(3 * M + 2 * nwin + 8, st);
+  c.s.i32b.resize(M, st);
+  int64_t* rbuf = c.s.i64c.p;
+  if (!ra.empty()) {
+    MSG_CUDA(cudaMemcpyAsync(rbuf, ra.data(), ra.size() * 8, cudaMemcpyHostToDevice, st));
+    MSG_CUDA(cudaMemcpyAsync(rbuf + M, rb.data(), rb.size() * 8, cudaMemcpyHostToDevice, st));
+    MSG_CUDA(cudaMemcpyAsync(c.s.i32b.p, rc.data(), rc.size() * 4, cudaMemcpyHostToDevice, st));
+  }
+  MSG_CUDA(cudaMemcpyAsync(rbuf + 3 * M, base.data(), nwin * 8, cudaMemcpyHostToDevice, st));
+  MSG_CUDA(cudaMemcpyAsync(rbuf + 3 * M + nwin, nr.data(), nwin * 8, cudaMemcpyHostToDevice, st));
+  int64_t Mb = (int64_t)ra.size() + 2;
+  int64_t mp = pow2_at_least(2 * Mb);
+  c.s.i64d.resize(4 * mp + 6 * Mb + 4, st);
+  c.s.u32a.resize(2 * Mb * (int64_t)nwin + 16, st);
+  c.s.i32c.resize(2 * Mb + 16, st);
+  CombineParams P{};
+  P.nwin = nwin;
+  P.run_a = rbuf; P.run_b = rbuf + M; P.run_lab = nullptr; P.run_base = rbuf + 3 * M; P.nruns = rbuf + 3 * M + nwin;
+  P.run_cls = c.s.i32b.p;
+  P.span_first = c.d_span_first.p; P.span_n = c.d_span_n.p; P.span_dense = c.d_span_dense.p;
+  P.nspans = (int32_t)c.span_first.size();
+  int64_t* d = c.s.i64d.p;
+  P.key = reinterpret_cast<uint64_t*>(d);
+  P.val = d + mp;
+  P.E = d + 2 * mp;
+  P.idx = d + 4 * mp;
+  P.T = reinterpret_cast<int32_t*>(c.s.u32a.p);
+  P.seg_lo = d + 4 * mp + 2 * Mb;
+  P.seg_hi = P.seg_lo + 2 * Mb;
+  P.seg_cls = c.s.i32c.p;
+  P.nseg_out = P.seg_hi + 2 * Mb;
+  P.ncls_out = P.nseg_out + 1;
+  k_window_combine<<<1, 1024, 0, st>>>(P);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, P.ncls_out, 8, cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaStreamSynchronize(st));
+  SegTab T{P.seg_lo, P.seg_hi, P.seg_cls, P.nseg_out};
+  multisplit(c, T, passes_for(c.hbuf.p[0]));
+  MSG_CUDA(cudaStreamSynchronize(st));
+}
+
+void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_always, msg_switch_out* out,
+                 int64_t* win_pages, int64_t* prefix, int64_t* touch_cnt) {
+  if (nwin < 1) throw Error(MSG_E_INVAL, "need at least one window");
+  cudaStream_t st = c.st;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  MSG_CUDA(cudaEventCreate(&e0)); MSG_CUDA(cudaEventCreate(&e1));
+  MSG_CUDA(cudaEventRecord(e0, st));
+  TaskTab& t0 = *c.tasks[win[0].task];
+  int32_t c0 = win[0].c0, c1 = win[0].c1, ncw = c1 - c0;
+  c.hbuf.reserve(4 * (int64_t)nwin + 2 * (int64_t)ncw + 64);
+  // ---- phase A: windows, class table, window-0 demand vs residency
+  WinBuild wb;
+  build_windows(c, win, nwin, wb);
+  WinPtrs wp = win_ptrs(c, nwin, wb);
+  int64_t nrun_cap = std::max<int64_t>(2 * (t0.pred_off[c1] - t0.pred_off[c0]) + 2, 2);
+  c.s.i64e.resize(std::max<int64_t>(5 * nrun_cap + ncw + 4, 64), st);
+  DemandParams D{};
+  D.run_a = wp.run_a; D.run_b = wp.run_b; D.run_lab = wp.run_lab; D.run_base = wb.win_base.empty() ? 0 : 0;
+  D.run_base = 0;  // window 0 scratch starts at 0
+  D.nruns = wp.nruns;
+  D.selfpop = t0.d_selfpop.p; D.c0 = c0;
+  D.span_first = c.d_span_first.p; D.span_n = c.d_span_n.p; D.span_dense = c.d_span_dense.p;
+  D.nspans = (int32_t)c.span_first.size();
+  D.bits = c.bits.p;
+  // demand arrays live in a dedicated buffer (i64e is used by scans: use a local DVec)
+  DVec<int64_t>& dem = c.s.dem;
+  dem.resize(4 * nrun_cap + ncw + 8, st);
+  D.dlo = dem.p; D.dlen = dem.p + nrun_cap; D.dmiss = dem.p + 2 * nrun_cap; D.dlab = dem.p + 3 * nrun_cap;
+  D.prefix = dem.p + 4 * nrun_cap;
+  D.ndemand = D.prefix + ncw;
+  MSG_CUDA(cudaMemsetAsync(D.prefix, 0, ncw * sizeof(int64_t), st));
+  k_demand_collect<<<1, 1024, 0, st>>>(D);
+  k_demand_count<<<grid_for(nrun_cap * 32, 256), 256, 0, st>>>(D);
+  k_demand_scan<<<1, 1024, 0, st>>>(D, c.dstate, c.C, c.len);
+  MSG_CHECK_LAUNCH();
+  add_launches(3);
+  int64_t* hb = c.hbuf.p;
+  MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaMemcpyAsync(hb + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaMemcpyAsync(hb + nwin + 1, D.prefix, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaStreamSynchronize(st));
+  DevState S = hs(c);
+  for (int w = 0; w < nwin; ++w) win_pages[w] = hb[w];
+  for (int k = 0; k < ncw; ++k) prefix[k] = hb[nwin + 1 + k];
+  int64_t ncls = hb[nwin];
+  out->missing = S.missing;
+  out->nwin = nwin;
+  out->early_exit = S.missing == 0 && !reorder_always;
+  out->free_before = c.C - c.len;
+  out->populate = out->evict = out->truncated = 0;
+  // ---- phase B
+  int64_t* mig = nullptr;
+  if (!out->early_exit) {
+    multisplit(c, wp.tab, passes_for(ncls));
+    if (c.debug) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
+    out->free_before = c.C - c.len;
+    int64_t pop = S.populate, ev = S.evict;
+    out->populate = pop; out->evict = ev; out->truncated = S.truncated;
+    if (pop > c.C - c.len + ev) throw Error(MSG_E_CAPACITY, "migration plan overflowed HBM capacity");
+    // populate list computed against pre-apply residency
+    c.s.i32c.resize(std::max<int64_t>(pop, 1) + c.s.i32c.n, st);
+    DVec<int32_t>& poplist = c.s.poplist;
+    poplist.resize(std::max<int64_t>(pop, 1), st);
+    if (pop) {
+      k_demand_fill<<<grid_for(nrun_cap * 32, 256), 256, 0, st>>>(D, c.dstate, poplist.p);
+      MSG_CHECK_LAUNCH();
+      add_launches(1);
+    }
+    mig = mig_buf(c, ev + pop);
+    if (c.debug) {
+      dump_dense(c, c.order[c.cur].p + c.head, ev, c.dbg[1]);
+      dump_dense(c, poplist.p, pop, c.dbg[2]);
+    }
+    evict_head_n(c, ev, mig);
+    compact_if_needed(c);
+    install_pages(c, poplist.p, pop, mig ? mig + ev : nullptr);
+    if (mig) migrate_batch(c, ev, pop, out->free_before, true);
+  }
+  // ---- K8 touch scan of the slice (post-apply residency)
+  DVec<int64_t>& tc = c.s.tc;
+  tc.resize(std::max(ncw, 1), st);
+  MSG_CUDA(cudaMemsetAsync(tc.p, 0, std::max(ncw, 1) * sizeof(int64_t), st));
+  if (ncw) {
+    int64_t niv = t0.act_off[c1] - t0.act_off[c0];
+    k_touch_scan<<<grid_for(std::max<int64_t>(niv, 1) * 32, 256), 256, 0, st>>>(t0.act_pool.p, t0.d_act_off.p, c0, c1,
+                                                                                c.bits.p, tc.p);
+    MSG_CHECK_LAUNCH();
+    add_launches(1);
+    MSG_CUDA(cudaMemcpyAsync(hb, tc.p, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  }
+  MSG_CUDA(cudaEventRecord(e1, st));
+  MSG_CUDA(cudaStreamSynchronize(st));
+  out->first_missing = -1;
+  out->first_missing_pages = 0;
+  for (int k = 0; k < ncw; ++k) {
+    touch_cnt[k] = hb[k];
+    if (hb[k] && out->first_missing < 0) { out->first_missing = c0 + k; out->first_missing_pages = hb[k]; }
+  }
+  out->resident_after = c.len;
+  float ms = 0;
+  cudaEventElapsedTime(&ms, e0, e1);
+  c.stats.plan_ms += ms;
+  cudaEventDestroy(e0); cudaEventDestroy(e1);
+}
+
+void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_window* win, int32_t nwin,
+                int32_t scan_end, bool write_tags, msg_touch_out* out, int64_t* win_pages) {
+  if (task < 0 || task >= (int32_t)c.tasks.size() || !c.tasks[task]) throw Error(MSG_E_INVAL, "unknown task");
+  TaskTab& t = *c.tasks[task];
+  if (cmd < 0 || cmd >= t.ncmd || scan_end > t.ncmd) throw Error(MSG_E_INVAL, "bad command index");
+  cudaStream_t st = c.st;
+  c.hbuf.reserve(4 * (int64_t)nwin + (scan_end - cmd) + 64);
+  // missing list of cmd against current residency (before any eviction)
+  int64_t i0 = t.act_off[cmd], i1 = t.act_off[cmd + 1], niv = i1 - i0;
+  DVec<int64_t>& cnt = c.s.cnt;
+  DVec<int32_t>& miss = c.s.miss;
+  cnt.resize(niv + 2, st);
+  int64_t n = 0;
+  if (niv) {
+    k_missing_count<<<grid_for(niv * 32, 256), 256, 0, st>>>(t.act_pool.p, i0, i1, c.bits.p, cnt.p);
+    k_scan_small<<<1, 1024, 0, st>>>(cnt.p, niv, cnt.p + niv);
+    MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, cnt.p + niv, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    MSG_CUDA(cudaStreamSynchronize(st));
+    n = c.hbuf.p[0];
+    miss.resize(std::max<int64_t>(n, 1), st);
+    k_missing_fill<<<grid_for(niv * 32, 256), 256, 0, st>>>(t.act_pool.p, i0, i1, c.bits.p, cnt.p, miss.p);
+    MSG_CHECK_LAUNCH();
+    add_launches(3);
+  }
+  out->missing = n;
+  out->refreshed = 0;
+  out->evicted = 0;
+  int64_t* mig = mig_buf(c, std::max<int64_t>(evict, 0) + n);
+  int64_t ev_done = 0;
+  if (evict > 0) {
+    if (nwin > 0) {
+      reorder_with_windows(c, win, nwin, win_pages);
+      out->refreshed = 1;
+      if (c.debug) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
+    }
+    ev_done = std::min(evict, c.len);
+    if (c.debug) dump_dense(c, c.order[c.cur].p + c.head, ev_done, c.dbg[1]);
+    int64_t free_before = c.C - c.len;
+    (void)free_before;
+    evict_head_n(c, ev_done, mig);
+    out->evicted = ev_done;
+  }
+  if (c.debug) {
+    if (evict <= 0) c.dbg[1].clear();
+    dump_dense(c, miss.p, n, c.dbg[2]);
+  }
+  compact_if_needed(c);
+  int64_t free_before = c.C - c.len;
+  install_pages(c, miss.p, n, mig ? mig + ev_done : nullptr);
+  if (mig) migrate_batch(c, ev_done, n, free_before, !write_tags);
+  out->resident_after = c.len;
+  // rescan (cmd, scan_end)
+  out->next_missing = -1;
+  out->next_missing_pages = 0;
+  int32_t lo = cmd + 1, hi = scan_end;
+  if (hi > lo) {
+    DVec<int64_t>& tc = c.s.tc;
+    tc.resize(hi - lo, st);
+    MSG_CUDA(cudaMemsetAsync(tc.p, 0, (hi - lo) * sizeof(int64_t), st));
+    int64_t nv = t.act_off[hi] - t.act_off[lo];
+    k_touch_scan<<<grid_for(std::max<int64_t>(nv, 1) * 32, 256), 256, 0, st>>>(t.act_pool.p, t.d_act_off.p, lo, hi,
+                                                                               c.bits.p, tc.p);
+    MSG_CHECK_LAUNCH();
+    add_launches(1);
+    MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, tc.p, (hi - lo) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    MSG_CUDA(cudaStreamSynchronize(st));
+    for (int k = 0; k < hi - lo; ++k)
+      if (c.hbuf.p[k]) { out->next_missing = lo + k; out->next_missing_pages = c.hbuf.p[k]; break; }
+  } else {
+    MSG_CUDA(cudaStreamSynchronize(st));
+  }
+}
+
+// madvise / remove with an explicit dense range table (class 1 = member)
+static void split_by_ranges(Ctx& c, const std::vector<int64_t>& lo, const std::vector<int64_t>& len) {
+  int64_t n = (int64_t)lo.size();
+  DVec<int64_t>& tb = c.s.tb;
+  DVec<int32_t>& tcls = c.s.tcls;
+  tb.resize(4 * n + 4, c.st);
+  tcls.resize(n + 1, c.st);
+  if (n) {
+    MSG_CUDA(cudaMemcpyAsync(tb.p, lo.data(), n * 8, cudaMemcpyHostToDevice, c.st));
+    MSG_CUDA(cudaMemcpyAsync(tb.p + n, len.data(), n * 8, cudaMemcpyHostToDevice, c.st));
+  }
+  k_table_from_ranges<<<grid_for(n, 256), 256, 0, c.st>>>(tb.p, tb.p + n, n, tb.p + 2 * n, tb.p + 3 * n, tcls.p,
+                                                         tb.p + 4 * n);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  SegTab T{tb.p + 2 * n, tb.p + 3 * n, tcls.p, tb.p + 4 * n};
+  multisplit(c, T, 1);
+}
+
+// sort + merge absolute runs, convert to dense ranges (host side, small inputs)
+static void dense_ranges(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, std::vector<int64_t>& lo,
+                         std::vector<int64_t>& len, bool strict) {
+  std::vector<std::pair<int64_t, int64_t>> r;
+  for (int i = 0; i < n; ++i)
+    if (end[i] > first[i]) r.push_back({first[i], end[i]});
+  std::sort(r.begin(), r.end());
+  std::vector<std::pair<int64_t, int64_t>> m;
+  for (auto& x : r) {
+    if (!m.empty() && x.first <= m.back().second) m.back().second = std::max(m.back().second, x.second);
+    else m.push_back(x);
+  }
+  // clip to spans (pages outside the domain can never be resident)
+  for (auto& x : m) {
+    int64_t a = x.first;
+    while (a < x.second) {
+      auto it = std::upper_bound(c.span_first.begin(), c.span_first.end(), a);
+      int64_t s = (it - c.span_first.begin()) - 1;
+      if (s < 0 || a >= c.span_first[s] + c.span_n[s]) {
+        if (strict) throw Error(MSG_E_DOMAIN, "page outside the dense page map");
+        // skip to next span start
+        if ((size_t)(s + 1) >= c.span_first.size()) break;
+        a = std::max(a + 1, c.span_first[s + 1]);
+        continue;
+      }
+      int64_t b = std::min(x.second, c.span_first[s] + c.span_n[s]);
+      lo.push_back(c.span_dense[s] + (a - c.span_first[s]));
+      len.push_back(b - a);
+      a = b;
+    }
+  }
+}
+
+__global__ void k_release_pages(const int32_t* pages, int64_t n, uint32_t* bits, int32_t* frame, int32_t* fifo,
+                                int64_t fifo_tail, int64_t C) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    int32_t p = pages[e];
+    atomicAnd(&bits[p >> 5], ~(1u << (p & 31)));
+    fifo[(fifo_tail + e) % C] = frame[p];
+    frame[p] = -1;
+  }
+}
+
+__global__ void k_count_resident(const int64_t* lo, const int64_t* len, int64_t n, const uint32_t* bits,
+                                 unsigned long long* out) {
+  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t r = warp; r < n; r += nwarps) {
+    int64_t m = len[r] - warp_count_nonres(bits, lo[r], len[r]);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)m);
+  }
+}
+
+static int64_t count_resident(Ctx& c, const std::vector<int64_t>& lo, const std::vector<int64_t>& len) {
+  int64_t n = (int64_t)lo.size();
+  if (!n) return 0;
+  DVec<int64_t>& b = c.s.rb;
+  b.resize(2 * n + 1, c.st);
+  MSG_CUDA(cudaMemcpyAsync(b.p, lo.data(), n * 8, cudaMemcpyHostToDevice, c.st));
+  MSG_CUDA(cudaMemcpyAsync(b.p + n, len.data(), n * 8, cudaMemcpyHostToDevice, c.st));
+  MSG_CUDA(cudaMemsetAsync(b.p + 2 * n, 0, 8, c.st));
+  k_count_resident<<<grid_for(n * 32, 256), 256, 0, c.st>>>(b.p, b.p + n, n, c.bits.p,
+                                                           reinterpret_cast<unsigned long long*>(b.p + 2 * n));
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, b.p + 2 * n, 8, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  return c.hbuf.p[0];
+}
+
+void release_pages(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int64_t* removed) {
+  c.hbuf.reserve(64);
+  std::vector<int64_t> lo, len;
+  dense_ranges(c, first, end, n, lo, len, false);
+  int64_t k = count_resident(c, lo, len);
+  *removed = k;
+  if (k == 0 || c.len == 0) return;
+  split_by_ranges(c, lo, len);   // members (class 1) now at the tail
+  int64_t keep = c.len - k;
+  const int32_t* gone = c.order[c.cur].p + c.head + keep;
+  k_release_pages<<<grid_for(k, 256), 256, 0, c.st>>>(gone, k, c.bits.p, c.frame.p, c.fifo.p,
+                                                      c.fifo_head + c.fifo_len, c.C);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  c.fifo_len += k;
+  c.len = keep;
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+}
+
+// ---- eviction-list facade ----------------------------------------------
+
+void list_append_abs(Ctx& c, const int64_t* first, const int64_t* end, int32_t n) {
+  // pages in the given run order; already-resident pages are skipped
+  std::vector<int32_t> pages;
+  for (int i = 0; i < n; ++i) {
+    for (int64_t p = first[i]; p < end[i]; ++p) {
+      int64_t d = dense_of_host(c, p);
+      if (d < 0) throw Error(MSG_E_DOMAIN, "page outside the dense page map");
+      pages.push_back((int32_t)d);
+    }
+  }
+  if (pages.empty()) return;
+  // filter resident on host via a bitmap snapshot (facade path, small)
+  std::vector<uint32_t> words((c.D + 31) / 32);
+  MSG_CUDA(cudaMemcpyAsync(words.data(), c.bits.p, words.size() * 4, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  std::vector<int32_t> fresh;
+  for (int32_t p : pages) {
+    uint32_t& w = words[p >> 5];
+    if (!((w >> (p & 31)) & 1u)) { fresh.push_back(p); w |= 1u << (p & 31); }
+  }
+  if ((int64_t)fresh.size() + c.len > c.C) throw Error(MSG_E_CAPACITY, "eviction list exceeds HBM capacity");
+  DVec<int32_t>& d = c.s.miss;
+  d.resize(std::max<size_t>(fresh.size(), 1), c.st);
+  MSG_CUDA(cudaMemcpyAsync(d.p, fresh.data(), fresh.size() * 4, cudaMemcpyHostToDevice, c.st));
+  compact_if_needed(c);
+  int64_t* mig = mig_buf(c, fresh.size());
+  int64_t fb = c.C - c.len;
+  install_pages(c, d.p, (int64_t)fresh.size(), mig);
+  if (mig) migrate_batch(c, 0, (int64_t)fresh.size(), fb, true);
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+}
+
+void list_madvise_abs(Ctx& c, const int64_t* first, const int64_t* end, int32_t n) {
+  std::vector<int64_t> lo, len;
+  dense_ranges(c, first, end, n, lo, len, false);
+  if (lo.empty() || c.len == 0) return;
+  split_by_ranges(c, lo, len);
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+}
+
+void list_evict_head(Ctx& c, int64_t n, int64_t* pages_out, int64_t* nout) {
+  n = std::min(std::max<int64_t>(n, 0), c.len);
+  *nout = n;
+  if (!n) return;
+  std::vector<int32_t> h(n);
+  MSG_CUDA(cudaMemcpyAsync(h.data(), c.order[c.cur].p + c.head, n * 4, cudaMemcpyDeviceToHost, c.st));
+  int64_t* mig = mig_buf(c, n);
+  int64_t fb = c.C - c.len;
+  evict_head_n(c, n, mig);
+  if (mig) migrate_batch(c, n, 0, fb, true);
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  for (int64_t i = 0; i < n; ++i) {
+    int64_t d = h[i];
+    auto it = std::upper_bound(c.span_dense.begin(), c.span_dense.end(), d);
+    int64_t s = (it - c.span_dense.begin()) - 1;
+    pages_out[i] = c.span_first[s] + (d - c.span_dense[s]);
+  }
+}
+
+void list_read(Ctx& c, int64_t* pages_out, int64_t cap, int64_t* n) {
+  *n = c.len;
+  if (!pages_out) return;
+  int64_t k = std::min(cap, c.len);
+  std::vector<int32_t> h(k);
+  if (k) MSG_CUDA(cudaMemcpyAsync(h.data(), c.order[c.cur].p + c.head, k * 4, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  for (int64_t i = 0; i < k; ++i) {
+    int64_t d = h[i];
+    auto it = std::upper_bound(c.span_dense.begin(), c.span_dense.end(), d);
+    int64_t s = (it - c.span_dense.begin()) - 1;
+    pages_out[i] = c.span_first[s] + (d - c.span_dense[s]);
+  }
+}
+
+// ---- demand paging (Mode.um): per command, sequential on the device -------
+
+void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out, int64_t* evicted_out) {
+  TaskTab& t = *c.tasks[task];
+  c.dbg[3].clear();
+  for (int32_t cmd = c0; cmd < c1; ++cmd) {
+    // missing count
+    msg_touch_out o{};
+    int64_t i0 = t.act_off[cmd], i1 = t.act_off[cmd + 1];
+    std::vector<int64_t> lo, len;
+    DVec<int64_t>& cnt = c.s.cnt;
+    int64_t niv = i1 - i0;
+    int64_t n = 0;
+    cnt.resize(niv + 2, c.st);
+    if (niv) {
+      k_missing_count<<<grid_for(niv * 32, 256), 256, 0, c.st>>>(t.act_pool.p, i0, i1, c.bits.p, cnt.p);
+      k_scan_small<<<1, 1024, 0, c.st>>>(cnt.p, niv, cnt.p + niv);
+      add_launches(2);
+      MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, cnt.p + niv, 8, cudaMemcpyDeviceToHost, c.st));
+      MSG_CUDA(cudaStreamSynchronize(c.st));
+      n = c.hbuf.p[0];
+    }
+    missing_out[cmd - c0] = n;
+    evicted_out[cmd - c0] = 0;
+    if (n > c.C) {
+      throw Error(MSG_E_CAPACITY, "command working set (" + std::to_string(n) + " pages) exceeds HBM capacity (" +
+                                      std::to_string(c.C) + " pages)");
+    }
+    if (n) {
+      int64_t over = c.len + n - c.C;
+      touch_slow(c, task, cmd, over > 0 ? over : 0, nullptr, 0, cmd + 1, t.kind[cmd] == MSG_CMD_H2D, &o, nullptr);
+      evicted_out[cmd - c0] = o.evicted;
+      if (c.debug) {  // [cmd, nmiss, miss..., nev, ev...] per faulting command
+        auto& u = c.dbg[3];
+        u.push_back(cmd);
+        u.push_back((int64_t)c.dbg[2].size());
+        u.insert(u.end(), c.dbg[2].begin(), c.dbg[2].end());
+        u.push_back((int64_t)c.dbg[1].size());
+        u.insert(u.end(), c.dbg[1].begin(), c.dbg[1].end());
+      }
+    }
+    // LRU refresh: madvise(actual) (engine.py:398-401, 425-426)
+    std::vector<Iv> hiv(niv);
+    if (niv) {
+      MSG_CUDA(cudaMemcpyAsync(hiv.data(), t.act_pool.p + i0, niv * sizeof(Iv), cudaMemcpyDeviceToHost, c.st));
+      MSG_CUDA(cudaStreamSynchronize(c.st));
+      for (auto& v : hiv) { lo.push_back(v.d); len.push_back(v.b - v.a); }
+      if (c.len) split_by_ranges(c, lo, len);
+    }
+  }
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+}
+
+}  // namespace msg
+
+namespace msg {
+
+// ---- facade helpers: compute_window / plan_migration on explicit runs ----
+
+void window_runs_explicit(Ctx& c, const int64_t* first, const int64_t* end, const int32_t* cmd, int32_t niv,
+                          int32_t ncmd, int64_t* runs_out, int64_t* nruns, int64_t* pages) {
+  cudaStream_t st = c.st;
+  std::vector<Iv> iv(std::max(niv, 1));
+  std::vector<int64_t> off(ncmd + 1, 0);
+  for (int i = 0; i < niv; ++i) {
+    if (cmd[i] < 0 || cmd[i] >= ncmd || (i && cmd[i] < cmd[i - 1])) throw Error(MSG_E_INVAL, "bad run command index");
+    iv[i] = Iv{first[i], end[i], 0};
+    off[cmd[i] + 1]++;
+  }
+  for (int k = 0; k < ncmd; ++k) off[k + 1] += off[k];
+  DVec<Iv> d_iv; d_iv.exact(iv.size());
+  DVec<int64_t> d_off; d_off.exact(ncmd + 1);
+  DVec<uint8_t> d_sp; d_sp.exact(std::max(ncmd, 1));
+  MSG_CUDA(cudaMemcpyAsync(d_iv.p, iv.data(), iv.size() * sizeof(Iv), cudaMemcpyHostToDevice, st));
+  MSG_CUDA(cudaMemcpyAsync(d_off.p, off.data(), off.size() * 8, cudaMemcpyHostToDevice, st));
+  MSG_CUDA(cudaMemsetAsync(d_sp.p, 0, std::max(ncmd, 1), st));
+  WinDesc wd{};
+  wd.pool = d_iv.p;
+  wd.pool_lo = 0; wd.pool_hi = niv; wd.c0 = 0; wd.c1 = ncmd; wd.w = 0;
+  wd.cmd_off = d_off.p; wd.selfpop = d_sp.p; wd.scratch = 0;
+  int64_t scratch = 4 * pow2_at_least(2 * std::max<int64_t>(niv, 1)) + 16;
+  DVec<WinDesc> d_wd; d_wd.exact(1);
+  MSG_CUDA(cudaMemcpyAsync(d_wd.p, &wd, sizeof(wd), cudaMemcpyHostToDevice, st));
+  DVec<int64_t> ka, va, rb; ka.exact(scratch); va.exact(scratch); rb.exact(3 * scratch + 8);
+  DVec<int32_t> lab, rl; lab.exact(scratch); rl.exact(scratch);
+  WinOut o;
+  o.run_a = rb.p; o.run_b = rb.p + scratch; o.run_d = rb.p + 2 * scratch;
+  o.run_base = rb.p + 3 * scratch; o.nruns = o.run_base + 1; o.pages = o.nruns + 1;
+  o.run_lab = rl.p;
+  k_window_runs<<<1, 1024, 0, st>>>(d_wd.p, ka.p, va.p, lab.p, o);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  int64_t hb[3];
+  MSG_CUDA(cudaMemcpyAsync(hb, o.run_base, 3 * 8, cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaStreamSynchronize(st));
+  int64_t nr = hb[1];
+  *nruns = nr;
+  *pages = hb[2];
+  if (runs_out && nr) {
+    std::vector<int64_t> a(nr), b(nr);
+    std::vector<int32_t> l(nr);
+    MSG_CUDA(cudaMemcpyAsync(a.data(), o.run_a, nr * 8, cudaMemcpyDeviceToHost, st));
+    MSG_CUDA(cudaMemcpyAsync(b.data(), o.run_b, nr * 8, cudaMemcpyDeviceToHost, st));
+    MSG_CUDA(cudaMemcpyAsync(l.data(), o.run_lab, nr * 4, cudaMemcpyDeviceToHost, st));
+    MSG_CUDA(cudaStreamSynchronize(st));
+    for (int64_t i = 0; i < nr; ++i) { runs_out[3 * i] = a[i]; runs_out[3 * i + 1] = b[i]; runs_out[3 * i + 2] = l[i]; }
+  }
+}
+
+void list_plan(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int64_t capacity, int64_t* pop_out,
+               int64_t* npop, int64_t* ev_out, int64_t* nev, int64_t* truncated) {
+  cudaStream_t st = c.st;
+  std::vector<int64_t> a, b;
+  for (int i = 0; i < n; ++i) {
+    if (end[i] <= first[i]) continue;
+    int64_t d0 = dense_of_host(c, first[i]), d1 = dense_of_host(c, end[i] - 1);
+    if (d0 < 0 || d1 < 0 || d1 - d0 != end[i] - 1 - first[i]) throw Error(MSG_E_DOMAIN, "run outside the page map");
+    a.push_back(first[i]); b.push_back(end[i]);
+  }
+  int64_t m = (int64_t)a.size();
+  int64_t cap = std::max<int64_t>(m, 1);
+  DVec<int64_t> buf; buf.exact(8 * cap + 8);
+  DVec<int32_t> lab; lab.exact(cap);
+  DVec<uint8_t> sp; sp.exact(cap);
+  std::vector<int32_t> hl(cap);
+  for (int64_t i = 0; i < cap; ++i) hl[i] = (int32_t)i;
+  if (m) {
+    MSG_CUDA(cudaMemcpyAsync(buf.p, a.data(), m * 8, cudaMemcpyHostToDevice, st));
+    MSG_CUDA(cudaMemcpyAsync(buf.p + cap, b.data(), m * 8, cudaMemcpyHostToDevice, st));
+  }
+  MSG_CUDA(cudaMemcpyAsync(lab.p, hl.data(), cap * 4, cudaMemcpyHostToDevice, st));
+  MSG_CUDA(cudaMemsetAsync(sp.p, 0, cap, st));
+  MSG_CUDA(cudaMemcpyAsync(buf.p + 8 * cap, &m, 8, cudaMemcpyHostToDevice, st));
+  DemandParams D{};
+  D.run_a = buf.p; D.run_b = buf.p + cap; D.run_lab = lab.p; D.run_base = 0; D.nruns = buf.p + 8 * cap;
+  D.selfpop = sp.p; D.c0 = 0;
+  D.span_first = c.d_span_first.p; D.span_n = c.d_span_n.p; D.span_dense = c.d_span_dense.p;
+  D.nspans = (int32_t)c.span_first.size();
+  D.bits = c.bits.p;
+  D.dlo = buf.p + 2 * cap; D.dlen = buf.p + 3 * cap; D.dmiss = buf.p + 4 * cap; D.dlab = buf.p + 5 * cap;
+  D.prefix = buf.p + 6 * cap; D.ndemand = buf.p + 7 * cap;
+  MSG_CUDA(cudaMemsetAsync(D.prefix, 0, cap * 8, st));
+  k_demand_collect<<<1, 1024, 0, st>>>(D);
+  k_demand_count<<<grid_for(cap * 32, 256), 256, 0, st>>>(D);
+  k_demand_scan<<<1, 1024, 0, st>>>(D, c.dstate, capacity, c.len);
+  MSG_CHECK_LAUNCH();
+  add_launches(3);
+  MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaStreamSynchronize(st));
+  DevState S = *c.hstate;
+  *npop = S.populate;
+  *truncated = S.truncated;
+  int64_t ev = std::min<int64_t>(S.evict, c.len);
+  *nev = ev;
+  DVec<int32_t> pl; pl.exact(std::max<int64_t>(S.populate, 1));
+  if (S.populate) {
+    k_demand_fill<<<grid_for(cap * 32, 256), 256, 0, st>>>(D, c.dstate, pl.p);
+    MSG_CHECK_LAUNCH();
+    add_launches(1);
+  }
+  std::vector<int64_t> tmp;
+  dump_dense(c, pl.p, S.populate, tmp);
+  if (pop_out) std::copy(tmp.begin(), tmp.end(), pop_out);
+  dump_dense(c, c.order[c.cur].p + c.head, ev, tmp);
+  if (ev_out) std::copy(tmp.begin(), tmp.end(), ev_out);
+}
+
+}  // namespace msg

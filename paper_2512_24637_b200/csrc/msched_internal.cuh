@@ -1,0 +1,223 @@
+// Internal declarations shared by the msched_b200 translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <vector>
+#include <stdexcept>
+
+#include "../../include/msched_b200.h"
+
+namespace msg {
+
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define MSG_CUDA(x)                                                                          \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      throw ::msg::Error(MSG_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_) + " (" + \
+                                         __FILE__ + ":" + std::to_string(__LINE__) + ")");   \
+  } while (0)
+
+#define MSG_CHECK_LAUNCH() MSG_CUDA(cudaGetLastError())
+
+constexpr int32_t kNone = 0x7fffffff;
+
+// Page interval in absolute page ids [a, b) plus its dense start d.
+struct Iv {
+  int64_t a, b, d;
+};
+
+// Owning device buffer with geometric growth.
+template <class T>
+struct DVec {
+  T* p = nullptr;
+  size_t n = 0, cap = 0;
+  DVec() = default;
+  DVec(const DVec&) = delete;
+  DVec& operator=(const DVec&) = delete;
+  ~DVec() { if (p) cudaFree(p); }
+  void reserve(size_t want, cudaStream_t s) {
+    if (want <= cap) return;
+    size_t nc = cap ? cap : 256;
+    while (nc < want) nc *= 2;
+    T* q = nullptr;
+    if (cudaMalloc(&q, nc * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(MSG_E_OOM, "device allocation of " + std::to_string(nc * sizeof(T)) + " bytes failed");
+    }
+    if (n) MSG_CUDA(cudaMemcpyAsync(q, p, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
+    if (p) { MSG_CUDA(cudaStreamSynchronize(s)); cudaFree(p); }
+    p = q;
+    cap = nc;
+  }
+  void resize(size_t want, cudaStream_t s) { reserve(want, s); n = want; }
+  void exact(size_t want) {  // allocate exactly, discarding contents
+    if (p) cudaFree(p);
+    p = nullptr; n = cap = 0;
+    if (want == 0) return;
+    if (cudaMalloc(&p, want * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(MSG_E_OOM, "device allocation of " + std::to_string(want * sizeof(T)) + " bytes failed");
+    }
+    n = cap = want;
+  }
+};
+
+// Pinned host buffer.
+template <class T>
+struct HVec {
+  T* p = nullptr;
+  size_t cap = 0;
+  ~HVec() { if (p) cudaFreeHost(p); }
+  void reserve(size_t want) {
+    if (want <= cap) return;
+    size_t nc = cap ? cap : 256;
+    while (nc < want) nc *= 2;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    if (cudaMallocHost(&p, nc * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      throw Error(MSG_E_OOM, "pinned allocation failed");
+    }
+    cap = nc;
+  }
+};
+
+struct Rule {
+  int32_t kind, ptr;
+  int64_t off;
+  msg_expr e[3];
+};
+
+struct TaskTab {
+  int32_t id = -1;
+  int64_t ncmd = 0;
+  // host mirrors of the interval CSR offsets (pred / actual) into the pools
+  std::vector<int64_t> pred_off{0}, act_off{0};
+  std::vector<uint8_t> selfpop, kind;
+  std::vector<Rule> rules;
+  std::vector<int32_t> kern_off{0};
+  std::vector<msg_range> allocs;   // sorted by start
+  DVec<int64_t> d_pred_off, d_act_off;
+  DVec<uint8_t> d_selfpop;
+  DVec<Iv> pred_pool, act_pool;   // this task's intervals (CSR by command)
+};
+
+// Per-switch planner scratch.
+struct Scratch {
+  DVec<int64_t> i64a, i64b, i64c, i64d, i64e;
+  DVec<int32_t> i32a, i32b, i32c;
+  DVec<uint32_t> u32a;
+  DVec<Iv> iv;
+  DVec<int64_t> dem, tc, cnt, tb, rb;
+  DVec<int32_t> poplist, miss, tcls;
+  DVec<int32_t> mflag;
+  DVec<int64_t> moff, msegs;
+};
+
+// Device-side scalar state (one struct in device memory).
+struct DevState {
+  int64_t head;         // index of the list head in the current order buffer
+  int64_t len;          // resident pages
+  int64_t fifo_head;    // free-frame FIFO (ring over capacity)
+  int64_t fifo_len;
+  int64_t missing;      // scratch results
+  int64_t populate, evict, truncated, free_before;
+  int32_t skip, first_missing;
+  int64_t first_missing_pages;
+  int64_t nclass;       // classes of the current multisplit
+  int64_t aux[8];
+};
+
+struct Ctx {
+  msg_cfg cfg{};
+  std::string err;
+  int device = 0;
+  cudaStream_t st = nullptr;          // planner stream
+  cudaStream_t st_d2h = nullptr, st_h2d = nullptr;
+  cudaEvent_t ev_plan_done = nullptr, ev_h2d_done = nullptr, ev_d2h_prev = nullptr;
+  int64_t P = 4096, C = 0;            // page size, capacity pages
+  // dense map
+  std::vector<int64_t> span_first, span_n, span_dense;
+  DVec<int64_t> d_span_first, d_span_n, d_span_dense;
+  int64_t D = 0;                      // dense pages
+  // residency
+  DVec<uint32_t> bits;                // resident bitmap over dense pages
+  DVec<int32_t> order[2];             // eviction order ping-pong buffers
+  int cur = 0;                        // which order buffer is live
+  int64_t head = 0, len = 0;          // host mirror of DevState head/len
+  int64_t order_cap = 0;
+  DVec<int32_t> frame;                // frame of each dense page, -1 if none
+  DVec<int32_t> fifo;                 // free frames (ring)
+  int64_t fifo_head = 0, fifo_len = 0;
+  DevState* dstate = nullptr;
+  DevState* hstate = nullptr;         // pinned mirror
+  // tasks and interval pools
+  std::vector<TaskTab*> tasks;
+  DVec<msg_range> d_allocs;           // scratch for the allocation predictor
+  Scratch s;
+  HVec<int64_t> hbuf;                 // pinned readback buffer
+  // migration
+  char* arena = nullptr;              // HBM frames
+  char* pool = nullptr;               // pinned host backing (mapped)
+  char* pool_dev = nullptr;           // device alias of pool
+  int64_t pool_pages = 0;
+  DVec<int64_t> mig_list[2];          // (page<<32|frame) per migrated page: [d2h..., h2d...]
+  int mig_par = 0;
+  cudaEvent_t ev_mig[2] = {nullptr, nullptr};
+  std::vector<cudaEvent_t> ev_pool;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_h2d, busy_d2h;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_plan;
+  msg_stats stats{};
+  // parity dumps
+  bool debug = false;
+  std::vector<int64_t> dbg[4];
+  ~Ctx();
+};
+
+// ---- helpers implemented in the .cu files ----
+int64_t dense_of_host(const Ctx& c, int64_t abs_page);   // -1 if outside
+void launch_count();                                     // bump kernel counter
+
+// predictor
+void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, const msg_arg* args,
+                      const uint8_t* blob, int64_t blob_len, const msg_range* gt, uint8_t* complete_out);
+
+// planner
+void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_always, msg_switch_out* out,
+                 int64_t* win_pages, int64_t* prefix, int64_t* touch_cnt);
+void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_window* win, int32_t nwin,
+                int32_t scan_end, bool write_tags, msg_touch_out* out, int64_t* win_pages);
+void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing, int64_t* evicted);
+void release_pages(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int64_t* removed);
+void list_append_abs(Ctx& c, const int64_t* first, const int64_t* end, int32_t n);
+void list_madvise_abs(Ctx& c, const int64_t* first, const int64_t* end, int32_t n);
+void list_evict_head(Ctx& c, int64_t n, int64_t* pages_out, int64_t* nout);
+void list_read(Ctx& c, int64_t* pages_out, int64_t cap, int64_t* n);
+void window_runs_explicit(Ctx& c, const int64_t* first, const int64_t* end, const int32_t* cmd, int32_t niv,
+                          int32_t ncmd, int64_t* runs_out, int64_t* nruns, int64_t* pages);
+void list_plan(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int64_t capacity, int64_t* pop_out,
+               int64_t* npop, int64_t* ev_out, int64_t* nev, int64_t* truncated);
+void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_t* win, int32_t n, int32_t nwin,
+                  int64_t* win_pages);
+void pull_state(Ctx& c);   // sync + copy DevState to the host mirrors
+void push_state(Ctx& c);
+
+void scan_flags(Ctx& c, const int32_t* in, int64_t n, int64_t* out);   // exclusive scan
+
+// migration
+void migration_init(Ctx& c);
+void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bool copy_h2d);
+void verify_tags(Ctx& c, int64_t* bad);
+
+int64_t kernel_launches();
+void add_launches(int64_t n);
+
+}  // namespace msg

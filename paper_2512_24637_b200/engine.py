@@ -1,0 +1,570 @@
+"""Trace replay of one oversubscribed GPU with the memory manager on a B200.
+
+Drop-in for the reference engine (engine.py:42-511): same `Mode`, `Metrics`,
+`SimEvent`, `Simulator`, `simulate`, `simulate_normalized` surface.  The
+host keeps what the north star keeps on the host — task-level scheduling,
+the event loop and every FP64 timing decision, in the reference's
+accumulation order, so timelines compare with `==`.  Everything that is set
+algebra over pages runs on the GPU through the C ABI (`_abi.Context`):
+
+  * per-command predicted / actual page sets   -> msg_add_commands (K1/K2)
+  * window build, OPT reorder, plan, apply,
+    early-start gating counts, slice touch scan -> msg_plan_switch (K3-K6, K8)
+  * fault fallback with OPT refresh             -> msg_touch
+  * demand paging (Mode.um)                     -> msg_um_slice
+  * task release                                -> msg_release_task (K9)
+  * real pinned-host <-> HBM page migration     -> the context's copy engines
+
+There is no CPU fallback: constructing a Simulator for a memory-managed mode
+without the CUDA library or a GPU raises.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+from typing import Callable, Optional, Sequence
+
+from . import _abi
+from .analyzer import build_descriptors
+from .model import CommandKind, HwConfig, PageSet, Task
+from .scheduler import Policy, TimelineEntry, build_timeline, project_cursor
+
+__all__ = [
+    "SimulationError", "Mode", "Metrics", "SimEvent", "evict_page_cost_s", "populate_page_cost_s",
+    "sequential_time", "populate_ready", "pipeline_time", "Simulator", "simulate", "simulate_normalized",
+    "um_command_duration",
+]
+
+
+class SimulationError(RuntimeError):
+    pass
+
+
+@dataclass(frozen=True)
+class Mode:
+    """engine.py:46-74."""
+
+    name: str  # "um" | "proactive" | "ideal" | "reference"
+    prefetch_pages: int = 16
+    pipelined: bool = True
+    early_start: bool = True
+    predictor: str = "template"  # "template" | "allocation" | "oracle"
+
+    @classmethod
+    def um(cls, prefetch_pages: int = 16) -> "Mode":
+        return cls("um", prefetch_pages=prefetch_pages)
+
+    @classmethod
+    def proactive(cls, pipelined: bool = True, early_start: bool = True, predictor: str = "template") -> "Mode":
+        return cls("proactive", pipelined=pipelined, early_start=early_start, predictor=predictor)
+
+    @classmethod
+    def ideal(cls) -> "Mode":
+        return cls("ideal", predictor="oracle")
+
+    @classmethod
+    def reference(cls) -> "Mode":
+        return cls("reference")
+
+
+@dataclass
+class Metrics:
+    """engine.py:77-115 (same fields, same order)."""
+
+    total_time_s: float = 0.0
+    exec_s: float = 0.0
+    save_restore_s: float = 0.0
+    madvise_s: float = 0.0
+    migration_s: float = 0.0
+    fault_s: float = 0.0
+    fault_count: int = 0
+    fault_pages: int = 0
+    prefetched_pages: int = 0
+    migrated_in_pages: int = 0
+    migrated_out_pages: int = 0
+    evicted_capacity_pages: int = 0
+    memcpy_installed_pages: int = 0
+    context_switches: int = 0
+    completed_tasks: int = 0
+    plan_truncations: int = 0
+    page_size_bytes: int = 4096
+    completion_s: dict = None
+    normalized_throughput: Optional[float] = None
+
+    def __post_init__(self):
+        if self.completion_s is None:
+            self.completion_s = {}
+
+    @property
+    def h2d_migration_pages(self) -> int:
+        return self.migrated_in_pages + self.fault_pages
+
+    @property
+    def migrated_bytes_h2d(self) -> int:
+        return self.h2d_migration_pages * self.page_size_bytes
+
+    @property
+    def migrated_bytes_d2h(self) -> int:
+        return (self.migrated_out_pages + self.evicted_capacity_pages) * self.page_size_bytes
+
+    @property
+    def planned_pages(self) -> int:
+        """The benchmark metric's numerator."""
+        return self.migrated_in_pages + self.migrated_out_pages + self.fault_pages
+
+
+@dataclass(frozen=True)
+class SimEvent:
+    t: float
+    kind: str
+    task_id: str
+    pages: int = 0
+
+
+# ---------------------------------------------------------------------------
+# timing model (engine.py:126-166) — host FP64, unchanged
+
+
+def evict_page_cost_s(hw: HwConfig) -> float:
+    return hw.per_page_unmap_s + hw.page_size_bytes / hw.bw_d2h_bytes_per_s
+
+
+def populate_page_cost_s(hw: HwConfig) -> float:
+    return hw.page_size_bytes / hw.bw_h2d_bytes_per_s + hw.per_page_map_s
+
+
+def sequential_time(hw: HwConfig, n_evict: int, n_populate: int) -> float:
+    return n_evict * evict_page_cost_s(hw) + n_populate * populate_page_cost_s(hw)
+
+
+def populate_ready(hw: HwConfig, j: int, free_pages: int, n_evict: int) -> float:
+    """Completion of the j-th populate with eviction and population on
+    separate copy engines; the makespan maximum sits at an endpoint or the
+    free-frame breakpoint (engine.py:139-158)."""
+    if j <= 0:
+        return 0.0
+    e, p = evict_page_cost_s(hw), populate_page_cost_s(hw)
+    f = max(0, free_pages)
+    best = 0.0
+    for i in (1, min(f + 1, j), j):
+        if i >= 1:
+            lag = max(0, min(i, n_evict + f) - f)
+            best = max(best, lag * e + (j - i + 1) * p)
+    return best
+
+
+def pipeline_time(hw: HwConfig, n_evict: int, n_populate: int, free_pages: int) -> float:
+    return max(n_evict * evict_page_cost_s(hw), populate_ready(hw, n_populate, free_pages, n_evict))
+
+
+def um_command_duration(hw: HwConfig, cmd, missing_pages: int, prefetch_pages: int = 16) -> float:
+    batches = math.ceil(missing_pages / prefetch_pages) if missing_pages else 0
+    return cmd.latency_s + batches * (hw.fault_control_plane_s + hw.fault_transfer_s * prefetch_pages)
+
+
+def _copy_task(t: Task) -> Task:
+    return Task(id=t.id, allocations=t.allocations, commands=list(t.commands), cursor=t.cursor,
+                priority=t.priority, arrival_s=t.arrival_s)
+
+
+def _page_span(a, page):
+    return a.base_addr // page, (a.base_addr + a.size_bytes - 1) // page + 1
+
+
+def domain_spans(tasks, page: int) -> list:
+    """Every page the replay can name: allocations, ground-truth ranges and
+    memcpy extents (the dense page map's domain)."""
+    spans = []
+    for t in tasks:
+        for a in t.allocations:
+            lo, hi = _page_span(a, page)
+            if hi > lo:
+                spans.append((lo, hi))
+        for c in t.commands:
+            for r in c.ground_truth_access:
+                spans.append((r.start_addr // page, (r.start_addr + r.length_bytes - 1) // page + 1))
+            if c.kind is not CommandKind.KERNEL and c.memcpy_size > 0:
+                d = c.device_range()
+                spans.append((d.start_addr // page, (d.end_addr - 1) // page + 1))
+    return spans
+
+
+class Simulator:
+    """engine.py:169-473 with the memory manager on the GPU.
+
+    Extra keyword arguments (not in the reference):
+      migrate    perform the real pinned-host <-> HBM copies of every plan
+      verify     stamp page ids into payloads so migration is checkable
+      device     CUDA device ordinal
+      recorder   list receiving per-switch planner records (parity dumps)
+      host_pool_pages  bound the pinned backing store (pages alias beyond it)
+    """
+
+    def __init__(self, tasks: Sequence[Task], hw: HwConfig, policy: Policy, mode: Mode,
+                 feeder: Optional[Callable[["Simulator"], None]] = None, record_events: bool = False, *,
+                 migrate: bool = False, verify: bool = False, device: int = 0, recorder: list | None = None,
+                 host_pool_pages: int = 0, descriptors: dict | None = None):
+        self.hw, self.policy, self.mode, self.feeder = hw, policy, mode, feeder
+        self.page = hw.page_size_bytes
+        self.capacity = hw.hbm_capacity_pages
+        self.tasks = [_copy_task(t) for t in tasks]
+        for t in self.tasks:
+            t.validate()
+        self.by_id = {t.id: t for t in self.tasks}
+        if len(self.by_id) != len(self.tasks):
+            raise SimulationError("duplicate task ids")
+        self._rr_order = [t.id for t in self.tasks]
+        total_alloc = sum(a.size_bytes for t in self.tasks for a in t.allocations)
+        if total_alloc > hw.dram_capacity_bytes:
+            raise SimulationError(f"allocations ({total_alloc} B) exceed DRAM backing "
+                                  f"({hw.dram_capacity_bytes} B)")
+        self.metrics = Metrics(page_size_bytes=self.page)
+        self.t = 0.0
+        self.events: list = []
+        self.record_events = record_events
+        self.recorder = recorder
+        self._idx = {t.id: i for i, t in enumerate(self.tasks)}
+        self._lat = {t.id: [c.latency_s for c in t.commands] for t in self.tasks}
+        self._selfpop = {t.id: [c.kind is CommandKind.MEMCPY_H2D for c in t.commands] for t in self.tasks}
+        self._resident = 0
+        self.ctx = None
+        if mode.name == "reference":
+            return  # no memory management at all (engine.py:390-391, 464-465)
+        if mode.name == "ideal" or mode.predictor == "oracle" or mode.name == "um":
+            pred = _abi.PRED_TRUTH
+        elif mode.predictor == "allocation":
+            pred = _abi.PRED_ALLOCATION
+        else:
+            pred = _abi.PRED_TEMPLATE
+        flags = (_abi.F_MIGRATE if migrate else 0) | (_abi.F_VERIFY_TAGS if verify else 0)
+        self.ctx = _abi.Context(self.page, self.capacity, predictor=pred, device=device, flags=flags,
+                                host_pool_pages=host_pool_pages)
+        self.ctx.set_domain(domain_spans(self.tasks, self.page))
+        if recorder is not None:
+            self.ctx.debug(True)
+        self._kernel_ids: dict = {}
+        self._lossy: dict = {}
+        self.complete: dict = {}
+        for t in self.tasks:
+            i = self._idx[t.id]
+            self.ctx.add_task(i, [(a.base_addr, a.size_bytes) for a in t.allocations])
+            kid, lossy = {}, []
+            if pred == _abi.PRED_TEMPLATE and mode.name == "proactive":
+                descs = (descriptors or {}).get(t.id) or build_descriptors(t)
+                names, rules, offs, lossy = _abi.lower_rules(descs)
+                kid = {n: k for k, n in enumerate(names)}
+                self.ctx.set_rules(i, rules, offs)
+            self._kernel_ids[t.id] = kid
+            self._lossy[t.id] = lossy
+            self.complete[t.id] = []
+            self._extend_task_tables(t, t.commands)
+
+    # -- prediction tables (engine.py:222-258) ----------------------------
+
+    def _extend_task_tables(self, task: Task, commands: Sequence):
+        if not commands:
+            return
+        kid = self._kernel_ids[task.id]
+        comp = self.ctx.add_commands(self._idx[task.id], _abi.encode_commands(commands, kid))
+        lossy = self._lossy[task.id]
+        for c, ok in zip(commands, comp):
+            k = kid.get(c.kernel_name, -1)
+            self.complete[task.id].append(bool(ok) and not (c.kind is CommandKind.KERNEL and k >= 0 and lossy[k]))
+
+    def append_commands(self, task_id: str, commands: Sequence):
+        task = self.by_id[task_id]
+        if task.remaining() == 0 and task.commands:
+            raise SimulationError(f"cannot append to completed task {task_id!r}")
+        commands = list(commands)
+        task.commands.extend(commands)
+        self._lat[task_id].extend(c.latency_s for c in commands)
+        self._selfpop[task_id].extend(c.kind is CommandKind.MEMCPY_H2D for c in commands)
+        if self.ctx is not None:
+            self._extend_task_tables(task, commands)
+
+    def predicted_pages(self, task_id: str, cmd: int) -> PageSet:
+        return PageSet._raw(self.ctx.read_pages(self._idx[task_id], cmd, 0))
+
+    def actual_pages(self, task_id: str, cmd: int) -> PageSet:
+        return PageSet._raw(self.ctx.read_pages(self._idx[task_id], cmd, 1))
+
+    # -- main loop (engine.py:262-293) ---------------------------------------
+
+    def run(self, max_switches: int = 1_000_000) -> Metrics:
+        proactive = self.mode.name in ("proactive", "ideal")
+        for _ in range(max_switches):
+            if self.feeder is not None:
+                self.feeder(self)
+            live = [t for t in self.tasks if t.remaining() > 0]
+            if not live:
+                break
+            ready = [t for t in live if t.arrival_s <= self.t + 1e-15]
+            if not ready:
+                self.t = min(t.arrival_s for t in live)
+                continue
+            rank = {tid: i for i, tid in enumerate(self._rr_order)}
+            ready.sort(key=lambda t: rank[t.id])
+            timeline = build_timeline(self.policy, ready, latencies=self._lat)
+            entry = timeline[0]
+            task = self.by_id[entry.task_id]
+            self._rr_order.remove(task.id)
+            self._rr_order.append(task.id)
+            self.metrics.context_switches += 1
+            self._charge(self.hw.save_restore_s, "save_restore_s")
+            slice_state = None
+            if proactive:
+                slice_state = self._prepare_slice(entry, timeline)
+            self._emit("switch", task.id)
+            self._run_slice(task, entry, timeline, slice_state)
+            if task.remaining() == 0:
+                self._release(task)
+        else:
+            raise SimulationError("context-switch budget exhausted")
+        self.metrics.total_time_s = self.t
+        return self.metrics
+
+    def _charge(self, dt: float, bucket: str):
+        self.t += dt
+        setattr(self.metrics, bucket, getattr(self.metrics, bucket) + dt)
+
+    def _emit(self, kind: str, task_id: str, pages: int = 0):
+        if self.record_events:
+            self.events.append(SimEvent(self.t, kind, task_id, pages))
+
+    def _windows(self, timeline) -> list:
+        """(task index, cursor, end) per timeline entry: compute_window's
+        FP64 walk (memman.py:186-195) on the host, integers to the GPU."""
+        out = []
+        for e in timeline:
+            lat = self._lat[e.task_id]
+            out.append((self._idx[e.task_id], e.resume_command_cursor,
+                        project_cursor(lat, e.resume_command_cursor, e.timeslice_s)))
+        return out
+
+    def _advised(self, windows, win_pages) -> dict:
+        """ReorderStats.pages_advised: reversed windows, dict first-insertion
+        order (memman.py:238-241)."""
+        adv: dict = {}
+        for (ti, _, _), n in zip(reversed(windows), reversed(list(win_pages))):
+            tid = self.tasks[ti].id
+            adv[tid] = adv.get(tid, 0) + int(n)
+        return adv
+
+    def _madvise_cost(self, adv: dict) -> float:
+        return sum(self.hw.madvise_call_s + n * self.hw.per_page_madvise_s for n in adv.values())
+
+    # -- proactive switch (engine.py:305-361) -------------------------------
+
+    def _prepare_slice(self, entry: TimelineEntry, timeline):
+        windows = self._windows(timeline)
+        out, win_pages, prefix_cnt, touch_cnt = self.ctx.plan_switch(windows)
+        rec = None
+        if self.recorder is not None:
+            rec = {"ev": "switch", "task": entry.task_id,
+                   "windows": [[self.tasks[t].id, a, b] for t, a, b in windows], "missing": int(out.missing)}
+            self.recorder.append(rec)
+        state = {"windows": windows, "next_missing": out.first_missing,
+                 "next_missing_pages": out.first_missing_pages, "pending": None}
+        if out.early_exit:
+            self._resident = out.resident_after
+            return state
+        adv = self._advised(windows, win_pages)
+        if self.mode.name == "proactive":
+            self._charge(self._madvise_cost(adv), "madvise_s")
+        free = int(out.free_before)
+        n_pop, n_ev = int(out.populate), int(out.evict)
+        if rec is not None:
+            rec.update(advised=[[k, v] for k, v in adv.items()], order_after_reorder=self.ctx.debug_read(0),
+                       free=free, evict=self.ctx.debug_read(1), populate=self.ctx.debug_read(2),
+                       truncated=int(out.truncated))
+        if out.truncated:
+            self.metrics.plan_truncations += 1
+        self.metrics.migrated_in_pages += n_pop
+        self.metrics.migrated_out_pages += n_ev
+        self._emit("migrate", entry.task_id, n_pop)
+        if not self.mode.pipelined:
+            self._charge(sequential_time(self.hw, n_ev, n_pop), "migration_s")
+        elif self.mode.early_start:
+            c0, c1 = windows[0][1], windows[0][2]
+            pop = self._selfpop[entry.task_id]
+            prefix, cum = {}, 0
+            for c in range(c0, c1):
+                if not pop[c]:
+                    cum += int(prefix_cnt[c - c0])
+                prefix[c] = min(cum, n_pop)
+            if rec is not None:
+                rec["prefix"] = [prefix[c] for c in range(c0, c1)]
+            state["pending"] = {"prefix": prefix, "free": free, "n_evict": n_ev,
+                                "evict_done": n_ev * evict_page_cost_s(self.hw)}
+        else:
+            self._charge(pipeline_time(self.hw, n_ev, n_pop, free), "migration_s")
+        self._resident = int(out.resident_after)
+        if self._resident > self.capacity:
+            raise SimulationError("migration plan overflowed HBM capacity")
+        return state
+
+    # -- slice execution (engine.py:365-445) ---------------------------------
+
+    def _run_slice(self, task: Task, entry, timeline, state):
+        budget = entry.timeslice_s
+        elapsed = 0.0
+        offset = 0.0
+        slice_start = self.t
+        pending = state["pending"] if state else None
+        um = None
+        if self.mode.name == "um":
+            end = project_cursor(self._lat[task.id], task.cursor, budget)
+            try:
+                um = (task.cursor,) + self.ctx.um_slice(self._idx[task.id], task.cursor, end)
+            except _abi.MsgError as e:
+                if e.code == _abi.MSG_E_CAPACITY:
+                    raise SimulationError(str(e)) from None
+                raise
+            if self.recorder is not None:
+                self._um_records(task.id, self.ctx.debug_read(3))
+        while task.cursor < len(task.commands) and elapsed < budget:
+            cur = task.cursor
+            cmd = task.commands[cur]
+            if pending is not None:
+                j = pending["prefix"].get(cur, 0)
+                ready = populate_ready(self.hw, j, pending["free"], pending["n_evict"])
+                if ready > offset:
+                    self.metrics.migration_s += ready - offset
+                    offset = ready
+            offset += self._touch(task, cmd, cur, timeline, state, budget - elapsed, um)
+            offset += cmd.latency_s
+            elapsed += cmd.latency_s
+            task.cursor = cur + 1
+        if pending is not None and pending["evict_done"] > offset:
+            self.metrics.migration_s += pending["evict_done"] - offset
+            offset = pending["evict_done"]
+        self.t = slice_start + offset
+        self.metrics.exec_s += elapsed
+
+    def _um_records(self, task_id, flat):
+        i = 0
+        flat = [int(x) for x in flat]
+        while i < len(flat):
+            cmd, nm = flat[i], flat[i + 1]
+            miss = flat[i + 2:i + 2 + nm]
+            i += 2 + nm
+            ne = flat[i]
+            ev = flat[i + 1:i + 1 + ne]
+            i += 1 + ne
+            self.recorder.append({"ev": "touch", "task": task_id, "cmd": cmd, "missing": miss, "evicted": ev})
+
+    def _capacity_guard(self, n: int):
+        if n > self.capacity:
+            raise SimulationError(f"command working set ({n} pages) exceeds HBM capacity ({self.capacity} pages)")
+
+    def _touch(self, task, cmd, cur, timeline, state, remaining_budget, um) -> float:
+        name = self.mode.name
+        if name == "reference":
+            return 0.0
+        if name == "um":
+            c0, miss, ev = um
+            n = int(miss[cur - c0])
+            if not n:
+                return 0.0
+            self.metrics.evicted_capacity_pages += int(ev[cur - c0])
+            stall = 0.0
+            if cmd.kind is CommandKind.MEMCPY_H2D:
+                self.metrics.memcpy_installed_pages += n
+            else:
+                stall += self._fault(n)
+            self._emit("fault", task.id, n)
+            return stall
+        # proactive / ideal: the switch-time scan says which command misses next
+        if state["next_missing"] != cur:
+            return 0.0
+        n = int(state["next_missing_pages"])
+        self._capacity_guard(n)
+        stall = 0.0
+        over = self._resident + n - self.capacity
+        wins = []
+        head_end = None
+        if over > 0:
+            head_end = project_cursor(self._lat[task.id], cur, max(remaining_budget, 1e-12))
+            wins = [(self._idx[task.id], cur, head_end)] + state["windows"][1:]
+        scan_end = state["windows"][0][2]
+        out, win_pages = self.ctx.touch(self._idx[task.id], cur, max(over, 0), wins, scan_end,
+                                        cmd.kind is CommandKind.MEMCPY_H2D)
+        if over > 0:
+            if self.recorder is not None:
+                self.recorder.append({"ev": "refresh", "task": task.id, "cmd": cur,
+                                      "windows": [[self.tasks[t].id, a, b] for t, a, b in wins],
+                                      "order": self.ctx.debug_read(0)})
+            if self.mode.name == "proactive":
+                dt = self._madvise_cost(self._advised(wins, win_pages))
+                self.metrics.madvise_s += dt
+                stall += dt
+            self.metrics.evicted_capacity_pages += int(out.evicted)
+        if cmd.kind is CommandKind.MEMCPY_H2D:
+            self.metrics.memcpy_installed_pages += n
+        else:
+            stall += self._fault(n)
+        self._resident = int(out.resident_after)
+        if self._resident > self.capacity:
+            raise SimulationError(f"residency {self._resident} pages exceeds capacity "
+                                  f"{self.capacity} after command {cur} of task {task.id!r}")
+        if self.recorder is not None:
+            self.recorder.append({"ev": "touch", "task": task.id, "cmd": cur,
+                                  "missing": self.ctx.debug_read(2),
+                                  "evicted": self.ctx.debug_read(1) if over > 0 else []})
+        self._emit("fault", task.id, n)
+        state["next_missing"] = out.next_missing
+        state["next_missing_pages"] = out.next_missing_pages
+        return stall
+
+    def _fault(self, n_pages: int) -> float:
+        hw = self.hw
+        self.metrics.fault_pages += n_pages
+        if self.mode.name == "ideal":
+            dt = n_pages * populate_page_cost_s(hw)
+        else:
+            batches = math.ceil(n_pages / self.mode.prefetch_pages)
+            self.metrics.fault_count += batches
+            self.metrics.prefetched_pages += batches * self.mode.prefetch_pages - n_pages
+            dt = batches * (hw.fault_control_plane_s + hw.fault_transfer_s * self.mode.prefetch_pages)
+        self.metrics.fault_s += dt
+        return dt
+
+    def _release(self, task: Task):
+        self.metrics.completed_tasks += 1
+        self.metrics.completion_s[task.id] = self.t
+        if self.mode.name == "reference":
+            return
+        spans = PageSet(_page_span(a, self.page) for a in task.allocations)
+        self.ctx.release(list(spans.runs))
+        self._resident = self.ctx.list_len()
+        self._emit("release", task.id, len(spans))
+
+    # -- diagnostics -------------------------------------------------------
+
+    def eviction_order(self) -> list:
+        return [int(p) for p in self.ctx.list_read()] if self.ctx else []
+
+    def stats(self) -> dict:
+        return self.ctx.stats() if self.ctx else {}
+
+    def close(self):
+        if self.ctx is not None:
+            self.ctx.close()
+            self.ctx = None
+
+
+def simulate(tasks, hw, policy, mode, feeder=None, record_events: bool = False, **kw) -> Metrics:
+    sim = Simulator(tasks, hw, policy, mode, feeder, record_events, **kw)
+    try:
+        return sim.run()
+    finally:
+        sim.close()
+
+
+def simulate_normalized(tasks, hw, policy, mode, feeder=None, **kw) -> Metrics:
+    """engine.py:499-511."""
+    m = simulate(tasks, hw, policy, mode, feeder, **kw)
+    ref = simulate(tasks, hw, policy, Mode.reference(), feeder)
+    m.normalized_throughput = ref.total_time_s / m.total_time_s
+    return m

@@ -1,0 +1,58 @@
+"""GPU path vs the real reference: every golden simulation (tests/golden/,
+written by the reference itself) replayed through the CUDA C-ABI must give
+identical metrics (floats with ==), identical events and identical
+per-switch planner records — eviction order after each reorder, evicted
+and populated pages in order, truncation, gating prefixes, fault touches."""
+
+import dataclasses
+
+import pytest
+
+from paper_2512_24637_b200 import engine
+from tests.golden import loader
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(c["name"], m) for c in loader.sims() for m in c["runs"]]
+SLOW = {"cfg1", "cfg2", "cfg4"}
+
+
+
+
+def run_gpu(case, mode_name, **kw):
+    tasks = [loader.dec_task(t) for t in case["tasks"]]
+    tasks, feeder = loader.feeder_for(case["feeder"], tasks)
+    run = case["runs"][mode_name]
+    from paper_2512_24637_b200.model import HwConfig
+    from paper_2512_24637_b200.scheduler import Policy
+
+    hw = HwConfig(**case["hw"])
+    pol = Policy(**case["policy"])
+    mode = engine.Mode(**run["mode"])
+    rec = []
+    sim = engine.Simulator(tasks, hw, pol, mode, feeder=feeder, record_events=True, recorder=rec, **kw)
+    try:
+        m = sim.run()
+        return m, sim, rec
+    finally:
+        sim.close()
+
+
+@pytest.mark.parametrize("name,mode", [
+    pytest.param(n, m, marks=[pytest.mark.slow] if n in SLOW else []) for n, m in CASES])
+def test_gpu_matches_reference(name, mode):
+    case = loader.sim_case(name)
+    want = case["runs"][mode]
+    if "error" in want:
+        with pytest.raises(Exception) as ei:
+            run_gpu(case, mode)
+        assert type(ei.value).__name__ == want["error"]
+        assert str(ei.value) == want["message"]
+        return
+    m, sim, rec = run_gpu(case, mode)
+    got = dataclasses.asdict(m)
+    got.pop("normalized_throughput")
+    assert got == want["metrics"]
+    assert [[e.t, e.kind, e.task_id, e.pages] for e in sim.events] == want["events"]
+    want_rec = loader.canon_records(want["records"])
+    assert loader.align_sampled(loader.canon_records(rec), want_rec) == want_rec
