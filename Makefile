@@ -8,7 +8,7 @@ LIB := paper_2512_24637_b200/libmsched_b200.so
 
 all: $(LIB)
 
-build/%.o: paper_2512_24637_b200/csrc/%.cu paper_2512_24637_b200/csrc/msched_internal.cuh include/msched_b200.h
+build/%.o: paper_2512_24637_b200/csrc/%.cu $(wildcard paper_2512_24637_b200/csrc/*.cuh) include/msched_b200.h
 	@mkdir -p build
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> build/$*.ptxas.log || (cat build/$*.ptxas.log; false)
 

@@ -1,0 +1,384 @@
+"""Benchmark: MSched proactive memory scheduling on B200.
+
+One step = one full replay of the configuration's trace through the GPU
+path — device prediction tables resident, per switch: window build, OPT
+reorder (multisplit), plan, apply, gating and touch scan on the GPU, and
+the REAL migration of every planned page between pinned host DRAM and the
+HBM frame arena on the copy engines.  Metric (BASELINE.json): pages
+planned+migrated per second = (populate + evict + fault pages) / replay time.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config cfg2|cfg1|cfg4] [--no-migrate]
+
+Multi-GPU: one process per GPU (torchrun), each replaying its own
+independent tenant mix under its own HBM budget (weak scaling, no
+collective on the data path).  Timing is on the device
+(CUDA events on the planner stream, all copy streams joined), max over
+ranks.  `--impl reference` times the CPU oracle port of the reference
+algorithm (oracle/msched_port.py) on this host's cores, one core per tenant
+mix (the reference is single-threaded).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pages planned+migrated/s"
+UNIT = "pages/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg4"], default="cfg2")
+    ap.add_argument("--no-migrate", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=3, help="oracle replays in the cpu_baseline sample")
+    ap.add_argument("--skip-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def workload(name, rank):
+    from paper_2512_24637_b200 import scenarios
+
+    if name == "cfg1":
+        tasks, hw, pol = scenarios.config1_gemm(task_offset=2 * rank)
+        desc = "2x GEMM-chain (32768^3, 8 GEMMs), 16 GiB HBM budget, 2 MiB pages, RR 1.75 ms, proactive/template"
+    elif name == "cfg4":
+        tasks, hw, pol = scenarios.config4_llama70b(task_offset=4 * rank)
+        desc = "4x 70B-class decode (70 GB weights + 5 GB KV, 3 steps), 180 GB HBM budget, 4 KiB pages, RR 5 ms"
+    else:
+        tasks, hw, pol = scenarios.config2_llama8b(task_offset=3 * rank)
+        desc = ("3x Llama3-8B int8 decode (7.6 GB weights + 0.9 GB KV each, 32 layers, 8 steps), "
+                "16 GiB HBM budget, 4 KiB pages, RR 5 ms, proactive/template predictor")
+    return tasks, hw, pol, desc
+
+
+# ---------------------------------------------------------------------------
+# clocks sampling (B200_PROFILING.md recipe)
+
+
+class Clocks:
+    def __init__(self, device):
+        self.device = device
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        try:
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+            while not self._stop.is_set():
+                sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                get = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+                reasons = get(h)
+                self.samples.append((sm, reasons))
+                time.sleep(0.1)
+        except Exception as e:  # noqa: BLE001
+            self.error = str(e)
+
+    def __enter__(self):
+        self.max_mhz = None
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=2)
+
+    def summary(self):
+        names = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+                 0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
+        reasons = set()
+        for _, r in self.samples:
+            for bit, nm in names.items():
+                if r & bit:
+                    reasons.add(nm)
+        sm = [s for s, _ in self.samples]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# host-link peak (measured live: pinned 1 GiB copies on the copy engines)
+
+
+def link_peak(torch, dev):
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    out = {}
+    for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)),
+                     ("d2h", lambda: h.copy_(d, non_blocking=True))):
+        best = 0.0
+        for _ in range(3):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            best = max(best, n / (a.elapsed_time(b) * 1e6))
+        out[name] = best
+    del h, d
+    return out
+
+
+# ---------------------------------------------------------------------------
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def max_over_ranks(torch, x, ws, dev):
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(torch, x, ws, dev):
+    if ws == 1:
+        return x
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def run_reference(args):
+    """CPU oracle port of the reference path, timed on this host."""
+    ws, rank, _ = dist_init()
+    if rank != 0:
+        return 0
+    from oracle import msched_port as port
+    from paper_2512_24637_b200.engine import Mode
+
+    n_inst = max(1, args.gpus)
+    import multiprocessing as mp
+
+    def one(rk, q):
+        try:
+            os.sched_setaffinity(0, {rk % os.cpu_count()})
+        except Exception:  # noqa: BLE001
+            pass
+        tasks, hw, pol, _ = workload(args.config, rk)
+        times, pages = [], 0
+        for i in range(args.warmup + args.steps):
+            sim = port.PortSim(tasks, hw, pol, Mode.proactive())
+            t0 = time.perf_counter()
+            m = sim.run()
+            dt = time.perf_counter() - t0
+            if i >= args.warmup:
+                times.append(dt)
+            pages = m.migrated_in_pages + m.migrated_out_pages + m.fault_pages
+        q.put((times, pages))
+
+    ctx = mp.get_context("fork")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=one, args=(r, q)) for r in range(n_inst)]
+    for p in procs:
+        p.start()
+    res = [q.get() for _ in procs]
+    for p in procs:
+        p.join()
+    ms = max(statistics.mean(t) for t, _ in res) * 1e3
+    pages = sum(p for _, p in res)
+    value = pages / (ms / 1e3)
+    _, _, _, desc = workload(args.config, 0)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": args.config, "description": desc, "instances": n_inst},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": n_inst, "kind": "port",
+                         "sample": f"{args.steps} full replays of {args.config} per core (oracle/msched_port.py, "
+                                   "single-threaded like the reference)"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def cpu_baseline(args, tasks, hw, pol):
+    from oracle import msched_port as port
+    from paper_2512_24637_b200.engine import Mode
+
+    times, pages = [], 0
+    for _ in range(args.cpu_sample):
+        sim = port.PortSim(tasks, hw, pol, Mode.proactive())
+        t0 = time.perf_counter()
+        m = sim.run()
+        times.append(time.perf_counter() - t0)
+        pages = m.migrated_in_pages + m.migrated_out_pages + m.fault_pages
+    t = statistics.median(times)
+    return {"value": pages / t, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"{args.cpu_sample} full replays of {args.config} (oracle/msched_port.py; median run() "
+                      f"{t * 1e3:.0f} ms)"}, m
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    import torch
+
+    ws, rank, local = dist_init()
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=dev)
+    from paper_2512_24637_b200 import engine
+    from paper_2512_24637_b200.analyzer import build_descriptors
+
+    tasks, hw, pol, desc = workload(args.config, rank)
+    descs = {t.id: build_descriptors(t) for t in tasks}   # offline analysis: an input, not timed
+    peak = link_peak(torch, dev) if rank == 0 else None
+    migrate = not args.no_migrate
+    sim = engine.Simulator(tasks, hw, pol, engine.Mode.proactive(), migrate=migrate, device=local,
+                           descriptors=descs)
+    stream = torch.cuda.ExternalStream(sim.ctx.stream(), device=dev)
+
+    def barrier():
+        if ws > 1:
+            torch.distributed.barrier()
+
+    def one_step(reupload=False):
+        sim.reset(reupload=reupload)
+        sim.ctx.flush_l2()
+        barrier()
+        torch.cuda.synchronize(dev)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        m = sim.run()
+        sim.ctx.sync()
+        b.record(stream)
+        b.synchronize()
+        torch.cuda.synchronize(dev)
+        barrier()
+        return a.elapsed_time(b), m
+
+    for _ in range(args.warmup):
+        one_step()
+    k0 = sim.ctx.stats()["kernels"]
+    stats_acc = None
+    times = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            ms, m = one_step()
+            times.append(ms)
+            st = sim.ctx.stats()
+            if stats_acc is None:
+                stats_acc = {k: 0 for k in st}
+            for k, v in st.items():
+                stats_acc[k] += v if k != "kernels" else 0
+    launches = (sim.ctx.stats()["kernels"] - k0) // args.steps
+    ms_step = max_over_ranks(torch, statistics.mean(times), ws, dev)
+    pages_step = sum_over_ranks(torch, m.planned_pages, ws, dev)
+    value = pages_step / (ms_step / 1e3)
+    # e2e: the public API from host Task objects every step (encode, H2D of
+    # the command tables, K1 prediction on the device, replay, metrics back)
+    e2e = None
+    if not args.skip_e2e:
+        e_times, io = [], []
+        for _ in range(max(1, min(args.steps, 3))):
+            b0 = (sim.ctx.h2d_bytes, sim.ctx.d2h_bytes)
+            ms_e, _ = one_step(reupload=True)
+            e_times.append(ms_e)
+            io.append((sim.ctx.h2d_bytes - b0[0], sim.ctx.d2h_bytes - b0[1]))
+        e_ms = max_over_ranks(torch, statistics.mean(e_times), ws, dev)
+        e2e = {"value": pages_step / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(io[-1][0]),
+               "d2h_bytes_per_step": int(io[-1][1]), "ms_per_step": e_ms,
+               "includes": "host Task objects -> encode -> H2D command tables -> device K1 prediction -> "
+                           "replay with real migration -> metrics"}
+    if rank != 0:
+        barrier_done = True  # noqa: F841
+        sim.close()
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+    n = args.steps
+    st = {k: v / n for k, v in stats_acc.items()}
+    ms_kernel_ms = st["ms_ms"] / max(st["ms_passes"], 1)
+    ms_bytes = st["ms_bytes"] / max(st["ms_passes"], 1)
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            peaks = json.load(f)
+    except OSError:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    achieved = ms_bytes / (ms_kernel_ms * 1e6) if ms_kernel_ms else 0.0
+    cpu, cpu_m = cpu_baseline(args, tasks, hw, pol)
+    mig = None
+    if migrate:
+        h2d = st["h2d_bytes"] / (st["h2d_busy_ms"] * 1e6) if st["h2d_busy_ms"] else 0.0
+        d2h = st["d2h_bytes"] / (st["d2h_busy_ms"] * 1e6) if st["d2h_busy_ms"] else 0.0
+        both = (st["h2d_bytes"] + st["d2h_bytes"]) / (ms_step * 1e6)
+        mig = {"h2d_gbs": h2d, "d2h_gbs": d2h, "h2d_bytes_per_step": st["h2d_bytes"],
+               "d2h_bytes_per_step": st["d2h_bytes"], "duplex_gbs_over_step": both,
+               "peak_h2d_gbs": peak["h2d"], "peak_d2h_gbs": peak["d2h"],
+               "frac_h2d": h2d / peak["h2d"] if peak["h2d"] else None,
+               "frac_d2h": d2h / peak["d2h"] if peak["d2h"] else None,
+               "peak_kind": "measured live: pinned 1 GiB cudaMemcpyAsync, best of 3",
+               "ce_batches": st["ce_batches"], "sm_batches": st["sm_batches"],
+               "segments_per_step": st["h2d_segments"] + st["d2h_segments"]}
+    parity = {"metrics_equal_oracle": {k: getattr(m, k) for k in ("migrated_in_pages", "migrated_out_pages",
+                                                                   "fault_pages", "total_time_s")} ==
+              {k: getattr(cpu_m, k) for k in ("migrated_in_pages", "migrated_out_pages", "fault_pages",
+                                              "total_time_s")}}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": n, "warmup": args.warmup,
+        "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "int64", "data": "synthetic",
+        "config": {"workload": args.config, "description": desc, "migration": "real" if migrate else "off",
+                   "l2": "flushed between steps (256 MiB write)", "pages_per_step": pages_step},
+        "roofline": {"bound": "hbm", "kernel": "reorder multisplit (k_ms_count + scan + k_ms_scatter)",
+                     "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                     "algorithmic_bytes_per_launch": ms_bytes, "avg_launch_ms": ms_kernel_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
+        "migration": mig,
+        "planner_ms_per_step": st["plan_ms"],
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "parity": parity,
+    }
+    print(json.dumps(line))
+    sim.close()
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

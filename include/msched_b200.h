@@ -158,7 +158,18 @@ typedef struct {
   int64_t ce_batches, sm_batches;
   double h2d_busy_ms, d2h_busy_ms;   /* copy-engine busy time (CUDA events) */
   double plan_ms;                     /* planner kernel time (CUDA events) */
+  /* the reorder multisplit (the dominant planner kernel): launches, device
+   * time over its count+scan+scatter kernels, algorithmic bytes (8 B per
+   * list entry per pass: the list is read once and written once) */
+  int64_t ms_passes;
+  double ms_ms;
+  int64_t ms_bytes;
 } msg_stats;
+
+/* Forget all residency (bitmap, list, frames); keep the task tables and the
+ * predicted sets (keep_tasks=1) or drop the tasks too (keep_tasks=0).
+ * Allocations (HBM arena, pinned pool) are kept.  Clears msg_stats. */
+int msg_reset(msg_ctx *ctx, int32_t keep_tasks);
 
 int msg_create(const msg_cfg *cfg, msg_ctx **out);
 void msg_destroy(msg_ctx *ctx);

@@ -26,7 +26,7 @@ EXPORTS = [
     "msg_set_rules", "msg_add_commands", "msg_read_pages", "msg_plan_switch", "msg_touch",
     "msg_um_slice", "msg_release_task", "msg_list_append", "msg_list_madvise", "msg_list_evict_head",
     "msg_list_len", "msg_list_read", "msg_sync", "msg_get_stats", "msg_verify_residency",
-    "msg_flush_l2", "msg_list_reorder", "msg_debug", "msg_debug_read", "msg_window_runs", "msg_list_plan",
+    "msg_flush_l2", "msg_list_reorder", "msg_debug", "msg_debug_read", "msg_window_runs", "msg_list_plan", "msg_reset",
 ]
 
 
@@ -62,7 +62,8 @@ class Stats(C.Structure):
     _fields_ = [("kernels", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("h2d_segments", C.c_int64), ("d2h_segments", C.c_int64), ("ce_batches", C.c_int64),
                 ("sm_batches", C.c_int64), ("h2d_busy_ms", C.c_double), ("d2h_busy_ms", C.c_double),
-                ("plan_ms", C.c_double)]
+                ("plan_ms", C.c_double), ("ms_passes", C.c_int64), ("ms_ms", C.c_double),
+                ("ms_bytes", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -114,6 +115,7 @@ def load():
         "msg_window_runs": ([vp, vp, vp, vp, i32, i32, vp, C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "msg_list_plan": ([vp, vp, vp, i32, i64, vp, C.POINTER(i64), vp, C.POINTER(i64), C.POINTER(i64)], C.c_int),
         "msg_debug": ([vp, i32], C.c_int),
+        "msg_reset": ([vp, i32], C.c_int),
         "msg_debug_read": ([vp, i32, vp, i64, C.POINTER(i64)], C.c_int),
         "msg_sync": ([vp], C.c_int),
         "msg_get_stats": ([vp, C.POINTER(Stats)], C.c_int),
@@ -271,6 +273,8 @@ class Context:
         self.h = h
         self.page_size = page_size
         self.capacity = capacity_pages
+        self.h2d_bytes = 0   # host->device bytes handed to the ABI (inputs)
+        self.d2h_bytes = 0   # device->host result bytes read back
 
     def close(self):
         if getattr(self, "h", None):
@@ -306,6 +310,8 @@ class Context:
     def add_commands(self, idx, encoded):
         carr, aarr, barr, blen, garr = encoded
         n = len(carr)
+        self.h2d_bytes += carr.nbytes + aarr.nbytes + blen + garr.nbytes
+        self.d2h_bytes += n
         comp = np.zeros(max(n, 1), dtype=np.uint8)
         if n:
             self.check(self.lib.msg_add_commands(self.h, idx, n, _p(carr), _p(aarr), _p(barr), blen, _p(garr),
@@ -327,6 +333,8 @@ class Context:
         prefix = np.zeros(max(ncw, 1), dtype=np.int64)
         touch = np.zeros(max(ncw, 1), dtype=np.int64)
         out = SwitchOut()
+        self.h2d_bytes += C.sizeof(warr)
+        self.d2h_bytes += C.sizeof(out) + win_pages.nbytes + 2 * 8 * ncw
         self.check(self.lib.msg_plan_switch(self.h, warr, nw, int(reorder_always), C.byref(out), _p(win_pages),
                                             _p(prefix), _p(touch)))
         return out, win_pages, prefix[:ncw], touch[:ncw]
@@ -336,6 +344,8 @@ class Context:
         warr = (Window * max(nw, 1))(*[Window(t, a, b, 0) for t, a, b in windows])
         win_pages = np.zeros(max(nw, 1), dtype=np.int64)
         out = TouchOut()
+        self.h2d_bytes += C.sizeof(warr)
+        self.d2h_bytes += C.sizeof(out) + 8 * nw
         self.check(self.lib.msg_touch(self.h, idx, cmd, evict, warr if nw else None, nw, scan_end,
                                       int(write_tags), C.byref(out), _p(win_pages)))
         return out, win_pages[:nw]
@@ -432,6 +442,9 @@ class Context:
         out = np.zeros(max(n.value, 1), dtype=np.int64)
         self.check(self.lib.msg_debug_read(self.h, which, _p(out), n.value, C.byref(n)))
         return out[:n.value]
+
+    def reset(self, keep_tasks=True):
+        self.check(self.lib.msg_reset(self.h, int(keep_tasks)))
 
     def sync(self):
         self.check(self.lib.msg_sync(self.h))

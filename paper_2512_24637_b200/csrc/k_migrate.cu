@@ -116,6 +116,12 @@ void migration_init(Ctx& c) {
     throw Error(MSG_E_OOM, "pinned host pool of " + std::to_string(pbytes) + " bytes failed");
   }
   MSG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.pool_dev), c.pool, 0));
+  if (c.cfg.flags & MSG_F_MIGRATE) {
+    c.inst_ep.exact(std::max<int64_t>(c.C, 1));
+    c.free_ep.exact(std::max<int64_t>(c.C, 1));
+    MSG_CUDA(cudaMemsetAsync(c.inst_ep.p, 0xff, c.C * 4, c.st));
+    MSG_CUDA(cudaMemsetAsync(c.free_ep.p, 0xff, c.C * 4, c.st));
+  }
   if (c.cfg.flags & MSG_F_VERIFY_TAGS) {
     for (int64_t s = 0; s < c.pool_pages; ++s) *reinterpret_cast<int64_t*>(c.pool + s * c.P) = kTagMagic ^ s;
   }
@@ -169,19 +175,22 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
   int64_t* hb = c.hbuf.p;
   MSG_CUDA(cudaMemcpyAsync(hb, c.s.moff.p + n - 1, 8, cudaMemcpyDeviceToHost, c.st));
   MSG_CUDA(cudaMemcpyAsync(hb + 1, c.s.mflag.p + n - 1, 4, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaMemcpyAsync(hb + 2, &c.dstate->aux[0], 8, cudaMemcpyDeviceToHost, c.st));
   MSG_CUDA(cudaStreamSynchronize(c.st));
   int64_t nseg = hb[0] + (int64_t)(*reinterpret_cast<int32_t*>(hb + 1));
   bool use_ce = nseg <= kSegCeMax && n >= kMinCePages * nseg;
   cudaEvent_t planned = new_event(c, false);
   MSG_CUDA(cudaEventRecord(planned, c.st));
   // frames written by earlier installs must land before they are read back
-  MSG_CUDA(cudaStreamWaitEvent(c.st_d2h, c.ev_h2d_done, 0));
+  int32_t dep_d2h = reinterpret_cast<int32_t*>(hb + 2)[0];   // newest H2D batch whose frames we evict
+  int32_t dep_h2d = reinterpret_cast<int32_t*>(hb + 2)[1];   // newest D2H batch that freed reused frames
   cudaEvent_t d2h_start = new_event(c, true), d2h_end = new_event(c, true);
   cudaEvent_t h2d_start = new_event(c, true), h2d_end = new_event(c, true);
   if (!use_ce) {
     c.stats.sm_batches++;
     MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, planned, 0));
     MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_d2h_prev, 0));
+    MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_h2d_done, 0));
     MSG_CUDA(cudaEventRecord(d2h_start, c.st_h2d));
     if (n_d2h) k_sm_copy<<<296, 256, 0, c.st_h2d>>>(list, n_d2h, c.arena, c.pool_dev, c.P, c.pool_pages, 1);
     MSG_CUDA(cudaEventRecord(d2h_end, c.st_h2d));
@@ -219,6 +228,8 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     std::vector<std::pair<int64_t, cudaEvent_t>> done;   // (evictions complete up to, event)
     std::vector<void*> dd, ss;
     std::vector<size_t> zz;
+    if (dep_d2h >= 0 && dep_d2h < (int32_t)c.ev_h2d_of.size())
+      MSG_CUDA(cudaStreamWaitEvent(c.st_d2h, c.ev_h2d_of[dep_d2h], 0));
     MSG_CUDA(cudaEventRecord(d2h_start, c.st_d2h));
     int64_t k = 0, next_cut = chunk;
     for (; k < nseg; ++k) {
@@ -243,7 +254,8 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     done.push_back({n_d2h, d2h_end});
     // installs: frames that were free before this batch may still be draining
     // from earlier evictions; frames freed by this batch wait for their chunk
-    MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_d2h_prev, 0));
+    if (dep_h2d >= 0 && dep_h2d < (int32_t)c.ev_d2h_of.size())
+      MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_d2h_of[dep_h2d], 0));
     MSG_CUDA(cudaEventRecord(h2d_start, c.st_h2d));
     size_t waited = 0;
     bool any_wait = false;
@@ -284,6 +296,9 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     MSG_CUDA(cudaEventRecord(c.ev_d2h_prev, c.st_d2h));
   }
   c.busy_d2h.push_back({d2h_start, d2h_end});
+  c.ev_d2h_of.push_back(use_ce ? d2h_end : h2d_end);
+  c.ev_h2d_of.push_back(h2d_end);
+  c.mig_batch++;
   c.busy_h2d.push_back({h2d_start, h2d_end});
   c.mig_par ^= 1;
 }

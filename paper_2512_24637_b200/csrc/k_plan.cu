@@ -20,6 +20,7 @@
 // the list head (plan_migration reads evlist._runs head-first,
 // memman.py:292-301), so victim selection is a prefix, not a search.
 #include "msched_internal.cuh"
+#include "k_ranges.cuh"
 
 #include <algorithm>
 
@@ -428,92 +429,60 @@ struct DemandParams {
   const int64_t* run_a; const int64_t* run_b; const int32_t* run_lab; int64_t run_base; const int64_t* nruns;
   const uint8_t* selfpop; int32_t c0;
   const int64_t* span_first; const int64_t* span_n; const int64_t* span_dense; int32_t nspans;
-  const uint32_t* bits;
-  int64_t* dlo; int64_t* dlen; int64_t* dmiss; int64_t* dlab;  // compacted demand runs
-  int64_t* ndemand;
-  int64_t* prefix;   // per command of window 0
+  RangeOut R;            // compacted demand runs (dense), tag = first-access command - c0
 };
 
+// Window-0 runs whose first-access command is not self-populating, as a
+// RangeSet in first-access order (memman.py:189-193).  Single block.
 __global__ void __launch_bounds__(1024, 1) k_demand_collect(DemandParams P) {
-  // single block: compact window-0 runs whose first-access command is not self-populating
   int64_t nr = P.nruns[0];
   __shared__ int64_t ws[32];
-  __shared__ int64_t carry;
-  if (threadIdx.x == 0) carry = 0;
+  __shared__ int64_t carry, ucarry;
+  if (threadIdx.x == 0) { carry = 0; ucarry = 0; }
   __syncthreads();
   for (int64_t base = 0; base < nr; base += blockDim.x) {
     int64_t i = base + threadIdx.x;
     bool keep = false;
     int64_t r = P.run_base + i;
-    if (i < nr) keep = !P.selfpop[P.run_lab[r]];
-    int64_t tot;
-    int64_t ex = block_excl_scan<int64_t>(keep ? 1 : 0, ws, &tot);
-    if (keep) {
-      int64_t o = carry + ex;
+    int64_t dlo = 0, dlen = 0;
+    if (i < nr) {
+      keep = !P.selfpop[P.run_lab[r]];
       int64_t a = P.run_a[r];
       int lo = 0, hi = P.nspans;
       while (lo < hi) { int mid = (lo + hi) >> 1; if (P.span_first[mid] <= a) lo = mid + 1; else hi = mid; }
       int s = lo - 1;
-      P.dlo[o] = P.span_dense[s] + (a - P.span_first[s]);
-      P.dlen[o] = P.run_b[r] - a;
-      P.dlab[o] = P.run_lab[r] - P.c0;
+      dlo = P.span_dense[s] + (a - P.span_first[s]);
+      dlen = P.run_b[r] - a;
+    }
+    int64_t words = keep ? ((dlo + dlen + 31) >> 5) - (dlo >> 5) : 0;
+    int64_t tot, utot;
+    int64_t ex = block_scan_excl_i64(keep ? 1 : 0, ws, &tot);
+    int64_t uex = block_scan_excl_i64(words, ws, &utot);
+    if (keep) {
+      int64_t o = carry + ex;
+      P.R.lo[o] = dlo;
+      P.R.len[o] = dlen;
+      P.R.tag[o] = P.run_lab[r] - P.c0;
+      P.R.uoff[o] = ucarry + uex;
     }
     __syncthreads();
-    if (threadIdx.x == 0) carry += tot;
+    if (threadIdx.x == 0) { carry += tot; ucarry += utot; }
     __syncthreads();
   }
-  if (threadIdx.x == 0) *P.ndemand = carry;
+  if (threadIdx.x == 0) { *P.R.nr = carry; P.R.uoff[carry] = ucarry; }
 }
 
-__global__ void k_demand_count(DemandParams P) {
-  int64_t nd = *P.ndemand;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < nd; r += nwarps) {
-    int64_t c = warp_count_nonres(P.bits, P.dlo[r], P.dlen[r]);
-    if ((threadIdx.x & 31) == 0) {
-      P.dmiss[r] = c;
-      atomicAdd(reinterpret_cast<unsigned long long*>(&P.prefix[P.dlab[r]]), (unsigned long long)c);
-    }
-  }
-}
-
-// exclusive scan of dmiss (single block) and the plan scalars
-__global__ void __launch_bounds__(1024, 1) k_demand_scan(DemandParams P, DevState* S, int64_t capacity, int64_t len) {
-  int64_t nd = *P.ndemand;
-  int64_t total = block_scan_array<int64_t>(P.dmiss, nd);
-  if (threadIdx.x == 0) {
-    S->missing = total;
-    int64_t pop = total < capacity ? total : capacity;
-    S->populate = pop;
-    S->truncated = total - pop;
-    S->free_before = capacity - len;
-    int64_t ev = pop - (capacity - len);
-    S->evict = ev > 0 ? ev : 0;
-    S->skip = total == 0;
-  }
-}
-
-// write the populate list: non-resident pages of each demand run, in order,
-// truncated at `populate` (memman.py:284-291).  One warp per run.
-__global__ void k_demand_fill(DemandParams P, const DevState* S, int32_t* out) {
-  int64_t nd = *P.ndemand, cap = S->populate;
-  int lane = threadIdx.x & 31;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < nd; r += nwarps) {
-    int64_t o = P.dmiss[r];
-    if (o >= cap) continue;
-    int64_t lo = P.dlo[r], hi = lo + P.dlen[r];
-    for (int64_t p0 = lo; p0 < hi && o < cap; p0 += 32) {
-      int64_t p = p0 + lane;
-      bool want = p < hi && !is_res(P.bits, p);
-      uint32_t m = __ballot_sync(0xffffffffu, want);
-      int64_t at = o + __popc(m & ((1u << lane) - 1u));
-      if (want && at < cap) out[at] = (int32_t)p;
-      o += __popc(m);
-    }
-  }
+// plan scalars from the total missing count (memman.py:284-299)
+__global__ void k_plan_scalars(const int64_t* total_ptr, DevState* S, int64_t capacity, int64_t len) {
+  int64_t total = *total_ptr;
+  S->missing = total;
+  int64_t pop = total < capacity ? total : capacity;
+  S->populate = pop;
+  S->truncated = total - pop;
+  S->free_before = capacity - len;
+  int64_t ev = pop - (capacity - len);
+  S->evict = ev > 0 ? ev : 0;
+  S->skip = total == 0;
 }
 
 // ---------------------------------------------------------------------------
@@ -522,59 +491,149 @@ __global__ void k_demand_fill(DemandParams P, const DevState* S, int32_t* out) {
 constexpr int MS_THREADS = 256;
 constexpr int MS_ITEMS = 16;
 constexpr int MS_TILE = MS_THREADS * MS_ITEMS;
-constexpr int MS_SMEM_SEGS = 1536;
+constexpr int MS_SMEM_SEGS = 2048;
 
 struct SegTab {
   const int64_t* lo; const int64_t* hi; const int32_t* cls; const int64_t* n;
 };
 
+// Segment table staged in shared memory as 32-bit dense bounds (dense ids
+// are < 2^31), plus the per-warp digit counters of the ranking pass.
 struct MsSmem {
-  int64_t lo[MS_SMEM_SEGS];
-  int64_t hi[MS_SMEM_SEGS];
+  int32_t lo[MS_SMEM_SEGS];
+  int32_t hi[MS_SMEM_SEGS];
   int32_t cls[MS_SMEM_SEGS];
   int32_t cnt[MS_THREADS / 32][256];
 };
 
-__device__ __forceinline__ int32_t class_lookup(int64_t p, const int64_t* lo, const int64_t* hi,
-                                                const int32_t* cls, int64_t n) {
-  int64_t a = 0, b = n;
-  while (a < b) {
-    int64_t mid = (a + b) >> 1;
-    if (lo[mid] <= p) a = mid + 1; else b = mid;
+struct SegView {
+  const int32_t* lo32; const int32_t* hi32; const int32_t* cls32;   // smem copy (n <= MS_SMEM_SEGS)
+  const int64_t* lo; const int64_t* hi; const int32_t* cls;         // global fallback
+  int32_t n, steps;                                                 // steps = log2(pow2 >= n)
+  bool small;
+};
+
+// Branchless binary search with a fixed trip count, so the 16 independent
+// lookups of a thread overlap (ILP) instead of serialising on smem latency.
+__device__ __forceinline__ int32_t class_of(const SegView& S, int32_t p) {
+  int32_t pos = 0;
+  if (S.small) {
+    for (int32_t step = 1 << S.steps; step > 0; step >>= 1) {
+      int32_t q = pos + step;
+      if (q <= S.n && S.lo32[q - 1] <= p) pos = q;
+    }
+    return (pos > 0 && p < S.hi32[pos - 1]) ? S.cls32[pos - 1] : 0;
   }
-  --a;
-  return (a >= 0 && p < hi[a]) ? cls[a] : 0;
+  for (int32_t step = 1 << S.steps; step > 0; step >>= 1) {
+    int32_t q = pos + step;
+    if (q <= S.n && S.lo[q - 1] <= (int64_t)p) pos = q;
+  }
+  return (pos > 0 && (int64_t)p < S.hi[pos - 1]) ? S.cls[pos - 1] : 0;
 }
 
-__device__ void ms_load_table(const SegTab& T, MsSmem& sm, const int64_t** lo, const int64_t** hi,
-                              const int32_t** cls, int64_t* n) {
+__device__ SegView ms_load_table(const SegTab& T, MsSmem& sm) {
+  SegView S;
   int64_t nn = *T.n;
-  *n = nn;
-  if (nn <= MS_SMEM_SEGS) {
-    for (int64_t i = threadIdx.x; i < nn; i += blockDim.x) { sm.lo[i] = T.lo[i]; sm.hi[i] = T.hi[i]; sm.cls[i] = T.cls[i]; }
-    *lo = sm.lo; *hi = sm.hi; *cls = sm.cls;
-  } else {
-    *lo = T.lo; *hi = T.hi; *cls = T.cls;
-  }
+  S.n = (int32_t)nn;
+  int steps = 0;
+  while ((1ll << steps) < nn) ++steps;
+  S.steps = steps;
+  S.small = nn <= MS_SMEM_SEGS;
+  S.lo = T.lo; S.hi = T.hi; S.cls = T.cls;
+  S.lo32 = sm.lo; S.hi32 = sm.hi; S.cls32 = sm.cls;
+  if (S.small)
+    for (int64_t i = threadIdx.x; i < nn; i += blockDim.x) {
+      sm.lo[i] = (int32_t)T.lo[i]; sm.hi[i] = (int32_t)T.hi[i]; sm.cls[i] = T.cls[i];
+    }
   __syncthreads();
+  return S;
+}
+
+// The eviction list is made of long runs of consecutive page ids (pages are
+// appended run by run and every multisplit keeps relative order), so a warp
+// reads 128 consecutive list entries with one 16-byte load per lane and, when
+// they form one run inside one class segment (or one gap), classifies all 128
+// with a single lookup.  Anything else takes the per-entry slow path, staged
+// back into array order with shuffles so the ranking stays stable.
+constexpr int MS_CHUNK = 128;                       // entries per warp step
+constexpr int MS_CHUNKS = MS_ITEMS * 32 / MS_CHUNK;  // 4 steps per warp per tile
+
+__device__ __forceinline__ int4 ms_load4(const int32_t* __restrict__ src, int64_t i, int64_t n, bool aligned) {
+  if (aligned && i + 3 < n) return __ldg(reinterpret_cast<const int4*>(src + i));
+  int4 r;
+  r.x = i < n ? __ldg(src + i) : 0;
+  r.y = i + 1 < n ? __ldg(src + i + 1) : 0;
+  r.z = i + 2 < n ? __ldg(src + i + 2) : 0;
+  r.w = i + 3 < n ? __ldg(src + i + 3) : 0;
+  return r;
+}
+
+// Returns the digit shared by the 128-entry chunk [v0, v0+128) when it is one
+// run inside one class segment or one gap, else -1 (warp-uniform).
+__device__ __forceinline__ int ms_uniform_digit(const SegView& S, int32_t v0, int shift) {
+  int32_t pos = 0;
+  if (S.small) {
+    for (int32_t step = 1 << S.steps; step > 0; step >>= 1) {
+      int32_t q = pos + step;
+      if (q <= S.n && S.lo32[q - 1] <= v0) pos = q;
+    }
+    bool in = pos > 0 && v0 < S.hi32[pos - 1];
+    if (in) return v0 + MS_CHUNK - 1 < S.hi32[pos - 1] ? (S.cls32[pos - 1] >> shift) & 255 : -1;
+    return (pos == S.n || S.lo32[pos] > v0 + MS_CHUNK - 1) ? 0 : -1;
+  }
+  for (int32_t step = 1 << S.steps; step > 0; step >>= 1) {
+    int32_t q = pos + step;
+    if (q <= S.n && S.lo[q - 1] <= (int64_t)v0) pos = q;
+  }
+  bool in = pos > 0 && (int64_t)v0 < S.hi[pos - 1];
+  if (in) return (int64_t)v0 + MS_CHUNK - 1 < S.hi[pos - 1] ? (S.cls[pos - 1] >> shift) & 255 : -1;
+  return (pos == S.n || S.lo[pos] > (int64_t)v0 + MS_CHUNK - 1) ? 0 : -1;
+}
+
+__device__ __forceinline__ bool ms_is_run(const int4& v, int lane, int32_t* v0) {
+  *v0 = __shfl_sync(0xffffffffu, v.x, 0);
+  bool ok = v.y == v.x + 1 && v.z == v.x + 2 && v.w == v.x + 3 && v.x == *v0 + 4 * lane;
+  return __all_sync(0xffffffffu, ok);
+}
+
+// element (k*32 + lane) of the chunk, from the blocked int4 registers
+__device__ __forceinline__ int32_t ms_striped(const int4& v, int k, int lane) {
+  int src = k * 8 + (lane >> 2);
+  int32_t a = __shfl_sync(0xffffffffu, v.x, src), b = __shfl_sync(0xffffffffu, v.y, src);
+  int32_t c = __shfl_sync(0xffffffffu, v.z, src), d = __shfl_sync(0xffffffffu, v.w, src);
+  switch (lane & 3) { case 0: return a; case 1: return b; case 2: return c; default: return d; }
 }
 
 __global__ void __launch_bounds__(MS_THREADS) k_ms_count(const int32_t* __restrict__ src, int64_t n, SegTab T,
                                                          int shift, int32_t* __restrict__ hist, int64_t ntiles) {
   __shared__ MsSmem sm;
-  const int64_t *lo, *hi; const int32_t* cls; int64_t nt;
-  ms_load_table(T, sm, &lo, &hi, &cls, &nt);
+  SegView S = ms_load_table(T, sm);
   int32_t* h = sm.cnt[0];
   for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
   __syncthreads();
-  int64_t base = (int64_t)blockIdx.x * MS_TILE;
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-#pragma unroll 4
-  for (int it = 0; it < MS_ITEMS; ++it) {
-    int64_t i = base + warp * (MS_ITEMS * 32) + it * 32 + lane;
-    if (i < n) {
-      int32_t c = class_lookup(src[i], lo, hi, cls, nt);
-      atomicAdd(&h[(c >> shift) & 255], 1);
+  bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  int64_t wbase = (int64_t)blockIdx.x * MS_TILE + warp * (MS_ITEMS * 32);
+  int4 v[MS_CHUNKS];
+#pragma unroll
+  for (int j = 0; j < MS_CHUNKS; ++j) v[j] = ms_load4(src, wbase + j * MS_CHUNK + 4 * lane, n, aligned);
+#pragma unroll
+  for (int j = 0; j < MS_CHUNKS; ++j) {
+    int64_t cb = wbase + j * MS_CHUNK;
+    if (cb >= n) break;
+    int32_t v0;
+    bool run = ms_is_run(v[j], lane, &v0);
+    int d = (run && cb + MS_CHUNK <= n) ? ms_uniform_digit(S, v0, shift) : -1;
+    if (d >= 0) {
+      if (lane == 0) atomicAdd(&h[d], MS_CHUNK);
+      continue;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int32_t x = ms_striped(v[j], k, lane);
+      int dk = cb + k * 32 + lane < n ? (class_of(S, x) >> shift) & 255 : 256;
+      uint32_t peers = __match_any_sync(0xffffffffu, dk);
+      if (dk < 256 && lane == __ffs(peers) - 1) atomicAdd(&h[dk], __popc(peers));
     }
   }
   __syncthreads();
@@ -585,47 +644,56 @@ __global__ void __launch_bounds__(MS_THREADS) k_ms_scatter(const int32_t* __rest
                                                            int shift, const int64_t* __restrict__ goff, int64_t ntiles,
                                                            int32_t* __restrict__ dst) {
   __shared__ MsSmem sm;
-  const int64_t *lo, *hi; const int32_t* cls; int64_t nt;
-  ms_load_table(T, sm, &lo, &hi, &cls, &nt);
+  SegView S = ms_load_table(T, sm);
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = lane; i < 256; i += 32) sm.cnt[warp][i] = 0;
   __syncwarp();
-  int64_t base = (int64_t)blockIdx.x * MS_TILE;
-  int32_t v[MS_ITEMS];
-  int32_t dg[MS_ITEMS];
-  int32_t rk[MS_ITEMS];
+  bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
+  int64_t wbase = (int64_t)blockIdx.x * MS_TILE + warp * (MS_ITEMS * 32);
   const uint32_t lt = (1u << lane) - 1u;
+  int32_t val[MS_ITEMS];
+  int32_t key[MS_ITEMS];   // digit | (rank within warp & digit) << 9; 256 = invalid
 #pragma unroll
-  for (int it = 0; it < MS_ITEMS; ++it) {
-    int64_t i = base + warp * (MS_ITEMS * 32) + it * 32 + lane;
-    int d = 256;
-    if (i < n) {
-      v[it] = src[i];
-      d = (class_lookup(v[it], lo, hi, cls, nt) >> shift) & 255;
+  for (int j = 0; j < MS_CHUNKS; ++j) {
+    int64_t cb = wbase + j * MS_CHUNK;
+    int4 v = ms_load4(src, cb + 4 * lane, n, aligned);
+    int32_t v0;
+    bool run = ms_is_run(v, lane, &v0);
+    int d = (run && cb + MS_CHUNK <= n) ? ms_uniform_digit(S, v0, shift) : -1;
+    if (d >= 0) {
+      int32_t before = sm.cnt[warp][d];
+      __syncwarp();
+      if (lane == 0) sm.cnt[warp][d] = before + MS_CHUNK;
+      __syncwarp();
+      int32_t r = before + 4 * lane;
+      val[4 * j] = v.x; val[4 * j + 1] = v.y; val[4 * j + 2] = v.z; val[4 * j + 3] = v.w;
+      key[4 * j] = d | (r << 9); key[4 * j + 1] = d | ((r + 1) << 9);
+      key[4 * j + 2] = d | ((r + 2) << 9); key[4 * j + 3] = d | ((r + 3) << 9);
+      continue;
     }
-    dg[it] = d;
-    uint32_t peers = __match_any_sync(0xffffffffu, d);
-    int leader = __ffs(peers) - 1;
-    int32_t before = d < 256 ? sm.cnt[warp][d] : 0;
-    __syncwarp();
-    if (lane == leader && d < 256) sm.cnt[warp][d] = before + __popc(peers);
-    __syncwarp();
-    rk[it] = before + __popc(peers & lt);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int32_t x = ms_striped(v, k, lane);
+      int dk = cb + k * 32 + lane < n ? (class_of(S, x) >> shift) & 255 : 256;
+      uint32_t peers = __match_any_sync(0xffffffffu, dk);
+      int32_t before = dk < 256 ? sm.cnt[warp][dk] : 0;
+      __syncwarp();
+      if (dk < 256 && lane == __ffs(peers) - 1) sm.cnt[warp][dk] = before + __popc(peers);
+      __syncwarp();
+      val[4 * j + k] = x;
+      key[4 * j + k] = dk | ((before + __popc(peers & lt)) << 9);
+    }
   }
   __syncthreads();
-  // exclusive prefix over warps per digit
   for (int d = threadIdx.x; d < 256; d += blockDim.x) {
     int32_t s = 0;
     for (int w = 0; w < MS_THREADS / 32; ++w) { int32_t t = sm.cnt[w][d]; sm.cnt[w][d] = s; s += t; }
   }
   __syncthreads();
 #pragma unroll
-  for (int it = 0; it < MS_ITEMS; ++it) {
-    int d = dg[it];
-    if (d < 256) {
-      int64_t at = goff[(int64_t)d * ntiles + blockIdx.x] + sm.cnt[warp][d] + rk[it];
-      dst[at] = v[it];
-    }
+  for (int i = 0; i < MS_ITEMS; ++i) {
+    int d = key[i] & 511, r = key[i] >> 9;
+    if (d < 256) dst[goff[(int64_t)d * ntiles + blockIdx.x] + sm.cnt[warp][d] + r] = val[i];
   }
 }
 
@@ -685,6 +753,12 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
   int64_t ntiles = (n + MS_TILE - 1) / MS_TILE;
   c.s.i32a.resize(256 * ntiles, c.st);
   c.s.i64a.resize(256 * ntiles, c.st);
+  cudaEvent_t e0, e1;
+  MSG_CUDA(cudaEventCreate(&e0));
+  MSG_CUDA(cudaEventCreate(&e1));
+  c.ev_pool.push_back(e0);
+  c.ev_pool.push_back(e1);
+  MSG_CUDA(cudaEventRecord(e0, c.st));
   for (int pass = 0; pass < passes; ++pass) {
     const int32_t* src = c.order[c.cur].p + c.head;
     int32_t* dst = c.order[c.cur ^ 1].p;
@@ -697,13 +771,29 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     c.cur ^= 1;
     c.head = 0;
   }
+  MSG_CUDA(cudaEventRecord(e1, c.st));
+  c.busy_ms.push_back({e0, e1});
+  c.stats.ms_passes += passes;
+  c.stats.ms_bytes += 8 * n * passes;
 }
 
 // ---------------------------------------------------------------------------
 // apply: evict the list head, install pages at the tail (memman.py:43-56, 93-112)
 
+// Copy-ordering epochs (migration only): inst_ep[f] = batch whose H2D last
+// wrote frame f, free_ep[f] = batch whose D2H last read it.  A batch's D2H
+// waits only for the H2D batch that wrote the newest frame it evicts, and its
+// H2D into previously free frames only for the D2H batch that freed the
+// newest of them (dep[0], dep[1]).
+struct Epochs {
+  int32_t* inst_ep;
+  int32_t* free_ep;
+  int32_t batch;
+  int* dep;   // [0] max inst_ep over evicted frames, [1] max free_ep over reused free frames
+};
+
 __global__ void k_evict_head(const int32_t* order, int64_t n, uint32_t* bits, int32_t* frame, int32_t* fifo,
-                             int64_t fifo_tail, int64_t C, int64_t* mig) {
+                             int64_t fifo_tail, int64_t C, int64_t* mig, Epochs ep) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     int32_t p = order[e];
     atomicAnd(&bits[p >> 5], ~(1u << (p & 31)));
@@ -711,12 +801,17 @@ __global__ void k_evict_head(const int32_t* order, int64_t n, uint32_t* bits, in
     frame[p] = -1;
     fifo[(fifo_tail + e) % C] = f;
     if (mig) mig[e] = ((int64_t)p << 32) | (uint32_t)f;
+    if (ep.inst_ep) {
+      int32_t w = ep.inst_ep[f];
+      if (w >= 0) atomicMax(&ep.dep[0], w);
+      ep.free_ep[f] = ep.batch;
+    }
   }
 }
 
 __global__ void k_install(const int32_t* pages, const int64_t* np_dev, int64_t np_host, uint32_t* bits,
                           int32_t* frame, const int32_t* fifo, int64_t fifo_head, int64_t C, int32_t* order_tail,
-                          int64_t* mig) {
+                          int64_t* mig, Epochs ep, int64_t old_free) {
   int64_t n = np_dev ? *np_dev : np_host;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
     int32_t p = pages[j];
@@ -725,65 +820,23 @@ __global__ void k_install(const int32_t* pages, const int64_t* np_dev, int64_t n
     frame[p] = f;
     order_tail[j] = p;
     if (mig) mig[j] = ((int64_t)p << 32) | (uint32_t)f;
+    if (ep.inst_ep) {
+      if (j < old_free) {
+        int32_t r = ep.free_ep[f];
+        if (r >= 0) atomicMax(&ep.dep[1], r);
+      }
+      ep.inst_ep[f] = ep.batch;
+    }
   }
 }
 
 // ---------------------------------------------------------------------------
 // K8 touch scan: missing pages of each command's actual set (engine.py:396-397)
 
-__global__ void k_touch_scan(const Iv* act, const int64_t* act_off, int32_t c_lo, int32_t c_hi,
-                             const uint32_t* bits, int64_t* cnt) {
-  int64_t i0 = act_off[c_lo], i1 = act_off[c_hi];
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = i0 + warp; i < i1; i += nwarps) {
-    const Iv v = act[i];
-    int64_t m = warp_count_nonres(bits, v.d, v.b - v.a);
-    if ((threadIdx.x & 31) == 0 && m) {
-      int32_t lo = c_lo, hi = c_hi;  // command of interval i
-      while (lo < hi) {
-        int32_t mid = (lo + hi) >> 1;
-        if (act_off[mid + 1] <= i) lo = mid + 1; else hi = mid;
-      }
-      atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[lo - c_lo]), (unsigned long long)m);
-    }
-  }
-}
 
 // missing pages of one command in page order (for installs): one warp per interval
-__global__ void k_missing_count(const Iv* act, int64_t i0, int64_t i1, const uint32_t* bits, int64_t* cnt) {
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = i0 + warp; i < i1; i += nwarps) {
-    const Iv v = act[i];
-    int64_t m = warp_count_nonres(bits, v.d, v.b - v.a);
-    if ((threadIdx.x & 31) == 0) cnt[i - i0] = m;
-  }
-}
 
-__global__ void __launch_bounds__(1024, 1) k_scan_small(int64_t* a, int64_t n, int64_t* total) {
-  int64_t t = block_scan_array<int64_t>(a, n);
-  if (threadIdx.x == 0 && total) *total = t;
-}
 
-__global__ void k_missing_fill(const Iv* act, int64_t i0, int64_t i1, const uint32_t* bits, const int64_t* off,
-                               int32_t* out) {
-  int lane = threadIdx.x & 31;
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t i = i0 + warp; i < i1; i += nwarps) {
-    const Iv v = act[i];
-    int64_t o = off[i - i0];
-    int64_t lo = v.d, hi = v.d + (v.b - v.a);
-    for (int64_t p0 = lo; p0 < hi; p0 += 32) {
-      int64_t p = p0 + lane;
-      bool want = p < hi && !is_res(bits, p);
-      uint32_t m = __ballot_sync(0xffffffffu, want);
-      if (want) out[o + __popc(m & ((1u << lane) - 1u))] = (int32_t)p;
-      o += __popc(m);
-    }
-  }
-}
 
 // class table from explicit dense ranges (madvise / remove / release)
 __global__ void k_table_from_ranges(const int64_t* lo, const int64_t* len, int64_t n, int64_t* tlo, int64_t* thi,
@@ -933,7 +986,10 @@ static void compact_if_needed(Ctx& c) {
 }
 
 static int64_t* mig_buf(Ctx& c, int64_t n) {
+  c.batch_old_free = c.fifo_len;
   if (!(c.cfg.flags & MSG_F_MIGRATE) && !(c.cfg.flags & MSG_F_VERIFY_TAGS)) return nullptr;
+  // reset this batch's dependency maxima (DevState aux[0] holds two int32)
+  MSG_CUDA(cudaMemsetAsync(&c.dstate->aux[0], 0xff, sizeof(int64_t), c.st));
   int par = c.mig_par;
   // the copy work that last used this buffer must be finished
   MSG_CUDA(cudaStreamWaitEvent(c.st, c.ev_mig[par], 0));
@@ -942,10 +998,21 @@ static int64_t* mig_buf(Ctx& c, int64_t n) {
 }
 
 // evict `n` pages from the head; pushes frames; fills mig[0..n)
+static Epochs epochs(Ctx& c, int64_t* mig) {
+  Epochs e{nullptr, nullptr, c.mig_batch, nullptr};
+  if (mig && (c.cfg.flags & MSG_F_MIGRATE)) {
+    e.inst_ep = c.inst_ep.p;
+    e.free_ep = c.free_ep.p;
+    e.dep = reinterpret_cast<int*>(&c.dstate->aux[0]);
+  }
+  return e;
+}
+
 static void evict_head_n(Ctx& c, int64_t n, int64_t* mig) {
+  c.batch_old_free = c.fifo_len;   // frames already free before this batch's evictions
   if (n <= 0) return;
   k_evict_head<<<grid_for(n, 256), 256, 0, c.st>>>(c.order[c.cur].p + c.head, n, c.bits.p, c.frame.p, c.fifo.p,
-                                                  c.fifo_head + c.fifo_len, c.C, mig);
+                                                  c.fifo_head + c.fifo_len, c.C, mig, epochs(c, mig));
   MSG_CHECK_LAUNCH();
   add_launches(1);
   c.head += n;
@@ -957,7 +1024,8 @@ static void evict_head_n(Ctx& c, int64_t n, int64_t* mig) {
 static void install_pages(Ctx& c, const int32_t* pages, int64_t n, int64_t* mig) {
   if (n <= 0) return;
   k_install<<<grid_for(n, 256), 256, 0, c.st>>>(pages, nullptr, n, c.bits.p, c.frame.p, c.fifo.p, c.fifo_head, c.C,
-                                               c.order[c.cur].p + c.head + c.len, mig);
+                                               c.order[c.cur].p + c.head + c.len, mig, epochs(c, mig),
+                                               c.batch_old_free);
   MSG_CHECK_LAUNCH();
   add_launches(1);
   c.fifo_head = (c.fifo_head + n) % c.C;
@@ -1069,6 +1137,36 @@ void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_
   MSG_CUDA(cudaStreamSynchronize(st));
 }
 
+// per-command missing counts of the actual sets of commands [lo, hi) of t
+// (K8, engine.py:396-397); result in c.s.tc on the device
+static void touch_counts(Ctx& c, TaskTab& t, int32_t lo, int32_t hi) {
+  int32_t n = hi - lo;
+  c.s.tc.resize(std::max(n, 1), c.st);
+  MSG_CUDA(cudaMemsetAsync(c.s.tc.p, 0, std::max(n, 1) * sizeof(int64_t), c.st));
+  if (n <= 0 || t.act_off[hi] == t.act_off[lo]) return;
+  ranges_from_actual(c, t, lo, hi, c.s.ract);
+  units_count(c, c.s.ract.set(), nullptr, c.s.tc.p, nullptr);
+}
+
+// the missing pages of one command in page order, into c.s.miss; returns n
+static int64_t missing_list(Ctx& c, TaskTab& t, int32_t cmd) {
+  int64_t nu = t.act_units[cmd + 1] - t.act_units[cmd];
+  if (t.act_off[cmd + 1] == t.act_off[cmd]) return 0;
+  ranges_from_actual(c, t, cmd, cmd + 1, c.s.ract);
+  c.s.ucnt.resize(std::max<int64_t>(nu, 1), c.st);
+  c.s.uofs.resize(std::max<int64_t>(nu, 1), c.st);
+  c.s.uscr.resize(512, c.st);
+  RangeSet R = c.s.ract.set();
+  units_count(c, R, c.s.ucnt.p, nullptr, nullptr);
+  units_scan(c, R, c.s.ucnt.p, c.s.uofs.p, c.s.uscr.p + 400, c.s.uscr.p);
+  MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, c.s.uscr.p + 400, 8, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  int64_t n = c.hbuf.p[0];
+  c.s.miss.resize(std::max<int64_t>(n, 1), c.st);
+  units_fill(c, R, c.s.uofs.p, nullptr, c.s.miss.p);
+  return n;
+}
+
 void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_always, msg_switch_out* out,
                  int64_t* win_pages, int64_t* prefix, int64_t* touch_cnt) {
   if (nwin < 1) throw Error(MSG_E_INVAL, "need at least one window");
@@ -1083,33 +1181,38 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   WinBuild wb;
   build_windows(c, win, nwin, wb);
   WinPtrs wp = win_ptrs(c, nwin, wb);
-  int64_t nrun_cap = std::max<int64_t>(2 * (t0.pred_off[c1] - t0.pred_off[c0]) + 2, 2);
-  c.s.i64e.resize(std::max<int64_t>(5 * nrun_cap + ncw + 4, 64), st);
+  int64_t niv0 = t0.pred_off[c1] - t0.pred_off[c0];
+  int64_t nrun_cap = std::max<int64_t>(2 * niv0 + 2, 2);
+  int64_t units_cap = t0.pred_units[c1] - t0.pred_units[c0] + 2 * nrun_cap + 2;
+  c.s.rdem.reserve(nrun_cap, st);
+  c.s.ucnt.resize(units_cap, st);
+  c.s.uofs.resize(units_cap, st);
+  c.s.uscr.resize(512 + ncw, st);
+  int64_t* pref_d = c.s.uscr.p + 512;   // per-command gating counts
+  int64_t* total_d = c.s.uscr.p + 400;
   DemandParams D{};
-  D.run_a = wp.run_a; D.run_b = wp.run_b; D.run_lab = wp.run_lab; D.run_base = wb.win_base.empty() ? 0 : 0;
-  D.run_base = 0;  // window 0 scratch starts at 0
+  D.run_a = wp.run_a; D.run_b = wp.run_b; D.run_lab = wp.run_lab;
+  D.run_base = 0;  // window 0's scratch region starts at offset 0
   D.nruns = wp.nruns;
   D.selfpop = t0.d_selfpop.p; D.c0 = c0;
   D.span_first = c.d_span_first.p; D.span_n = c.d_span_n.p; D.span_dense = c.d_span_dense.p;
   D.nspans = (int32_t)c.span_first.size();
-  D.bits = c.bits.p;
-  // demand arrays live in a dedicated buffer (i64e is used by scans: use a local DVec)
-  DVec<int64_t>& dem = c.s.dem;
-  dem.resize(4 * nrun_cap + ncw + 8, st);
-  D.dlo = dem.p; D.dlen = dem.p + nrun_cap; D.dmiss = dem.p + 2 * nrun_cap; D.dlab = dem.p + 3 * nrun_cap;
-  D.prefix = dem.p + 4 * nrun_cap;
-  D.ndemand = D.prefix + ncw;
-  MSG_CUDA(cudaMemsetAsync(D.prefix, 0, ncw * sizeof(int64_t), st));
+  D.R = c.s.rdem.out();
+  RangeSet R = c.s.rdem.set();
+  if (ncw) MSG_CUDA(cudaMemsetAsync(pref_d, 0, ncw * sizeof(int64_t), st));
   k_demand_collect<<<1, 1024, 0, st>>>(D);
-  k_demand_count<<<grid_for(nrun_cap * 32, 256), 256, 0, st>>>(D);
-  k_demand_scan<<<1, 1024, 0, st>>>(D, c.dstate, c.C, c.len);
   MSG_CHECK_LAUNCH();
-  add_launches(3);
+  add_launches(1);
+  units_count(c, R, c.s.ucnt.p, pref_d, nullptr);
+  units_scan(c, R, c.s.ucnt.p, c.s.uofs.p, total_d, c.s.uscr.p);
+  k_plan_scalars<<<1, 1, 0, st>>>(total_d, c.dstate, c.C, c.len);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
   int64_t* hb = c.hbuf.p;
   MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(hb + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  MSG_CUDA(cudaMemcpyAsync(hb + nwin + 1, D.prefix, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  if (ncw) MSG_CUDA(cudaMemcpyAsync(hb + nwin + 1, pref_d, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaStreamSynchronize(st));
   DevState S = hs(c);
   for (int w = 0; w < nwin; ++w) win_pages[w] = hb[w];
@@ -1120,8 +1223,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   out->early_exit = S.missing == 0 && !reorder_always;
   out->free_before = c.C - c.len;
   out->populate = out->evict = out->truncated = 0;
-  // ---- phase B
-  int64_t* mig = nullptr;
+  // ---- phase B: reorder (multisplit), plan, apply, migrate
   if (!out->early_exit) {
     multisplit(c, wp.tab, passes_for(ncls));
     if (c.debug) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
@@ -1129,16 +1231,11 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     int64_t pop = S.populate, ev = S.evict;
     out->populate = pop; out->evict = ev; out->truncated = S.truncated;
     if (pop > c.C - c.len + ev) throw Error(MSG_E_CAPACITY, "migration plan overflowed HBM capacity");
-    // populate list computed against pre-apply residency
-    c.s.i32c.resize(std::max<int64_t>(pop, 1) + c.s.i32c.n, st);
+    // populate list against pre-apply residency, truncated at capacity
     DVec<int32_t>& poplist = c.s.poplist;
     poplist.resize(std::max<int64_t>(pop, 1), st);
-    if (pop) {
-      k_demand_fill<<<grid_for(nrun_cap * 32, 256), 256, 0, st>>>(D, c.dstate, poplist.p);
-      MSG_CHECK_LAUNCH();
-      add_launches(1);
-    }
-    mig = mig_buf(c, ev + pop);
+    if (pop) units_fill(c, R, c.s.uofs.p, &c.dstate->populate, poplist.p);
+    int64_t* mig = mig_buf(c, ev + pop);
     if (c.debug) {
       dump_dense(c, c.order[c.cur].p + c.head, ev, c.dbg[1]);
       dump_dense(c, poplist.p, pop, c.dbg[2]);
@@ -1149,17 +1246,8 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     if (mig) migrate_batch(c, ev, pop, out->free_before, true);
   }
   // ---- K8 touch scan of the slice (post-apply residency)
-  DVec<int64_t>& tc = c.s.tc;
-  tc.resize(std::max(ncw, 1), st);
-  MSG_CUDA(cudaMemsetAsync(tc.p, 0, std::max(ncw, 1) * sizeof(int64_t), st));
-  if (ncw) {
-    int64_t niv = t0.act_off[c1] - t0.act_off[c0];
-    k_touch_scan<<<grid_for(std::max<int64_t>(niv, 1) * 32, 256), 256, 0, st>>>(t0.act_pool.p, t0.d_act_off.p, c0, c1,
-                                                                                c.bits.p, tc.p);
-    MSG_CHECK_LAUNCH();
-    add_launches(1);
-    MSG_CUDA(cudaMemcpyAsync(hb, tc.p, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  }
+  touch_counts(c, t0, c0, c1);
+  if (ncw) MSG_CUDA(cudaMemcpyAsync(hb, c.s.tc.p, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaEventRecord(e1, st));
   MSG_CUDA(cudaStreamSynchronize(st));
   out->first_missing = -1;
@@ -1183,22 +1271,7 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   cudaStream_t st = c.st;
   c.hbuf.reserve(4 * (int64_t)nwin + (scan_end - cmd) + 64);
   // missing list of cmd against current residency (before any eviction)
-  int64_t i0 = t.act_off[cmd], i1 = t.act_off[cmd + 1], niv = i1 - i0;
-  DVec<int64_t>& cnt = c.s.cnt;
-  DVec<int32_t>& miss = c.s.miss;
-  cnt.resize(niv + 2, st);
-  int64_t n = 0;
-  if (niv) {
-    k_missing_count<<<grid_for(niv * 32, 256), 256, 0, st>>>(t.act_pool.p, i0, i1, c.bits.p, cnt.p);
-    k_scan_small<<<1, 1024, 0, st>>>(cnt.p, niv, cnt.p + niv);
-    MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, cnt.p + niv, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    MSG_CUDA(cudaStreamSynchronize(st));
-    n = c.hbuf.p[0];
-    miss.resize(std::max<int64_t>(n, 1), st);
-    k_missing_fill<<<grid_for(niv * 32, 256), 256, 0, st>>>(t.act_pool.p, i0, i1, c.bits.p, cnt.p, miss.p);
-    MSG_CHECK_LAUNCH();
-    add_launches(3);
-  }
+  int64_t n = missing_list(c, t, cmd);
   out->missing = n;
   out->refreshed = 0;
   out->evicted = 0;
@@ -1212,18 +1285,16 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     }
     ev_done = std::min(evict, c.len);
     if (c.debug) dump_dense(c, c.order[c.cur].p + c.head, ev_done, c.dbg[1]);
-    int64_t free_before = c.C - c.len;
-    (void)free_before;
     evict_head_n(c, ev_done, mig);
     out->evicted = ev_done;
   }
   if (c.debug) {
     if (evict <= 0) c.dbg[1].clear();
-    dump_dense(c, miss.p, n, c.dbg[2]);
+    dump_dense(c, c.s.miss.p, n, c.dbg[2]);
   }
   compact_if_needed(c);
   int64_t free_before = c.C - c.len;
-  install_pages(c, miss.p, n, mig ? mig + ev_done : nullptr);
+  install_pages(c, c.s.miss.p, n, mig ? mig + ev_done : nullptr);
   if (mig) migrate_batch(c, ev_done, n, free_before, !write_tags);
   out->resident_after = c.len;
   // rescan (cmd, scan_end)
@@ -1231,15 +1302,8 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   out->next_missing_pages = 0;
   int32_t lo = cmd + 1, hi = scan_end;
   if (hi > lo) {
-    DVec<int64_t>& tc = c.s.tc;
-    tc.resize(hi - lo, st);
-    MSG_CUDA(cudaMemsetAsync(tc.p, 0, (hi - lo) * sizeof(int64_t), st));
-    int64_t nv = t.act_off[hi] - t.act_off[lo];
-    k_touch_scan<<<grid_for(std::max<int64_t>(nv, 1) * 32, 256), 256, 0, st>>>(t.act_pool.p, t.d_act_off.p, lo, hi,
-                                                                               c.bits.p, tc.p);
-    MSG_CHECK_LAUNCH();
-    add_launches(1);
-    MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, tc.p, (hi - lo) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    touch_counts(c, t, lo, hi);
+    MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, c.s.tc.p, (hi - lo) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     MSG_CUDA(cudaStreamSynchronize(st));
     for (int k = 0; k < hi - lo; ++k)
       if (c.hbuf.p[k]) { out->next_missing = lo + k; out->next_missing_pages = c.hbuf.p[k]; break; }
@@ -1434,23 +1498,28 @@ void list_read(Ctx& c, int64_t* pages_out, int64_t cap, int64_t* n) {
 
 // ---- demand paging (Mode.um): per command, sequential on the device -------
 
+__global__ void k_table_from_iv(const Iv* iv, int64_t n, int64_t* lo, int64_t* hi, int32_t* cls, int64_t* tn) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    lo[i] = iv[i].d;
+    hi[i] = iv[i].d + (iv[i].b - iv[i].a);
+    cls[i] = 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) *tn = n;
+}
+
+// Demand paging slice (Mode.um, engine.py:389-445): per command, in order:
+// missing count, capacity evictions from the LRU head, install, and the LRU
+// refresh madvise(actual) as a two-class multisplit.
 void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out, int64_t* evicted_out) {
   TaskTab& t = *c.tasks[task];
   c.dbg[3].clear();
   for (int32_t cmd = c0; cmd < c1; ++cmd) {
-    // missing count
     msg_touch_out o{};
-    int64_t i0 = t.act_off[cmd], i1 = t.act_off[cmd + 1];
-    std::vector<int64_t> lo, len;
-    DVec<int64_t>& cnt = c.s.cnt;
-    int64_t niv = i1 - i0;
+    int64_t i0 = t.act_off[cmd], niv = t.act_off[cmd + 1] - i0;
     int64_t n = 0;
-    cnt.resize(niv + 2, c.st);
     if (niv) {
-      k_missing_count<<<grid_for(niv * 32, 256), 256, 0, c.st>>>(t.act_pool.p, i0, i1, c.bits.p, cnt.p);
-      k_scan_small<<<1, 1024, 0, c.st>>>(cnt.p, niv, cnt.p + niv);
-      add_launches(2);
-      MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, cnt.p + niv, 8, cudaMemcpyDeviceToHost, c.st));
+      touch_counts(c, t, cmd, cmd + 1);
+      MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, c.s.tc.p, 8, cudaMemcpyDeviceToHost, c.st));
       MSG_CUDA(cudaStreamSynchronize(c.st));
       n = c.hbuf.p[0];
     }
@@ -1473,13 +1542,17 @@ void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out
         u.insert(u.end(), c.dbg[1].begin(), c.dbg[1].end());
       }
     }
-    // LRU refresh: madvise(actual) (engine.py:398-401, 425-426)
-    std::vector<Iv> hiv(niv);
-    if (niv) {
-      MSG_CUDA(cudaMemcpyAsync(hiv.data(), t.act_pool.p + i0, niv * sizeof(Iv), cudaMemcpyDeviceToHost, c.st));
-      MSG_CUDA(cudaStreamSynchronize(c.st));
-      for (auto& v : hiv) { lo.push_back(v.d); len.push_back(v.b - v.a); }
-      if (c.len) split_by_ranges(c, lo, len);
+    if (niv && c.len) {
+      DVec<int64_t>& tb = c.s.tb;
+      DVec<int32_t>& tcls = c.s.tcls;
+      tb.resize(2 * niv + 2, c.st);
+      tcls.resize(niv, c.st);
+      k_table_from_iv<<<grid_for(niv, 256), 256, 0, c.st>>>(t.act_pool.p + i0, niv, tb.p, tb.p + niv, tcls.p,
+                                                           tb.p + 2 * niv);
+      MSG_CHECK_LAUNCH();
+      add_launches(1);
+      SegTab T{tb.p, tb.p + niv, tcls.p, tb.p + 2 * niv};
+      multisplit(c, T, 1);
     }
   }
   MSG_CUDA(cudaStreamSynchronize(c.st));
@@ -1553,32 +1626,43 @@ void list_plan(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int6
   }
   int64_t m = (int64_t)a.size();
   int64_t cap = std::max<int64_t>(m, 1);
-  DVec<int64_t> buf; buf.exact(8 * cap + 8);
+  DVec<int64_t> buf; buf.exact(3 * cap + 8);
   DVec<int32_t> lab; lab.exact(cap);
   DVec<uint8_t> sp; sp.exact(cap);
   std::vector<int32_t> hl(cap);
+  int64_t units = 0;
   for (int64_t i = 0; i < cap; ++i) hl[i] = (int32_t)i;
+  for (int64_t i = 0; i < m; ++i) {
+    int64_t d = dense_of_host(c, a[i]);
+    units += ((d + (b[i] - a[i]) + 31) >> 5) - (d >> 5);
+  }
   if (m) {
     MSG_CUDA(cudaMemcpyAsync(buf.p, a.data(), m * 8, cudaMemcpyHostToDevice, st));
     MSG_CUDA(cudaMemcpyAsync(buf.p + cap, b.data(), m * 8, cudaMemcpyHostToDevice, st));
   }
   MSG_CUDA(cudaMemcpyAsync(lab.p, hl.data(), cap * 4, cudaMemcpyHostToDevice, st));
   MSG_CUDA(cudaMemsetAsync(sp.p, 0, cap, st));
-  MSG_CUDA(cudaMemcpyAsync(buf.p + 8 * cap, &m, 8, cudaMemcpyHostToDevice, st));
+  MSG_CUDA(cudaMemcpyAsync(buf.p + 2 * cap, &m, 8, cudaMemcpyHostToDevice, st));
+  RangeBuf rb;
+  rb.reserve(cap, st);
   DemandParams D{};
-  D.run_a = buf.p; D.run_b = buf.p + cap; D.run_lab = lab.p; D.run_base = 0; D.nruns = buf.p + 8 * cap;
+  D.run_a = buf.p; D.run_b = buf.p + cap; D.run_lab = lab.p; D.run_base = 0; D.nruns = buf.p + 2 * cap;
   D.selfpop = sp.p; D.c0 = 0;
   D.span_first = c.d_span_first.p; D.span_n = c.d_span_n.p; D.span_dense = c.d_span_dense.p;
   D.nspans = (int32_t)c.span_first.size();
-  D.bits = c.bits.p;
-  D.dlo = buf.p + 2 * cap; D.dlen = buf.p + 3 * cap; D.dmiss = buf.p + 4 * cap; D.dlab = buf.p + 5 * cap;
-  D.prefix = buf.p + 6 * cap; D.ndemand = buf.p + 7 * cap;
-  MSG_CUDA(cudaMemsetAsync(D.prefix, 0, cap * 8, st));
+  D.R = rb.out();
+  RangeSet R = rb.set();
+  DVec<int32_t> ucnt; ucnt.exact(std::max<int64_t>(units, 1));
+  DVec<int64_t> uofs; uofs.exact(std::max<int64_t>(units, 1));
+  DVec<int64_t> scr; scr.exact(512);
   k_demand_collect<<<1, 1024, 0, st>>>(D);
-  k_demand_count<<<grid_for(cap * 32, 256), 256, 0, st>>>(D);
-  k_demand_scan<<<1, 1024, 0, st>>>(D, c.dstate, capacity, c.len);
   MSG_CHECK_LAUNCH();
-  add_launches(3);
+  add_launches(1);
+  units_count(c, R, ucnt.p, nullptr, nullptr);
+  units_scan(c, R, ucnt.p, uofs.p, scr.p + 400, scr.p);
+  k_plan_scalars<<<1, 1, 0, st>>>(scr.p + 400, c.dstate, capacity, c.len);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
   MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaStreamSynchronize(st));
   DevState S = *c.hstate;
@@ -1587,11 +1671,7 @@ void list_plan(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int6
   int64_t ev = std::min<int64_t>(S.evict, c.len);
   *nev = ev;
   DVec<int32_t> pl; pl.exact(std::max<int64_t>(S.populate, 1));
-  if (S.populate) {
-    k_demand_fill<<<grid_for(cap * 32, 256), 256, 0, st>>>(D, c.dstate, pl.p);
-    MSG_CHECK_LAUNCH();
-    add_launches(1);
-  }
+  if (S.populate) units_fill(c, R, uofs.p, &c.dstate->populate, pl.p);
   std::vector<int64_t> tmp;
   dump_dense(c, pl.p, S.populate, tmp);
   if (pop_out) std::copy(tmp.begin(), tmp.end(), pop_out);

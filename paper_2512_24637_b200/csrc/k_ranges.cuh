@@ -1,0 +1,39 @@
+// Range-list work units (k_ranges.cu).
+#pragma once
+#include "msched_internal.cuh"
+
+namespace msg {
+
+__device__ __forceinline__ int64_t block_scan_excl_i64(int64_t v, int64_t* smem_warp, int64_t* total) {
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int64_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) smem_warp[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    int64_t s = lane < nw ? smem_warp[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int64_t y = __shfl_up_sync(0xffffffffu, s, o);
+      if (lane >= o) s += y;
+    }
+    if (lane < nw) smem_warp[lane] = s;
+  }
+  __syncthreads();
+  int64_t before = (wid ? smem_warp[wid - 1] : 0) + x - v;
+  if (total) *total = smem_warp[nw - 1];
+  __syncthreads();
+  return before;
+}
+
+void units_count(Ctx& c, const RangeSet& R, int32_t* ucnt, int64_t* tag_cnt, int64_t* range_cnt);
+void units_scan(Ctx& c, const RangeSet& R, const int32_t* ucnt, int64_t* uofs, int64_t* total, int64_t* scratch);
+void units_fill(Ctx& c, const RangeSet& R, const int64_t* uofs, const int64_t* cap_ptr, int32_t* out);
+void ranges_from_actual(Ctx& c, TaskTab& t, int32_t c0, int32_t c1, RangeBuf& B);
+void units_scan_count(Ctx& c, const RangeSet& R, int32_t* ucnt, int64_t* uofs, int64_t* total, int64_t* scratch);
+
+}  // namespace msg

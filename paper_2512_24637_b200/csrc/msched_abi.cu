@@ -331,7 +331,46 @@ int msg_get_stats(msg_ctx* ctx, msg_stats* out) {
     cudaGetLastError();
     s.h2d_busy_ms = h;
     s.d2h_busy_ms = d;
+    double m = 0;
+    for (auto& pr : c.busy_ms) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) m += ms; }
+    cudaGetLastError();
+    s.ms_ms = m;
     *out = s;
+  });
+}
+
+int msg_reset(msg_ctx* ctx, int32_t keep_tasks) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    MSG_CUDA(cudaStreamSynchronize(c.st));
+    if (c.st_d2h) MSG_CUDA(cudaStreamSynchronize(c.st_d2h));
+    if (c.st_h2d) MSG_CUDA(cudaStreamSynchronize(c.st_h2d));
+    int64_t words = (std::max<int64_t>(c.D, 1) + 31) / 32 + 1;
+    MSG_CUDA(cudaMemsetAsync(c.bits.p, 0, words * 4, c.st));
+    k_fill_i32<<<1184, 256, 0, c.st>>>(c.frame.p, std::max<int64_t>(c.D, 1), -1);
+    k_iota_i32<<<1184, 256, 0, c.st>>>(c.fifo.p, c.C);
+    MSG_CHECK_LAUNCH();
+    add_launches(2);
+    c.cur = 0; c.head = 0; c.len = 0;
+    c.fifo_head = 0; c.fifo_len = c.C;
+    if (!keep_tasks) {
+      for (auto* t : c.tasks) delete t;
+      c.tasks.clear();
+    }
+    for (auto e : c.ev_pool) cudaEventDestroy(e);
+    c.ev_pool.clear();
+    c.busy_h2d.clear(); c.busy_d2h.clear(); c.busy_plan.clear(); c.busy_ms.clear();
+    c.ev_d2h_of.clear(); c.ev_h2d_of.clear();
+    c.mig_batch = 0;
+    if (c.inst_ep.p) {
+      MSG_CUDA(cudaMemsetAsync(c.inst_ep.p, 0xff, c.C * 4, c.st));
+      MSG_CUDA(cudaMemsetAsync(c.free_ep.p, 0xff, c.C * 4, c.st));
+    }
+    int64_t k = c.stats.kernels;
+    c.stats = msg_stats{};
+    c.stats.kernels = k;
+    for (auto& v : c.dbg) v.clear();
+    MSG_CUDA(cudaStreamSynchronize(c.st));
   });
 }
 

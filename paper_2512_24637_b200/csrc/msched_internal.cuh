@@ -101,6 +101,7 @@ struct TaskTab {
   int64_t ncmd = 0;
   // host mirrors of the interval CSR offsets (pred / actual) into the pools
   std::vector<int64_t> pred_off{0}, act_off{0};
+  std::vector<int64_t> pred_units{0}, act_units{0};   // cumulative bitmap-word units per command
   std::vector<uint8_t> selfpop, kind;
   std::vector<Rule> rules;
   std::vector<int32_t> kern_off{0};
@@ -108,6 +109,38 @@ struct TaskTab {
   DVec<int64_t> d_pred_off, d_act_off;
   DVec<uint8_t> d_selfpop;
   DVec<Iv> pred_pool, act_pool;   // this task's intervals (CSR by command)
+};
+
+// An ordered list of dense page ranges, processed one 32-page bitmap word
+// (a "unit") at a time.  uoff[r] = units before range r; uoff[nr] = total.
+struct RangeSet {
+  const int64_t* lo;
+  const int64_t* len;
+  const int32_t* tag;
+  const int64_t* uoff;
+  const int64_t* nr;
+};
+
+struct RangeOut {
+  int64_t* lo;
+  int64_t* len;
+  int32_t* tag;
+  int64_t* uoff;
+  int64_t* nr;
+};
+
+// Owning storage for a RangeSet plus its per-unit scratch.
+struct RangeBuf {
+  DVec<int64_t> i64;   // lo | len | uoff | nr
+  DVec<int32_t> tag;
+  int64_t cap = 0;
+  void reserve(int64_t n, cudaStream_t st) {
+    cap = n < 1 ? 1 : n;
+    i64.resize(3 * cap + 4, st);
+    tag.resize(cap, st);
+  }
+  RangeOut out() { return RangeOut{i64.p, i64.p + cap, tag.p, i64.p + 2 * cap, i64.p + 3 * cap + 2}; }
+  RangeSet set() { return RangeSet{i64.p, i64.p + cap, tag.p, i64.p + 2 * cap, i64.p + 3 * cap + 2}; }
 };
 
 // Per-switch planner scratch.
@@ -120,6 +153,9 @@ struct Scratch {
   DVec<int32_t> poplist, miss, tcls;
   DVec<int32_t> mflag;
   DVec<int64_t> moff, msegs;
+  RangeBuf rdem, ract;          // window-0 demand runs; actual sets of a command range
+  DVec<int32_t> ucnt;           // per-unit counts
+  DVec<int64_t> uofs, uscr;     // per-unit offsets, scan scratch
 };
 
 // Device-side scalar state (one struct in device memory).
@@ -171,10 +207,14 @@ struct Ctx {
   int64_t pool_pages = 0;
   DVec<int64_t> mig_list[2];          // (page<<32|frame) per migrated page: [d2h..., h2d...]
   int mig_par = 0;
+  int32_t mig_batch = 0;              // migration batch id (copy-ordering epochs)
+  int64_t batch_old_free = 0;         // free frames that predate the current batch
+  DVec<int32_t> inst_ep, free_ep;     // per frame: last H2D batch / last D2H batch
+  std::vector<cudaEvent_t> ev_d2h_of, ev_h2d_of;   // per batch completion events
   cudaEvent_t ev_mig[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_h2d, busy_d2h;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_plan;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_plan, busy_ms;
   msg_stats stats{};
   // parity dumps
   bool debug = false;

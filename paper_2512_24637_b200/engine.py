@@ -208,41 +208,51 @@ class Simulator:
         self.hw, self.policy, self.mode, self.feeder = hw, policy, mode, feeder
         self.page = hw.page_size_bytes
         self.capacity = hw.hbm_capacity_pages
-        self.tasks = [_copy_task(t) for t in tasks]
+        self._source = list(tasks)
+        self.record_events = record_events
+        self.recorder = recorder
+        self._descriptors = descriptors
+        self.ctx = None
+        self._host_state()
+        total_alloc = sum(a.size_bytes for t in self.tasks for a in t.allocations)
+        if total_alloc > hw.dram_capacity_bytes:
+            raise SimulationError(f"allocations ({total_alloc} B) exceed DRAM backing "
+                                  f"({hw.dram_capacity_bytes} B)")
+        if mode.name == "reference":
+            return  # no memory management at all (engine.py:390-391, 464-465)
+        if mode.name == "ideal" or mode.predictor == "oracle" or mode.name == "um":
+            self._pred = _abi.PRED_TRUTH
+        elif mode.predictor == "allocation":
+            self._pred = _abi.PRED_ALLOCATION
+        else:
+            self._pred = _abi.PRED_TEMPLATE
+        flags = (_abi.F_MIGRATE if migrate else 0) | (_abi.F_VERIFY_TAGS if verify else 0)
+        self.ctx = _abi.Context(self.page, self.capacity, predictor=self._pred, device=device, flags=flags,
+                                host_pool_pages=host_pool_pages)
+        self.ctx.set_domain(domain_spans(self.tasks, self.page))
+        if recorder is not None:
+            self.ctx.debug(True)
+        self._register_tasks()
+
+    def _host_state(self):
+        """Fresh copies of the input tasks and all host-side loop state."""
+        self.tasks = [_copy_task(t) for t in self._source]
         for t in self.tasks:
             t.validate()
         self.by_id = {t.id: t for t in self.tasks}
         if len(self.by_id) != len(self.tasks):
             raise SimulationError("duplicate task ids")
         self._rr_order = [t.id for t in self.tasks]
-        total_alloc = sum(a.size_bytes for t in self.tasks for a in t.allocations)
-        if total_alloc > hw.dram_capacity_bytes:
-            raise SimulationError(f"allocations ({total_alloc} B) exceed DRAM backing "
-                                  f"({hw.dram_capacity_bytes} B)")
         self.metrics = Metrics(page_size_bytes=self.page)
         self.t = 0.0
         self.events: list = []
-        self.record_events = record_events
-        self.recorder = recorder
         self._idx = {t.id: i for i, t in enumerate(self.tasks)}
         self._lat = {t.id: [c.latency_s for c in t.commands] for t in self.tasks}
         self._selfpop = {t.id: [c.kind is CommandKind.MEMCPY_H2D for c in t.commands] for t in self.tasks}
         self._resident = 0
-        self.ctx = None
-        if mode.name == "reference":
-            return  # no memory management at all (engine.py:390-391, 464-465)
-        if mode.name == "ideal" or mode.predictor == "oracle" or mode.name == "um":
-            pred = _abi.PRED_TRUTH
-        elif mode.predictor == "allocation":
-            pred = _abi.PRED_ALLOCATION
-        else:
-            pred = _abi.PRED_TEMPLATE
-        flags = (_abi.F_MIGRATE if migrate else 0) | (_abi.F_VERIFY_TAGS if verify else 0)
-        self.ctx = _abi.Context(self.page, self.capacity, predictor=pred, device=device, flags=flags,
-                                host_pool_pages=host_pool_pages)
-        self.ctx.set_domain(domain_spans(self.tasks, self.page))
-        if recorder is not None:
-            self.ctx.debug(True)
+
+    def _register_tasks(self):
+        """Allocations, rule tables and every command's page sets (K1) to the device."""
         self._kernel_ids: dict = {}
         self._lossy: dict = {}
         self.complete: dict = {}
@@ -250,8 +260,8 @@ class Simulator:
             i = self._idx[t.id]
             self.ctx.add_task(i, [(a.base_addr, a.size_bytes) for a in t.allocations])
             kid, lossy = {}, []
-            if pred == _abi.PRED_TEMPLATE and mode.name == "proactive":
-                descs = (descriptors or {}).get(t.id) or build_descriptors(t)
+            if self._pred == _abi.PRED_TEMPLATE and self.mode.name == "proactive":
+                descs = (self._descriptors or {}).get(t.id) or build_descriptors(t)
                 names, rules, offs, lossy = _abi.lower_rules(descs)
                 kid = {n: k for k, n in enumerate(names)}
                 self.ctx.set_rules(i, rules, offs)
@@ -259,6 +269,17 @@ class Simulator:
             self._lossy[t.id] = lossy
             self.complete[t.id] = []
             self._extend_task_tables(t, t.commands)
+
+    def reset(self, reupload: bool = False):
+        """Replay again from the start.  The device keeps its allocations; with
+        reupload=False it also keeps the predicted page sets (the trace stays
+        resident in HBM), with reupload=True the task tables are rebuilt from
+        the host Task objects (encode, H2D, K1 prediction)."""
+        self._host_state()
+        if self.ctx is not None:
+            self.ctx.reset(keep_tasks=not reupload)
+            if reupload:
+                self._register_tasks()
 
     # -- prediction tables (engine.py:222-258) ----------------------------
 

@@ -56,3 +56,35 @@ def test_gpu_matches_reference(name, mode):
     assert [[e.t, e.kind, e.task_id, e.pages] for e in sim.events] == want["events"]
     want_rec = loader.canon_records(want["records"])
     assert loader.align_sampled(loader.canon_records(rec), want_rec) == want_rec
+
+
+MIGRATION_CASES = ["llm_2.0", "stream_3.0", "stream_ind", "frag", "struct", "feed"]
+
+
+@pytest.mark.parametrize("name", MIGRATION_CASES)
+@pytest.mark.parametrize("mode", ["proactive", "ideal"])
+def test_gpu_migration_moves_the_right_bytes(name, mode):
+    """With real copies on: same metrics as the reference, and every resident
+    page's HBM frame holds that page's payload (page-id tags written into the
+    pinned host pool and carried by every D2H/H2D copy)."""
+    case = loader.sim_case(name)
+    if mode not in case["runs"]:
+        pytest.skip("mode not in fixture")
+    want = case["runs"][mode]
+    tasks = [loader.dec_task(t) for t in case["tasks"]]
+    tasks, feeder = loader.feeder_for(case["feeder"], tasks)
+    from paper_2512_24637_b200.model import HwConfig
+    from paper_2512_24637_b200.scheduler import Policy
+
+    sim = engine.Simulator(tasks, HwConfig(**case["hw"]), Policy(**case["policy"]), engine.Mode(**want["mode"]),
+                           feeder=feeder, migrate=True, verify=True)
+    try:
+        m = sim.run()
+        assert sim.ctx.verify() == 0
+        st = sim.ctx.stats()
+        assert st["h2d_bytes"] >= m.migrated_in_pages * m.page_size_bytes
+    finally:
+        sim.close()
+    got = dataclasses.asdict(m)
+    got.pop("normalized_throughput")
+    assert got == want["metrics"]
