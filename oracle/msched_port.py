@@ -876,7 +876,11 @@ class PortSim:
     """
 
     def __init__(self, tasks, hw, policy, mode, feeder=None, record_events=False,
-                 recorder=None, descriptors=None):
+                 recorder=None, descriptors=None, order_every=1, pack=None):
+        self.order_every = order_every   # record the full list order every k-th reorder (0: never)
+        self.pack = pack or (lambda pages: pages)   # applied to recorded page lists (e.g. a digest)
+        self._nreorder = 0
+        self._nrefresh = 0
         self.hw, self.policy, self.mode, self.feeder = hw, policy, mode, feeder
         self.page = hw.page_size_bytes
         self.capacity = hw.hbm_capacity_bytes // hw.page_size_bytes
@@ -986,9 +990,11 @@ class PortSim:
         free = self.capacity - len(self.rl)
         plan = make_plan(self.rl, w0.demand, self.capacity)
         if rec is not None:
-            rec.update(advised=list(advised.items()), order_after_reorder=self.rl.order(),
-                       evict=runs_pages(plan.evict), populate=runs_pages(plan.populate),
-                       truncated=plan.truncated, free=free)
+            rec.update(advised=list(advised.items()), evict=self.pack(runs_pages(plan.evict)),
+                       populate=self.pack(runs_pages(plan.populate)), truncated=plan.truncated, free=free)
+            if self.order_every and self._nreorder % self.order_every == 0:
+                rec["order_after_reorder"] = self.pack(self.rl.order())
+        self._nreorder += 1
         if plan.truncated:
             self.m.plan_truncations += 1
         self.m.migrated_in_pages += plan.n_populate
@@ -1000,7 +1006,7 @@ class PortSim:
         elif self.mode.early_start:
             pending = self._gating(tl[0], w0, plan, free)
             if rec is not None:
-                rec["prefix"] = [pending["prefix"][c] for c in range(w0.start, w0.end)]
+                rec["prefix"] = self.pack([pending["prefix"][c] for c in range(w0.start, w0.end)])
         else:
             self._charge(pipe_swap_time(self.hw, plan.n_evict, plan.n_populate, free), "migration_s")
         apply_plan_runs(self.rl, plan)
@@ -1078,8 +1084,8 @@ class PortSim:
             raise SimulationError(f"residency {len(self.rl)} pages exceeds capacity "
                                   f"{self.capacity} after command {c} of task {t.id!r}")
         if self.rec is not None:
-            self.rec.append({"ev": "touch", "task": t.id, "cmd": c, "missing": runs_pages(missing),
-                             "evicted": runs_pages(evicted)})
+            self.rec.append({"ev": "touch", "task": t.id, "cmd": c, "missing": self.pack(runs_pages(missing)),
+                             "evicted": self.pack(runs_pages(evicted))})
         if self.mode.name == "um":
             self.rl.advise(actual)
         self._emit("fault", t.id, n)
@@ -1105,9 +1111,12 @@ class PortSim:
         rest = windows_of(tl[1:], self.by_id)
         advised = opt_reorder(self.rl, [head] + rest)
         if self.rec is not None:
-            self.rec.append({"ev": "refresh", "task": t.id, "cmd": c,
-                             "windows": [(w.task_id, w.start, w.end) for w in [head] + rest],
-                             "order": self.rl.order()})
+            r = {"ev": "refresh", "task": t.id, "cmd": c,
+                 "windows": [(w.task_id, w.start, w.end) for w in [head] + rest]}
+            if self.order_every and self._nrefresh % self.order_every == 0:
+                r["order"] = self.pack(self.rl.order())
+            self.rec.append(r)
+        self._nrefresh += 1
         if self.mode.name == "proactive":
             dt = advise_cost(self.hw, advised)
             self.m.madvise_s += dt

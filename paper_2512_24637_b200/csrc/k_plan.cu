@@ -1226,7 +1226,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   // ---- phase B: reorder (multisplit), plan, apply, migrate
   if (!out->early_exit) {
     multisplit(c, wp.tab, passes_for(ncls));
-    if (c.debug) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
+    if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     out->free_before = c.C - c.len;
     int64_t pop = S.populate, ev = S.evict;
     out->populate = pop; out->evict = ev; out->truncated = S.truncated;
@@ -1281,7 +1281,7 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     if (nwin > 0) {
       reorder_with_windows(c, win, nwin, win_pages);
       out->refreshed = 1;
-      if (c.debug) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
+      if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     }
     ev_done = std::min(evict, c.len);
     if (c.debug) dump_dense(c, c.order[c.cur].p + c.head, ev_done, c.dbg[1]);

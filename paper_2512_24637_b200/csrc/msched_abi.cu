@@ -296,7 +296,7 @@ int msg_list_plan(msg_ctx* ctx, const int64_t* run_first, const int64_t* run_end
 }
 
 int msg_debug(msg_ctx* ctx, int32_t enable) {
-  return guard(ctx, [&] { ctx->c.debug = enable != 0; });
+  return guard(ctx, [&] { ctx->c.debug = enable; });
 }
 
 int msg_debug_read(msg_ctx* ctx, int32_t which, int64_t* out, int64_t cap, int64_t* n) {

@@ -217,7 +217,7 @@ struct Ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_plan, busy_ms;
   msg_stats stats{};
   // parity dumps
-  bool debug = false;
+  int debug = 0;   // 1: plan lists, 2: full list orders
   std::vector<int64_t> dbg[4];
   ~Ctx();
 };

@@ -204,13 +204,14 @@ class Simulator:
     def __init__(self, tasks: Sequence[Task], hw: HwConfig, policy: Policy, mode: Mode,
                  feeder: Optional[Callable[["Simulator"], None]] = None, record_events: bool = False, *,
                  migrate: bool = False, verify: bool = False, device: int = 0, recorder: list | None = None,
-                 host_pool_pages: int = 0, descriptors: dict | None = None):
+                 host_pool_pages: int = 0, descriptors: dict | None = None, order_every: int = 1):
         self.hw, self.policy, self.mode, self.feeder = hw, policy, mode, feeder
         self.page = hw.page_size_bytes
         self.capacity = hw.hbm_capacity_pages
         self._source = list(tasks)
         self.record_events = record_events
         self.recorder = recorder
+        self.order_every = max(1, order_every)   # dump the full list order every k-th reorder
         self._descriptors = descriptors
         self.ctx = None
         self._host_state()
@@ -231,7 +232,7 @@ class Simulator:
                                 host_pool_pages=host_pool_pages)
         self.ctx.set_domain(domain_spans(self.tasks, self.page))
         if recorder is not None:
-            self.ctx.debug(True)
+            self.ctx.debug(3)
         self._register_tasks()
 
     def _host_state(self):
@@ -250,6 +251,8 @@ class Simulator:
         self._lat = {t.id: [c.latency_s for c in t.commands] for t in self.tasks}
         self._selfpop = {t.id: [c.kind is CommandKind.MEMCPY_H2D for c in t.commands] for t in self.tasks}
         self._resident = 0
+        self._nreorder = 0
+        self._nrefresh = 0
 
     def _register_tasks(self):
         """Allocations, rule tables and every command's page sets (K1) to the device."""
@@ -379,6 +382,10 @@ class Simulator:
 
     def _prepare_slice(self, entry: TimelineEntry, timeline):
         windows = self._windows(timeline)
+        dump_order = False
+        if self.recorder is not None:
+            dump_order = self._nreorder % self.order_every == 0
+            self.ctx.debug(3 if dump_order else 1)
         out, win_pages, prefix_cnt, touch_cnt = self.ctx.plan_switch(windows)
         rec = None
         if self.recorder is not None:
@@ -395,10 +402,13 @@ class Simulator:
             self._charge(self._madvise_cost(adv), "madvise_s")
         free = int(out.free_before)
         n_pop, n_ev = int(out.populate), int(out.evict)
+        self._nreorder += 1
         if rec is not None:
-            rec.update(advised=[[k, v] for k, v in adv.items()], order_after_reorder=self.ctx.debug_read(0),
-                       free=free, evict=self.ctx.debug_read(1), populate=self.ctx.debug_read(2),
-                       truncated=int(out.truncated))
+            rec.update(advised=[[k, v] for k, v in adv.items()], free=free, evict=self.ctx.debug_read(1),
+                       populate=self.ctx.debug_read(2), truncated=int(out.truncated))
+            if dump_order:
+                rec["order_after_reorder"] = self.ctx.debug_read(0)
+            self.ctx.debug(3)
         if out.truncated:
             self.metrics.plan_truncations += 1
         self.metrics.migrated_in_pages += n_pop
@@ -509,13 +519,21 @@ class Simulator:
             head_end = project_cursor(self._lat[task.id], cur, max(remaining_budget, 1e-12))
             wins = [(self._idx[task.id], cur, head_end)] + state["windows"][1:]
         scan_end = state["windows"][0][2]
+        dump_order = False
+        if self.recorder is not None and over > 0:
+            dump_order = self._nrefresh % self.order_every == 0
+            self._nrefresh += 1
+            self.ctx.debug(3 if dump_order else 1)
         out, win_pages = self.ctx.touch(self._idx[task.id], cur, max(over, 0), wins, scan_end,
                                         cmd.kind is CommandKind.MEMCPY_H2D)
         if over > 0:
             if self.recorder is not None:
-                self.recorder.append({"ev": "refresh", "task": task.id, "cmd": cur,
-                                      "windows": [[self.tasks[t].id, a, b] for t, a, b in wins],
-                                      "order": self.ctx.debug_read(0)})
+                r = {"ev": "refresh", "task": task.id, "cmd": cur,
+                     "windows": [[self.tasks[t].id, a, b] for t, a, b in wins]}
+                if dump_order:
+                    r["order"] = self.ctx.debug_read(0)
+                self.recorder.append(r)
+                self.ctx.debug(3)
             if self.mode.name == "proactive":
                 dt = self._madvise_cost(self._advised(wins, win_pages))
                 self.metrics.madvise_s += dt

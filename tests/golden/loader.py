@@ -65,11 +65,14 @@ def ns(d):
 
 
 def digest(pages):
-    """Same digest make_golden.py stores for long page lists."""
-    pages = [int(p) for p in pages]
-    if len(pages) <= BIG:
-        return pages
-    return {"n": len(pages), "sha1": hashlib.sha1(struct.pack(f"<{len(pages)}q", *pages)).hexdigest()}
+    """Same digest make_golden.py stores for long page lists (sha1 of the
+    little-endian int64 array)."""
+    import numpy as np
+
+    arr = np.asarray(pages, dtype="<i8").reshape(-1)
+    if arr.size <= BIG:
+        return [int(p) for p in arr]
+    return {"n": int(arr.size), "sha1": hashlib.sha1(arr.tobytes()).hexdigest()}
 
 
 def feeder_for(spec, tasks):
@@ -121,3 +124,26 @@ def align_sampled(got, want):
         if g.get("ev") == "switch" and "order_after_reorder" in g and "order_after_reorder" not in w:
             del g["order_after_reorder"]
     return got
+
+
+def strip_orders(recs):
+    out = []
+    for r in recs:
+        r = dict(r)
+        r.pop("order_after_reorder", None)
+        r.pop("order", None)
+        out.append(r)
+    return out
+
+
+def sample_refresh_orders(recs, every):
+    """Keep the full-order digest of every k-th refresh record only."""
+    out, k = [], 0
+    for r in recs:
+        if r.get("ev") == "refresh":
+            r = dict(r)
+            if k % every:
+                r.pop("order", None)
+            k += 1
+        out.append(r)
+    return out
