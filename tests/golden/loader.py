@@ -25,7 +25,11 @@ def _load(name):
 
 @functools.lru_cache(maxsize=None)
 def sims():
-    return _load("sims.json.gz")
+    """Reference-generated simulations: make_golden.py + make_golden_extra.py."""
+    out = _load("sims.json.gz")
+    if os.path.exists(os.path.join(HERE, "sims_extra.json.gz")):
+        out = out + _load("sims_extra.json.gz")
+    return out
 
 
 @functools.lru_cache(maxsize=None)

@@ -14,7 +14,7 @@ from tests.golden import loader
 pytestmark = pytest.mark.gpu
 
 CASES = [(c["name"], m) for c in loader.sims() for m in c["runs"]]
-SLOW = {"cfg1", "cfg2", "cfg4"}
+SLOW = {"cfg1", "cfg2", "cfg4", "cfg5_16k", "cfg5_64k"}
 ORDER_EVERY = {"cfg4": 40}   # mirrors make_golden.py
 
 

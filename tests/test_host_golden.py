@@ -56,7 +56,7 @@ def test_scenarios_match_golden_inputs():
     for case in loader.sims():
         g = case.get("gen")
         if not g or g["fn"] not in ("streaming_scenario", "llm_scenario", "uniform_scenario", "cfg1", "cfg2",
-                                    "cfg4"):
+                                    "cfg4", "config3_mixed"):
             continue
         if g["fn"] == "streaming_scenario":
             tasks, _ = scenarios.streaming_scenario(hw, g["ratio"], indirect_rate=g.get("indirect_rate", 0.0),
@@ -66,6 +66,12 @@ def test_scenarios_match_golden_inputs():
         elif g["fn"] == "uniform_scenario":
             tasks, _ = scenarios.uniform_scenario(get_preset("rtx5080").with_capacity(16 << 20), g["n_tasks"],
                                                   g["footprint"])
+        elif g["fn"] == "config3_mixed":
+            from paper_2512_24637_b200.workload_extra import config3_mixed
+
+            tasks = config3_mixed(ratio=g["ratio"], timeslice_s=g["timeslice_s"])[0]
+        elif g["fn"] == "cfg2" and "page" in g:
+            tasks = scenarios.config2_llama8b(page=g["page"])[0]
         else:
             tasks = {"cfg1": scenarios.config1_gemm, "cfg2": scenarios.config2_llama8b,
                      "cfg4": scenarios.config4_llama70b}[g["fn"]]()[0]

@@ -11,10 +11,10 @@ from oracle import msched_port as port
 from tests.golden import loader
 
 CASES = [(c["name"], m) for c in loader.sims() for m in c["runs"]]
-SLOW = {"cfg1", "cfg2", "cfg4"}
+SLOW = {"cfg1", "cfg2", "cfg4", "cfg5_16k", "cfg5_64k"}
 # big cases: the golden generator sampled the full list order every k-th
 # reorder; the port skips orders there (its run-list order dump is O(pages))
-ORDER_EVERY = {"cfg4": 0, "cfg2": 0}
+ORDER_EVERY = {"cfg4": 0, "cfg2": 0, "cfg5_16k": 0, "cfg5_64k": 0}
 
 
 def run_port(case, mode_name):
