@@ -140,14 +140,29 @@ struct WinOut {
   int64_t* pages;   // per window |w.pages|
 };
 
+extern __shared__ __align__(16) unsigned char dyn_smem[];
+constexpr int64_t kWinSmem = 200 * 1024;
+
+// Scratch lives in shared memory when the window fits (44 B per padded
+// endpoint: key[4mp] val[mp] label[mp]), else in the global region the host
+// reserved (same layout).
 __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, int64_t* gkey_u, int64_t* gval,
-                              int32_t* glab, WinOut out) {
+                              int32_t* glab, WinOut out, int64_t smem_cap) {
   const WinDesc W = wins[blockIdx.x];
   const Iv* pool = W.pool;
   int64_t n = W.pool_hi - W.pool_lo;
   int64_t base = W.scratch;           // scratch: 4n slots of key/val, 2n labels
   uint64_t* key = reinterpret_cast<uint64_t*>(gkey_u) + base;
   int64_t* val = gval + base;
+  int32_t* L = glab + base;
+  {
+    int64_t mp0 = pow2_at_least(2 * n);
+    if (44 * mp0 <= smem_cap) {
+      key = reinterpret_cast<uint64_t*>(dyn_smem);
+      val = reinterpret_cast<int64_t*>(key + 4 * mp0);
+      L = reinterpret_cast<int32_t*>(val + mp0);
+    }
+  }
   __shared__ int64_t tot_s;
   if (n == 0) {
     if (threadIdx.x == 0) { out.nruns[W.w] = 0; out.pages[W.w] = 0; out.run_base[W.w] = base; }
@@ -179,7 +194,6 @@ __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, in
   }
   __syncthreads();
   int64_t nseg = nu - 1;
-  int32_t* L = glab + base;   // 2n labels available
   for (int64_t k = threadIdx.x; k < nseg; k += blockDim.x) L[k] = kNone;
   __syncthreads();
   // 3. label = min covering command (first access)
@@ -291,7 +305,7 @@ __device__ __forceinline__ int tuple_cmp(const int32_t* T, int64_t i, int64_t j,
   return 0;
 }
 
-__global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P) {
+__global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P, int64_t smem_cap) {
   __shared__ int64_t tot_runs_s;
   int W = P.nwin;
   // gather all runs' endpoints
@@ -307,6 +321,13 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P) {
     return;
   }
   int64_t m = 2 * M, mp = pow2_at_least(m);
+  if (8 * (4 * mp + m) + 4 * m * W <= smem_cap) {   // stage the scratch in shared memory
+    P.key = reinterpret_cast<uint64_t*>(dyn_smem);
+    P.val = reinterpret_cast<int64_t*>(P.key + mp);
+    P.E = P.val + mp;
+    P.idx = P.E + 2 * mp;
+    P.T = reinterpret_cast<int32_t*>(P.idx + m);
+  }
   // flatten (w, r) -> global run index g via per-window prefix (small W: linear walk)
   for (int64_t i = threadIdx.x; i < mp; i += blockDim.x) {
     if (i < m) {
@@ -358,7 +379,34 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P) {
   int64_t* perm = P.val;  // reuse
   for (int64_t i = threadIdx.x; i < cp; i += blockDim.x) perm[i] = i < nc ? P.idx[i] : -1;
   __syncthreads();
-  for (int64_t k = 2; k <= cp; k <<= 1) {
+  // Tuples fit a mixed-radix 64-bit key (radix K_w + 1 per window) in all
+  // practical cases; then sort plain keys.  Otherwise compare tuples.
+  __shared__ int use_key_s;
+  if (threadIdx.x == 0) {
+    double bits = 0;
+    for (int w = 0; w < W; ++w) bits += log2((double)P.nruns[w] + 1.0);
+    use_key_s = bits <= 40.0 && nc < (1ll << 24);   // 24 low bits: the segment index tie-break
+  }
+  __syncthreads();
+  bool use_key = use_key_s;
+  if (use_key) {
+    uint64_t* k3 = reinterpret_cast<uint64_t*>(P.key);
+    for (int64_t i = threadIdx.x; i < cp; i += blockDim.x) {
+      if (i < nc) {
+        int64_t sidx = P.idx[i];
+        uint64_t kk = 0;
+        for (int w = 0; w < W; ++w) kk = kk * (uint64_t)(P.nruns[w] + 1) + (uint64_t)P.T[sidx * W + w];
+        k3[i] = (kk << 24) | (uint64_t)i;
+        perm[i] = sidx;
+      } else {
+        k3[i] = ~0ull;
+        perm[i] = -1;
+      }
+    }
+    __syncthreads();
+    bitonic_kv(k3, perm, cp);
+  }
+  for (int64_t k = 2; k <= cp && !use_key; k <<= 1) {
     for (int64_t j = k >> 1; j > 0; j >>= 1) {
       for (int64_t i = threadIdx.x; i < cp; i += blockDim.x) {
         int64_t l = i ^ j;
@@ -377,7 +425,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P) {
     }
   }
   // dense rank of distinct tuples (1-based); write class per segment via key scratch
-  int64_t* rk = reinterpret_cast<int64_t*>(P.key);
+  int64_t* rk = reinterpret_cast<int64_t*>(P.key);   // sort keys are dead here
   for (int64_t i = threadIdx.x; i < nc; i += blockDim.x)
     rk[i] = (i == 0 || tuple_cmp(P.T, perm[i - 1], perm[i], W) != 0) ? 1 : 0;
   __syncthreads();
@@ -398,6 +446,14 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P) {
     P.seg_cls[ci] = (int32_t)P.E[nu + k];
   }
   if (threadIdx.x == 0) { *P.nseg_out = nc; *P.ncls_out = ndist; }
+}
+
+static void win_kernels_init() {
+  static bool done = false;
+  if (done) return;
+  MSG_CUDA(cudaFuncSetAttribute(k_window_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
+  MSG_CUDA(cudaFuncSetAttribute(k_window_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
+  done = true;
 }
 
 // ---------------------------------------------------------------------------
@@ -604,55 +660,74 @@ __device__ __forceinline__ int32_t ms_striped(const int4& v, int k, int lane) {
   switch (lane & 3) { case 0: return a; case 1: return b; case 2: return c; default: return d; }
 }
 
-__global__ void __launch_bounds__(MS_THREADS) k_ms_count(const int32_t* __restrict__ src, int64_t n, SegTab T,
-                                                         int shift, int32_t* __restrict__ hist, int64_t ntiles) {
-  __shared__ MsSmem sm;
-  SegView S = ms_load_table(T, sm);
-  int32_t* h = sm.cnt[0];
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
-  __syncthreads();
-  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-  int64_t wbase = (int64_t)blockIdx.x * MS_TILE + warp * (MS_ITEMS * 32);
-  int4 v[MS_CHUNKS];
-#pragma unroll
-  for (int j = 0; j < MS_CHUNKS; ++j) v[j] = ms_load4(src, wbase + j * MS_CHUNK + 4 * lane, n, aligned);
-#pragma unroll
-  for (int j = 0; j < MS_CHUNKS; ++j) {
-    int64_t cb = wbase + j * MS_CHUNK;
-    if (cb >= n) break;
-    int32_t v0;
-    bool run = ms_is_run(v[j], lane, &v0);
-    int d = (run && cb + MS_CHUNK <= n) ? ms_uniform_digit(S, v0, shift) : -1;
-    if (d >= 0) {
-      if (lane == 0) atomicAdd(&h[d], MS_CHUNK);
-      continue;
+// Digit totals without reading the list: the list holds exactly the resident
+// pages, so the entries of class c are the resident pages of c's segments
+// (popcount of the resident bitmap over the segment) and everything else is
+// class 0.  One warp per segment.  tot[256] accumulates all segment counts.
+__global__ void k_ms_digit_totals(SegTab T, const uint32_t* __restrict__ bits, int shift,
+                                  unsigned long long* tot) {
+  // one CTA per segment (grid-stride): segments are few and long
+  __shared__ unsigned long long red[8];
+  int64_t ns = *T.n;
+  for (int64_t s = blockIdx.x; s < ns; s += gridDim.x) {
+    int64_t lo = T.lo[s], hi = T.hi[s];
+    unsigned long long acc = 0;
+    for (int64_t w = (lo >> 5) + threadIdx.x; w < (hi + 31) >> 5; w += blockDim.x) {
+      int64_t p0 = w << 5;
+      uint32_t m = ~0u;
+      if (p0 < lo) m &= ~0u << (lo - p0);
+      if (p0 + 32 > hi) m &= (hi - p0) >= 32 ? ~0u : ((1u << (hi - p0)) - 1u);
+      acc += __popc(bits[w] & m);
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int32_t x = ms_striped(v[j], k, lane);
-      int dk = cb + k * 32 + lane < n ? (class_of(S, x) >> shift) & 255 : 256;
-      uint32_t peers = __match_any_sync(0xffffffffu, dk);
-      if (dk < 256 && lane == __ffs(peers) - 1) atomicAdd(&h[dk], __popc(peers));
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long t = 0;
+      for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+      if (t) {
+        atomicAdd(&tot[(T.cls[s] >> shift) & 255], t);
+        atomicAdd(&tot[256], t);
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int d = threadIdx.x; d < 256; d += blockDim.x) hist[(int64_t)d * ntiles + blockIdx.x] = h[d];
 }
 
-__global__ void __launch_bounds__(MS_THREADS) k_ms_scatter(const int32_t* __restrict__ src, int64_t n, SegTab T,
-                                                           int shift, const int64_t* __restrict__ goff, int64_t ntiles,
-                                                           int32_t* __restrict__ dst) {
+// Single-pass stable multisplit (decoupled look-back per digit).  Tiles are
+// claimed in order through an atomic counter, each publishes its per-digit
+// counts, looks back for the exclusive prefix, then scatters.  Status words:
+// epoch (16 bits) | flag (2 bits: 1 aggregate, 2 inclusive) | count (46 bits);
+// the epoch makes stale words from earlier passes invisible without clearing.
+struct Onesweep {
+  unsigned long long* status;
+  int32_t* tile_ctr;
+  const unsigned long long* tot;
+  uint32_t epoch;
+};
+
+__device__ __forceinline__ unsigned long long os_pack(uint32_t epoch, uint32_t flag, unsigned long long v) {
+  return ((unsigned long long)epoch << 48) | ((unsigned long long)flag << 46) | v;
+}
+
+__global__ void __launch_bounds__(MS_THREADS) k_ms_onesweep(const int32_t* __restrict__ src, int64_t n, SegTab T,
+                                                            int shift, int32_t* __restrict__ dst, Onesweep O) {
   __shared__ MsSmem sm;
-  SegView S = ms_load_table(T, sm);
+  __shared__ int32_t tile_s;
+  __shared__ int64_t base_s[256];
+  __shared__ int64_t warp_tot_s[MS_THREADS / 32];
+  if (threadIdx.x == 0) tile_s = atomicAdd(O.tile_ctr, 1);
+  SegView S = ms_load_table(T, sm);   // synchronises
+  const int64_t tile = tile_s;
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = lane; i < 256; i += 32) sm.cnt[warp][i] = 0;
   __syncwarp();
   bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-  int64_t wbase = (int64_t)blockIdx.x * MS_TILE + warp * (MS_ITEMS * 32);
+  int64_t wbase = tile * MS_TILE + warp * (MS_ITEMS * 32);
   const uint32_t lt = (1u << lane) - 1u;
   int32_t val[MS_ITEMS];
-  int32_t key[MS_ITEMS];   // digit | (rank within warp & digit) << 9; 256 = invalid
+  int32_t key[MS_ITEMS];
 #pragma unroll
   for (int j = 0; j < MS_CHUNKS; ++j) {
     int64_t cb = wbase + j * MS_CHUNK;
@@ -685,15 +760,54 @@ __global__ void __launch_bounds__(MS_THREADS) k_ms_scatter(const int32_t* __rest
     }
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < 256; d += blockDim.x) {
-    int32_t s = 0;
-    for (int w = 0; w < MS_THREADS / 32; ++w) { int32_t t = sm.cnt[w][d]; sm.cnt[w][d] = s; s += t; }
+  // per digit: exclusive prefix over warps, tile aggregate, decoupled look-back
+  {
+    int d = threadIdx.x;   // MS_THREADS == 256 digits
+    int32_t agg = 0;
+    for (int w = 0; w < MS_THREADS / 32; ++w) { int32_t t = sm.cnt[w][d]; sm.cnt[w][d] = agg; agg += t; }
+    unsigned long long* st = O.status + tile * 256 + d;
+    atomicExch(st, os_pack(O.epoch, tile == 0 ? 2u : 1u, (unsigned long long)agg));
+    // look back 8 predecessors per round (independent loads in flight), summing
+    // aggregates until an inclusive prefix is found
+    unsigned long long prefix = 0;
+    int64_t j = tile - 1;
+    while (j >= 0) {
+      unsigned long long w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        w[k] = j - k >= 0 ? *reinterpret_cast<volatile unsigned long long*>(O.status + (j - k) * 256 + d)
+                          : os_pack(O.epoch, 2u, 0ull);
+      bool done = false;
+      int k = 0;
+      for (; k < 8; ++k) {
+        if ((uint32_t)(w[k] >> 48) != O.epoch || ((w[k] >> 46) & 3) == 0) break;   // not ready: re-poll
+        prefix += w[k] & ((1ull << 46) - 1);
+        if (((w[k] >> 46) & 3) == 2) { done = true; break; }
+      }
+      if (done) break;
+      j -= k;
+    }
+    if (tile > 0) atomicExch(st, os_pack(O.epoch, 2u, prefix + agg));
+    // global base of digit d = entries of all smaller digits
+    unsigned long long td = O.tot[d] + (d == 0 ? (unsigned long long)n - O.tot[256] : 0ull);
+    // exclusive scan of td over the 256 digits (8 warps of 32)
+    unsigned long long x = td;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) warp_tot_s[warp] = (int64_t)x;
+    __syncthreads();
+    int64_t wp = 0;
+    for (int w = 0; w < warp; ++w) wp += warp_tot_s[w];
+    base_s[d] = wp + (int64_t)(x - td) + (int64_t)prefix;
   }
   __syncthreads();
 #pragma unroll
   for (int i = 0; i < MS_ITEMS; ++i) {
     int d = key[i] & 511, r = key[i] >> 9;
-    if (d < 256) dst[goff[(int64_t)d * ntiles + blockIdx.x] + sm.cnt[warp][d] + r] = val[i];
+    if (d < 256) dst[base_s[d] + sm.cnt[warp][d] + r] = val[i];
   }
 }
 
@@ -751,8 +865,15 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
   int64_t n = c.len;
   if (n == 0 || passes <= 0) return;
   int64_t ntiles = (n + MS_TILE - 1) / MS_TILE;
-  c.s.i32a.resize(256 * ntiles, c.st);
-  c.s.i64a.resize(256 * ntiles, c.st);
+  if ((int64_t)c.ms_status.n < 256 * ntiles) {
+    c.ms_status.exact(256 * ntiles);
+    MSG_CUDA(cudaMemsetAsync(c.ms_status.p, 0, 256 * ntiles * 8, c.st));
+    c.ms_epoch = 0;
+  }
+  if (!c.ms_ctr.p) {
+    c.ms_ctr.exact(1 << 16);
+    c.ms_tot.exact(257 * 4);
+  }
   cudaEvent_t e0, e1;
   MSG_CUDA(cudaEventCreate(&e0));
   MSG_CUDA(cudaEventCreate(&e1));
@@ -760,12 +881,18 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
   c.ev_pool.push_back(e1);
   MSG_CUDA(cudaEventRecord(e0, c.st));
   for (int pass = 0; pass < passes; ++pass) {
+    if (++c.ms_epoch >= (1u << 16)) {   // epochs wrap: clear the status words
+      MSG_CUDA(cudaMemsetAsync(c.ms_status.p, 0, c.ms_status.n * 8, c.st));
+      c.ms_epoch = 1;
+    }
+    if (c.ms_epoch == 1) MSG_CUDA(cudaMemsetAsync(c.ms_ctr.p, 0, (1 << 16) * 4, c.st));
     const int32_t* src = c.order[c.cur].p + c.head;
     int32_t* dst = c.order[c.cur ^ 1].p;
-    k_ms_count<<<ntiles, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, c.s.i32a.p, ntiles);
-    MSG_CHECK_LAUNCH();
-    scan_i32_to_i64(c, c.s.i32a.p, 256 * ntiles, c.s.i64a.p);
-    k_ms_scatter<<<ntiles, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, c.s.i64a.p, ntiles, dst);
+    unsigned long long* tot = reinterpret_cast<unsigned long long*>(c.ms_tot.p) + 257 * (pass & 3);
+    MSG_CUDA(cudaMemsetAsync(tot, 0, 257 * 8, c.st));
+    k_ms_digit_totals<<<296, 256, 0, c.st>>>(T, c.bits.p, 8 * pass, tot);
+    Onesweep O{c.ms_status.p, c.ms_ctr.p + c.ms_epoch, tot, c.ms_epoch};
+    k_ms_onesweep<<<ntiles, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, dst, O);
     MSG_CHECK_LAUNCH();
     add_launches(2);
     c.cur ^= 1;
@@ -912,8 +1039,9 @@ static void build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
   o.run_base = rbuf + 3 * off; o.nruns = o.run_base + nwin; o.pages = o.nruns + nwin;
   c.s.i32b.resize(off, st);
   o.run_lab = c.s.i32b.p;
-  k_window_runs<<<nwin, 1024, 0, st>>>(reinterpret_cast<const WinDesc*>(c.s.iv.p),
-                                       c.s.i64a.p, c.s.i64b.p, c.s.i32a.p, o);
+  win_kernels_init();
+  k_window_runs<<<nwin, 1024, kWinSmem, st>>>(reinterpret_cast<const WinDesc*>(c.s.iv.p),
+                                              c.s.i64a.p, c.s.i64b.p, c.s.i32a.p, o, kWinSmem);
   MSG_CHECK_LAUNCH();
   add_launches(1);
   // combine scratch: key[mp] | val[mp] | E[2mp] | idx[2M] | seg_lo[2M] | seg_hi[2M] | nseg | ncls
@@ -939,7 +1067,8 @@ static void build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
   P.seg_cls = c.s.i32c.p;
   P.nseg_out = P.seg_hi + 2 * M;
   P.ncls_out = P.nseg_out + 1;
-  k_window_combine<<<1, 1024, 0, st>>>(P);
+  win_kernels_init();
+  k_window_combine<<<1, 1024, kWinSmem, st>>>(P, kWinSmem);
   MSG_CHECK_LAUNCH();
   add_launches(1);
 }
@@ -1127,7 +1256,8 @@ void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_
   P.seg_cls = c.s.i32c.p;
   P.nseg_out = P.seg_hi + 2 * Mb;
   P.ncls_out = P.nseg_out + 1;
-  k_window_combine<<<1, 1024, 0, st>>>(P);
+  win_kernels_init();
+  k_window_combine<<<1, 1024, kWinSmem, st>>>(P, kWinSmem);
   MSG_CHECK_LAUNCH();
   add_launches(1);
   MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, P.ncls_out, 8, cudaMemcpyDeviceToHost, st));
@@ -1594,7 +1724,8 @@ void window_runs_explicit(Ctx& c, const int64_t* first, const int64_t* end, cons
   o.run_a = rb.p; o.run_b = rb.p + scratch; o.run_d = rb.p + 2 * scratch;
   o.run_base = rb.p + 3 * scratch; o.nruns = o.run_base + 1; o.pages = o.nruns + 1;
   o.run_lab = rl.p;
-  k_window_runs<<<1, 1024, 0, st>>>(d_wd.p, ka.p, va.p, lab.p, o);
+  win_kernels_init();
+  k_window_runs<<<1, 1024, kWinSmem, st>>>(d_wd.p, ka.p, va.p, lab.p, o, kWinSmem);
   MSG_CHECK_LAUNCH();
   add_launches(1);
   int64_t hb[3];

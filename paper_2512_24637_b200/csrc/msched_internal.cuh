@@ -218,6 +218,11 @@ struct Ctx {
   msg_stats stats{};
   // parity dumps
   int debug = 0;   // 1: plan lists, 2: full list orders
+  // single-pass multisplit state
+  DVec<unsigned long long> ms_status;   // 256 per tile, epoch-tagged
+  DVec<int32_t> ms_ctr;                 // tile claim counter per epoch
+  DVec<unsigned long long> ms_tot;      // digit totals (4 x 257)
+  uint32_t ms_epoch = 0;
   std::vector<int64_t> dbg[4];
   ~Ctx();
 };
