@@ -8,7 +8,7 @@ HBM frame arena on the copy engines.  Metric (BASELINE.json): pages
 planned+migrated per second = (populate + evict + fault pages) / replay time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config cfg2|cfg1|cfg4] [--no-migrate]
+                  [--config cfg2|cfg1|cfg3|cfg4] [--page-size B] [--no-migrate]
 
 Multi-GPU: one process per GPU (torchrun), each replaying its own
 independent tenant mix under its own HBM budget (weak scaling, no
@@ -43,26 +43,36 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg4"], default="cfg2")
+    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg3", "cfg4"], default="cfg2")
+    ap.add_argument("--page-size", type=int, default=0, help="config 5: override the page size (bytes)")
     ap.add_argument("--no-migrate", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=3, help="oracle replays in the cpu_baseline sample")
     ap.add_argument("--skip-e2e", action="store_true")
+    ap.add_argument("--skip-plan-only", action="store_true")
     return ap.parse_args()
 
 
-def workload(name, rank):
+def workload(name, rank, page=0):
     from paper_2512_24637_b200 import scenarios
 
     if name == "cfg1":
-        tasks, hw, pol = scenarios.config1_gemm(task_offset=2 * rank)
-        desc = "2x GEMM-chain (32768^3, 8 GEMMs), 16 GiB HBM budget, 2 MiB pages, RR 1.75 ms, proactive/template"
+        tasks, hw, pol = scenarios.config1_gemm(page_size=page or (2 << 20), task_offset=2 * rank)
+        desc = "2x GEMM-chain (32768^3, 8 GEMMs), 16 GiB HBM budget, RR 1.75 ms, proactive/template"
+    elif name == "cfg3":
+        from paper_2512_24637_b200.workload_extra import config3_mixed
+
+        tasks, hw, pol = config3_mixed(hbm_bytes=16 << 30, ratio=2.0, page_size=page or 4096,
+                                       task_offset=4 * rank, timeslice_s=5e-4)
+        desc = ("stencil + SpMV (indirect x) + ResNet-style training + stencil at 2x a 16 GiB budget, "
+                "RR 0.5 ms, proactive/template (faults on the SpMV gathers)")
     elif name == "cfg4":
-        tasks, hw, pol = scenarios.config4_llama70b(task_offset=4 * rank)
-        desc = "4x 70B-class decode (70 GB weights + 5 GB KV, 3 steps), 180 GB HBM budget, 4 KiB pages, RR 5 ms"
+        tasks, hw, pol = scenarios.config4_llama70b(page=page or 4096, task_offset=4 * rank)
+        desc = "4x 70B-class decode (70 GB weights + 5 GB KV, 3 steps), 180 GB HBM budget, RR 5 ms"
     else:
-        tasks, hw, pol = scenarios.config2_llama8b(task_offset=3 * rank)
+        tasks, hw, pol = scenarios.config2_llama8b(page=page or 4096, task_offset=3 * rank)
         desc = ("3x Llama3-8B int8 decode (7.6 GB weights + 0.9 GB KV each, 32 layers, 8 steps), "
-                "16 GiB HBM budget, 4 KiB pages, RR 5 ms, proactive/template predictor")
+                "16 GiB HBM budget, RR 5 ms, proactive/template predictor")
+    desc += f", {hw.page_size_bytes // 1024} KiB pages"
     return tasks, hw, pol, desc
 
 
@@ -187,7 +197,7 @@ def run_reference(args):
             os.sched_setaffinity(0, {rk % os.cpu_count()})
         except Exception:  # noqa: BLE001
             pass
-        tasks, hw, pol, _ = workload(args.config, rk)
+        tasks, hw, pol, _ = workload(args.config, rk, args.page_size)
         times, pages = [], 0
         for i in range(args.warmup + args.steps):
             sim = port.PortSim(tasks, hw, pol, Mode.proactive())
@@ -210,7 +220,7 @@ def run_reference(args):
     ms = max(statistics.mean(t) for t, _ in res) * 1e3
     pages = sum(p for _, p in res)
     value = pages / (ms / 1e3)
-    _, _, _, desc = workload(args.config, 0)
+    _, _, _, desc = workload(args.config, 0, args.page_size)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
@@ -258,7 +268,7 @@ def main():
     from paper_2512_24637_b200 import engine
     from paper_2512_24637_b200.analyzer import build_descriptors
 
-    tasks, hw, pol, desc = workload(args.config, rank)
+    tasks, hw, pol, desc = workload(args.config, rank, args.page_size)
     descs = {t.id: build_descriptors(t) for t in tasks}   # offline analysis: an input, not timed
     peak = link_peak(torch, dev) if rank == 0 else None
     migrate = not args.no_migrate
@@ -318,6 +328,22 @@ def main():
                "d2h_bytes_per_step": int(io[-1][1]), "ms_per_step": e_ms,
                "includes": "host Task objects -> encode -> H2D command tables -> device K1 prediction -> "
                            "replay with real migration -> metrics"}
+    # planning only: the same replay with the copies switched off — the work
+    # the reference itself does (it models migration time, it moves no bytes)
+    plan_only = None
+    if not args.skip_plan_only and migrate:
+        sim.close()
+        sim = engine.Simulator(tasks, hw, pol, engine.Mode.proactive(), migrate=False, device=local,
+                               descriptors=descs)
+        stream = torch.cuda.ExternalStream(sim.ctx.stream(), device=dev)
+        for _ in range(args.warmup):
+            one_step()
+        p_times = [one_step()[0] for _ in range(args.steps)]
+        p_ms = max_over_ranks(torch, statistics.mean(p_times), ws, dev)
+        pst = sim.ctx.stats()
+        plan_only = {"value": pages_step / (p_ms / 1e3), "unit": UNIT, "ms_per_step": p_ms,
+                     "multisplit_ms_per_step": pst["ms_ms"], "planner_ms_per_step": pst["plan_ms"],
+                     "note": "replay with migration off: the reference's own work (plans + modeled timing)"}
     if rank != 0:
         barrier_done = True  # noqa: F841
         sim.close()
@@ -335,6 +361,13 @@ def main():
     except OSError:
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    # DRAM traffic per launch of the dominant kernel from the committed
+    # `ncu --set full` capture (profiles/), when one exists for this config
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "r01", f"traffic_{args.config}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
     achieved = ms_bytes / (ms_kernel_ms * 1e6) if ms_kernel_ms else 0.0
     cpu, cpu_m = cpu_baseline(args, tasks, hw, pol)
     mig = None
@@ -362,11 +395,12 @@ def main():
                    "l2": "flushed between steps (256 MiB write)", "pages_per_step": pages_step},
         "roofline": {"bound": "hbm", "kernel": "reorder multisplit (k_ms_count + scan + k_ms_scatter)",
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak if hbm_peak else None, "traffic": None,
+                     "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": ms_bytes, "avg_launch_ms": ms_kernel_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
         "migration": mig,
         "planner_ms_per_step": st["plan_ms"],
+        "plan_only": plan_only,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),

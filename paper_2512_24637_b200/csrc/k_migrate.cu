@@ -14,6 +14,7 @@
 #include "msched_internal.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace msg {
 
@@ -138,7 +139,8 @@ static void ce_batch(std::vector<void*>& d, std::vector<void*>& s, std::vector<s
   if (d.empty()) return;
   cudaMemcpyAttributes attr = {};
   attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+  static const int overlap_flag = getenv("MSG_CE_NO_OVERLAP_HINT") ? 0 : 1;
+  attr.flags = overlap_flag ? cudaMemcpyFlagPreferOverlapWithCompute : 0;
   size_t idx0 = 0, fail = 0;
   MSG_CUDA(cudaMemcpyBatchAsync(d.data(), s.data(), z.data(), d.size(), &attr, &idx0, 1, &fail, st));
   d.clear(); s.clear(); z.clear();
@@ -223,7 +225,7 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     };
     // evictions, in chunks; each chunk's completion is an event that gates
     // the installs reusing its frames
-    const int kChunks = 8;
+    static const int kChunks = getenv("MSG_MIG_CHUNKS") ? atoi(getenv("MSG_MIG_CHUNKS")) : 8;
     int64_t chunk = std::max<int64_t>((n_d2h + kChunks - 1) / kChunks, 1);
     std::vector<std::pair<int64_t, cudaEvent_t>> done;   // (evictions complete up to, event)
     std::vector<void*> dd, ss;

@@ -715,19 +715,21 @@ __global__ void __launch_bounds__(MS_THREADS) k_ms_onesweep(const int32_t* __res
                                                             int shift, int32_t* __restrict__ dst, Onesweep O) {
   __shared__ MsSmem sm;
   __shared__ int32_t tile_s;
+  __shared__ int32_t hist_s[256];
   __shared__ int64_t base_s[256];
   __shared__ int64_t warp_tot_s[MS_THREADS / 32];
   if (threadIdx.x == 0) tile_s = atomicAdd(O.tile_ctr, 1);
+  hist_s[threadIdx.x] = 0;
   SegView S = ms_load_table(T, sm);   // synchronises
   const int64_t tile = tile_s;
   int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int i = lane; i < 256; i += 32) sm.cnt[warp][i] = 0;
-  __syncwarp();
   bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
   int64_t wbase = tile * MS_TILE + warp * (MS_ITEMS * 32);
   const uint32_t lt = (1u << lane) - 1u;
+  // ---- phase 1: load + classify every entry once; tile histogram
   int32_t val[MS_ITEMS];
-  int32_t key[MS_ITEMS];
+  int32_t dig[MS_ITEMS];   // digit per register slot, 256 = invalid
+  uint32_t fast = 0;       // bit j: chunk j is one run with one digit (slots 4j..4j+3, blocked)
 #pragma unroll
   for (int j = 0; j < MS_CHUNKS; ++j) {
     int64_t cb = wbase + j * MS_CHUNK;
@@ -736,39 +738,60 @@ __global__ void __launch_bounds__(MS_THREADS) k_ms_onesweep(const int32_t* __res
     bool run = ms_is_run(v, lane, &v0);
     int d = (run && cb + MS_CHUNK <= n) ? ms_uniform_digit(S, v0, shift) : -1;
     if (d >= 0) {
-      int32_t before = sm.cnt[warp][d];
-      __syncwarp();
-      if (lane == 0) sm.cnt[warp][d] = before + MS_CHUNK;
-      __syncwarp();
-      int32_t r = before + 4 * lane;
+      fast |= 1u << j;
       val[4 * j] = v.x; val[4 * j + 1] = v.y; val[4 * j + 2] = v.z; val[4 * j + 3] = v.w;
-      key[4 * j] = d | (r << 9); key[4 * j + 1] = d | ((r + 1) << 9);
-      key[4 * j + 2] = d | ((r + 2) << 9); key[4 * j + 3] = d | ((r + 3) << 9);
+      dig[4 * j] = dig[4 * j + 1] = dig[4 * j + 2] = dig[4 * j + 3] = d;
+      if (lane == 0) atomicAdd(&hist_s[d], MS_CHUNK);
       continue;
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
       int32_t x = ms_striped(v, k, lane);
       int dk = cb + k * 32 + lane < n ? (class_of(S, x) >> shift) & 255 : 256;
+      val[4 * j + k] = x;
+      dig[4 * j + k] = dk;
+      uint32_t peers = __match_any_sync(0xffffffffu, dk);
+      if (dk < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist_s[dk], __popc(peers));
+    }
+  }
+  __syncthreads();
+  // ---- publish this tile's aggregate as early as possible
+  const int d = threadIdx.x;   // MS_THREADS == 256 digits
+  const int32_t agg = hist_s[d];
+  unsigned long long* st = O.status + tile * 256 + d;
+  atomicExch(st, os_pack(O.epoch, tile == 0 ? 2u : 1u, (unsigned long long)agg));
+  // ---- phase 2: stable ranking within the tile (overlaps the predecessors' publishing)
+  for (int i = lane; i < 256; i += 32) sm.cnt[warp][i] = 0;
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < MS_CHUNKS; ++j) {
+    if (fast & (1u << j)) {
+      int dj = dig[4 * j];
+      int32_t before = sm.cnt[warp][dj];
+      __syncwarp();
+      if (lane == 0) sm.cnt[warp][dj] = before + MS_CHUNK;
+      __syncwarp();
+      int32_t r = before + 4 * lane;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) dig[4 * j + k] = dj | ((r + k) << 9);
+      continue;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int dk = dig[4 * j + k];
       uint32_t peers = __match_any_sync(0xffffffffu, dk);
       int32_t before = dk < 256 ? sm.cnt[warp][dk] : 0;
       __syncwarp();
       if (dk < 256 && lane == __ffs(peers) - 1) sm.cnt[warp][dk] = before + __popc(peers);
       __syncwarp();
-      val[4 * j + k] = x;
-      key[4 * j + k] = dk | ((before + __popc(peers & lt)) << 9);
+      dig[4 * j + k] = dk | ((before + __popc(peers & lt)) << 9);
     }
   }
   __syncthreads();
-  // per digit: exclusive prefix over warps, tile aggregate, decoupled look-back
+  // ---- phase 3: warp prefix per digit, decoupled look-back, global base
   {
-    int d = threadIdx.x;   // MS_THREADS == 256 digits
-    int32_t agg = 0;
-    for (int w = 0; w < MS_THREADS / 32; ++w) { int32_t t = sm.cnt[w][d]; sm.cnt[w][d] = agg; agg += t; }
-    unsigned long long* st = O.status + tile * 256 + d;
-    atomicExch(st, os_pack(O.epoch, tile == 0 ? 2u : 1u, (unsigned long long)agg));
-    // look back 8 predecessors per round (independent loads in flight), summing
-    // aggregates until an inclusive prefix is found
+    int32_t acc = 0;
+    for (int w = 0; w < MS_THREADS / 32; ++w) { int32_t t = sm.cnt[w][d]; sm.cnt[w][d] = acc; acc += t; }
     unsigned long long prefix = 0;
     int64_t j = tile - 1;
     while (j >= 0) {
@@ -788,9 +811,7 @@ __global__ void __launch_bounds__(MS_THREADS) k_ms_onesweep(const int32_t* __res
       j -= k;
     }
     if (tile > 0) atomicExch(st, os_pack(O.epoch, 2u, prefix + agg));
-    // global base of digit d = entries of all smaller digits
     unsigned long long td = O.tot[d] + (d == 0 ? (unsigned long long)n - O.tot[256] : 0ull);
-    // exclusive scan of td over the 256 digits (8 warps of 32)
     unsigned long long x = td;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
@@ -800,14 +821,15 @@ __global__ void __launch_bounds__(MS_THREADS) k_ms_onesweep(const int32_t* __res
     if (lane == 31) warp_tot_s[warp] = (int64_t)x;
     __syncthreads();
     int64_t wp = 0;
-    for (int w = 0; w < warp; ++w) wp += warp_tot_s[w];
+    for (int w2 = 0; w2 < warp; ++w2) wp += warp_tot_s[w2];
     base_s[d] = wp + (int64_t)(x - td) + (int64_t)prefix;
   }
   __syncthreads();
+  // ---- phase 4: scatter
 #pragma unroll
   for (int i = 0; i < MS_ITEMS; ++i) {
-    int d = key[i] & 511, r = key[i] >> 9;
-    if (d < 256) dst[base_s[d] + sm.cnt[warp][d] + r] = val[i];
+    int dd = dig[i] & 511, r = dig[i] >> 9;
+    if (dd < 256) dst[base_s[dd] + sm.cnt[warp][dd] + r] = val[i];
   }
 }
 
