@@ -711,7 +711,7 @@ __device__ __forceinline__ unsigned long long os_pack(uint32_t epoch, uint32_t f
   return ((unsigned long long)epoch << 48) | ((unsigned long long)flag << 46) | v;
 }
 
-__global__ void __launch_bounds__(MS_THREADS) k_ms_onesweep(const int32_t* __restrict__ src, int64_t n, SegTab T,
+__global__ void __launch_bounds__(MS_THREADS, 4) k_ms_onesweep(const int32_t* __restrict__ src, int64_t n, SegTab T,
                                                             int shift, int32_t* __restrict__ dst, Onesweep O) {
   __shared__ MsSmem sm;
   __shared__ int32_t tile_s;
