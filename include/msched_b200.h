@@ -249,7 +249,10 @@ int msg_list_plan(msg_ctx *ctx, const int64_t *run_first, const int64_t *run_end
 
 /* Parity dumps (the reference's promised but unimplemented SPEC.md:415-416
  * debug dump).  which: 0 list order after the last reorder, 1 last evicted
- * pages (head order), 2 last installed pages (install order). */
+ * pages (head order), 2 last installed pages (install order).  enable is a
+ * bit set: 1 plan dumps, 2 full list orders, 8 run the reorder multisplit on
+ * the look-back (onesweep) kernel instead of the on-chip cooperative one, so
+ * tests cover both. */
 int msg_debug(msg_ctx *ctx, int32_t enable);
 int msg_debug_read(msg_ctx *ctx, int32_t which, int64_t *out, int64_t cap, int64_t *n);
 

@@ -545,21 +545,33 @@ __global__ void k_plan_scalars(const int64_t* total_ptr, DevState* S, int64_t ca
 // Multisplit of the eviction list (the reorder / madvise / remove kernel).
 
 constexpr int MS_THREADS = 256;
-constexpr int MS_ITEMS = 16;
-constexpr int MS_TILE = MS_THREADS * MS_ITEMS;
+constexpr int MS_WARPS = MS_THREADS / 32;
+constexpr int MS_CHUNK = 128;                             // entries per warp step (4 per lane, striped)
+constexpr int MS_CHUNKS = 4;                              // warp steps per tile
+constexpr int MS_ITEMS = MS_CHUNKS * 4;                   // entries per thread per tile
+constexpr int MS_TILE = MS_WARPS * MS_CHUNKS * MS_CHUNK;  // 4096 entries
 constexpr int MS_SMEM_SEGS = 2048;
+constexpr int MS_CTAS_PER_SM = 4;
+constexpr int MS_MAX_PASSES = 4;
 
 struct SegTab {
   const int64_t* lo; const int64_t* hi; const int32_t* cls; const int64_t* n;
 };
 
 // Segment table staged in shared memory as 32-bit dense bounds (dense ids
-// are < 2^31), plus the per-warp digit counters of the ranking pass.
+// are < 2^31), the per-warp digit counters of the ranking, and the per-CTA
+// digit bookkeeping of the look-back.
 struct MsSmem {
   int32_t lo[MS_SMEM_SEGS];
   int32_t hi[MS_SMEM_SEGS];
   int32_t cls[MS_SMEM_SEGS];
-  int32_t cnt[MS_THREADS / 32][256];
+  int32_t cnt[MS_WARPS][256];   // per-warp digit counts, then exclusive warp offsets
+  int64_t gbase[256];           // first output index of each digit (all tiles)
+  int64_t base[256];            // gbase + this tile's look-back prefix
+  int32_t agg[256];             // this tile's digit counts
+  int32_t act[256];             // digits present anywhere in the list
+  int32_t nact;
+  int32_t tile;
 };
 
 struct SegView {
@@ -569,22 +581,35 @@ struct SegView {
   bool small;
 };
 
-// Branchless binary search with a fixed trip count, so the 16 independent
-// lookups of a thread overlap (ILP) instead of serialising on smem latency.
-__device__ __forceinline__ int32_t class_of(const SegView& S, int32_t p) {
+// The interval [ilo, ihi) around page p on which the class is constant (a
+// segment, or the gap between two), and that class.  Branchless binary search
+// with a fixed trip count.
+struct Span { int32_t lo, hi, cls; };
+
+__device__ __forceinline__ Span seg_find(const SegView& S, int32_t p) {
   int32_t pos = 0;
+  Span r;
   if (S.small) {
     for (int32_t step = 1 << S.steps; step > 0; step >>= 1) {
       int32_t q = pos + step;
       if (q <= S.n && S.lo32[q - 1] <= p) pos = q;
     }
-    return (pos > 0 && p < S.hi32[pos - 1]) ? S.cls32[pos - 1] : 0;
+    if (pos > 0 && p < S.hi32[pos - 1]) { r.lo = S.lo32[pos - 1]; r.hi = S.hi32[pos - 1]; r.cls = S.cls32[pos - 1]; }
+    else { r.lo = pos > 0 ? S.hi32[pos - 1] : INT32_MIN; r.hi = pos < S.n ? S.lo32[pos] : INT32_MAX; r.cls = 0; }
+    return r;
   }
   for (int32_t step = 1 << S.steps; step > 0; step >>= 1) {
     int32_t q = pos + step;
     if (q <= S.n && S.lo[q - 1] <= (int64_t)p) pos = q;
   }
-  return (pos > 0 && (int64_t)p < S.hi[pos - 1]) ? S.cls[pos - 1] : 0;
+  if (pos > 0 && (int64_t)p < S.hi[pos - 1]) {
+    r.lo = (int32_t)S.lo[pos - 1]; r.hi = (int32_t)S.hi[pos - 1]; r.cls = S.cls[pos - 1];
+  } else {
+    r.lo = pos > 0 ? (int32_t)S.hi[pos - 1] : INT32_MIN;
+    r.hi = pos < S.n ? (int32_t)S.lo[pos] : INT32_MAX;
+    r.cls = 0;
+  }
+  return r;
 }
 
 __device__ SegView ms_load_table(const SegTab& T, MsSmem& sm) {
@@ -601,72 +626,16 @@ __device__ SegView ms_load_table(const SegTab& T, MsSmem& sm) {
     for (int64_t i = threadIdx.x; i < nn; i += blockDim.x) {
       sm.lo[i] = (int32_t)T.lo[i]; sm.hi[i] = (int32_t)T.hi[i]; sm.cls[i] = T.cls[i];
     }
-  __syncthreads();
   return S;
 }
 
-// The eviction list is made of long runs of consecutive page ids (pages are
-// appended run by run and every multisplit keeps relative order), so a warp
-// reads 128 consecutive list entries with one 16-byte load per lane and, when
-// they form one run inside one class segment (or one gap), classifies all 128
-// with a single lookup.  Anything else takes the per-entry slow path, staged
-// back into array order with shuffles so the ranking stays stable.
-constexpr int MS_CHUNK = 128;                       // entries per warp step
-constexpr int MS_CHUNKS = MS_ITEMS * 32 / MS_CHUNK;  // 4 steps per warp per tile
-
-__device__ __forceinline__ int4 ms_load4(const int32_t* __restrict__ src, int64_t i, int64_t n, bool aligned) {
-  if (aligned && i + 3 < n) return __ldg(reinterpret_cast<const int4*>(src + i));
-  int4 r;
-  r.x = i < n ? __ldg(src + i) : 0;
-  r.y = i + 1 < n ? __ldg(src + i + 1) : 0;
-  r.z = i + 2 < n ? __ldg(src + i + 2) : 0;
-  r.w = i + 3 < n ? __ldg(src + i + 3) : 0;
-  return r;
-}
-
-// Returns the digit shared by the 128-entry chunk [v0, v0+128) when it is one
-// run inside one class segment or one gap, else -1 (warp-uniform).
-__device__ __forceinline__ int ms_uniform_digit(const SegView& S, int32_t v0, int shift) {
-  int32_t pos = 0;
-  if (S.small) {
-    for (int32_t step = 1 << S.steps; step > 0; step >>= 1) {
-      int32_t q = pos + step;
-      if (q <= S.n && S.lo32[q - 1] <= v0) pos = q;
-    }
-    bool in = pos > 0 && v0 < S.hi32[pos - 1];
-    if (in) return v0 + MS_CHUNK - 1 < S.hi32[pos - 1] ? (S.cls32[pos - 1] >> shift) & 255 : -1;
-    return (pos == S.n || S.lo32[pos] > v0 + MS_CHUNK - 1) ? 0 : -1;
-  }
-  for (int32_t step = 1 << S.steps; step > 0; step >>= 1) {
-    int32_t q = pos + step;
-    if (q <= S.n && S.lo[q - 1] <= (int64_t)v0) pos = q;
-  }
-  bool in = pos > 0 && (int64_t)v0 < S.hi[pos - 1];
-  if (in) return (int64_t)v0 + MS_CHUNK - 1 < S.hi[pos - 1] ? (S.cls[pos - 1] >> shift) & 255 : -1;
-  return (pos == S.n || S.lo[pos] > (int64_t)v0 + MS_CHUNK - 1) ? 0 : -1;
-}
-
-__device__ __forceinline__ bool ms_is_run(const int4& v, int lane, int32_t* v0) {
-  *v0 = __shfl_sync(0xffffffffu, v.x, 0);
-  bool ok = v.y == v.x + 1 && v.z == v.x + 2 && v.w == v.x + 3 && v.x == *v0 + 4 * lane;
-  return __all_sync(0xffffffffu, ok);
-}
-
-// element (k*32 + lane) of the chunk, from the blocked int4 registers
-__device__ __forceinline__ int32_t ms_striped(const int4& v, int k, int lane) {
-  int src = k * 8 + (lane >> 2);
-  int32_t a = __shfl_sync(0xffffffffu, v.x, src), b = __shfl_sync(0xffffffffu, v.y, src);
-  int32_t c = __shfl_sync(0xffffffffu, v.z, src), d = __shfl_sync(0xffffffffu, v.w, src);
-  switch (lane & 3) { case 0: return a; case 1: return b; case 2: return c; default: return d; }
-}
-
-// Digit totals without reading the list: the list holds exactly the resident
-// pages, so the entries of class c are the resident pages of c's segments
-// (popcount of the resident bitmap over the segment) and everything else is
-// class 0.  One warp per segment.  tot[256] accumulates all segment counts.
-__global__ void k_ms_digit_totals(SegTab T, const uint32_t* __restrict__ bits, int shift,
+// Digit totals of every pass without reading the list: the list holds
+// exactly the resident pages, so the entries of class c are the resident
+// pages of c's segments (popcount of the resident bitmap over the segment);
+// everything else is class 0.  One CTA per segment (grid-stride).
+// tot[p*257 + d] for pass p, tot[p*257 + 256] = all advised entries.
+__global__ void k_ms_digit_totals(SegTab T, const uint32_t* __restrict__ bits, int passes,
                                   unsigned long long* tot) {
-  // one CTA per segment (grid-stride): segments are few and long
   __shared__ unsigned long long red[8];
   int64_t ns = *T.n;
   for (int64_t s = blockIdx.x; s < ns; s += gridDim.x) {
@@ -677,31 +646,46 @@ __global__ void k_ms_digit_totals(SegTab T, const uint32_t* __restrict__ bits, i
       uint32_t m = ~0u;
       if (p0 < lo) m &= ~0u << (lo - p0);
       if (p0 + 32 > hi) m &= (hi - p0) >= 32 ? ~0u : ((1u << (hi - p0)) - 1u);
-      acc += __popc(bits[w] & m);
+      acc += __popc(__ldg(bits + w) & m);
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < passes) {
       unsigned long long t = 0;
       for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
       if (t) {
-        atomicAdd(&tot[(T.cls[s] >> shift) & 255], t);
-        atomicAdd(&tot[256], t);
+        int p = threadIdx.x;
+        atomicAdd(&tot[p * 257 + ((T.cls[s] >> (8 * p)) & 255)], t);
+        atomicAdd(&tot[p * 257 + 256], t);
       }
     }
     __syncthreads();
   }
 }
 
-// Single-pass stable multisplit (decoupled look-back per digit).  Tiles are
-// claimed in order through an atomic counter, each publishes its per-digit
-// counts, looks back for the exclusive prefix, then scatters.  Status words:
-// epoch (16 bits) | flag (2 bits: 1 aggregate, 2 inclusive) | count (46 bits);
-// the epoch makes stale words from earlier passes invisible without clearing.
+// Single-pass stable multisplit with decoupled look-back, persistent CTAs.
+//
+// Tiles of 4096 list entries are claimed in order through an atomic counter.
+// A warp owns 4 consecutive 128-entry chunks of its tile and reads each with
+// four coalesced 128-byte loads (entry lane + 32k).  The eviction list is
+// made of long runs of consecutive page ids (pages are appended run by run,
+// and every multisplit keeps relative order), so a chunk that is one run
+// inside one constant-class interval is classified with one check against
+// the warp's cached interval — no search, no per-entry work — and later
+// written back as four coalesced stores of computed ids.  Anything else takes
+// the per-entry path (ranked with match_any in array order, so the split is
+// stable).
+//
+// Look-back: status[d * stride + tile] = epoch (16) | flag (2: 1 aggregate,
+// 2 inclusive) | count (46).  Only digits present in the list take part (the
+// digit totals are known up front); one warp resolves a digit 32 predecessor
+// tiles at a time with one coalesced load.  The epoch makes stale words from
+// earlier passes invisible without clearing.
 struct Onesweep {
   unsigned long long* status;
+  int64_t stride;               // tiles per digit row
   int32_t* tile_ctr;
   const unsigned long long* tot;
   uint32_t epoch;
@@ -711,106 +695,16 @@ __device__ __forceinline__ unsigned long long os_pack(uint32_t epoch, uint32_t f
   return ((unsigned long long)epoch << 48) | ((unsigned long long)flag << 46) | v;
 }
 
-__global__ void __launch_bounds__(MS_THREADS, 4) k_ms_onesweep(const int32_t* __restrict__ src, int64_t n, SegTab T,
-                                                            int shift, int32_t* __restrict__ dst, Onesweep O) {
+__global__ void __launch_bounds__(MS_THREADS, MS_CTAS_PER_SM)
+k_ms_onesweep(const int32_t* __restrict__ src, int64_t n, SegTab T, int shift, int32_t* __restrict__ dst,
+              Onesweep O) {
   __shared__ MsSmem sm;
-  __shared__ int32_t tile_s;
-  __shared__ int32_t hist_s[256];
-  __shared__ int64_t base_s[256];
-  __shared__ int64_t warp_tot_s[MS_THREADS / 32];
-  if (threadIdx.x == 0) tile_s = atomicAdd(O.tile_ctr, 1);
-  hist_s[threadIdx.x] = 0;
-  SegView S = ms_load_table(T, sm);   // synchronises
-  const int64_t tile = tile_s;
-  int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  bool aligned = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
-  int64_t wbase = tile * MS_TILE + warp * (MS_ITEMS * 32);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  // ---- phase 1: load + classify every entry once; tile histogram
-  int32_t val[MS_ITEMS];
-  int32_t dig[MS_ITEMS];   // digit per register slot, 256 = invalid
-  uint32_t fast = 0;       // bit j: chunk j is one run with one digit (slots 4j..4j+3, blocked)
-#pragma unroll
-  for (int j = 0; j < MS_CHUNKS; ++j) {
-    int64_t cb = wbase + j * MS_CHUNK;
-    int4 v = ms_load4(src, cb + 4 * lane, n, aligned);
-    int32_t v0;
-    bool run = ms_is_run(v, lane, &v0);
-    int d = (run && cb + MS_CHUNK <= n) ? ms_uniform_digit(S, v0, shift) : -1;
-    if (d >= 0) {
-      fast |= 1u << j;
-      val[4 * j] = v.x; val[4 * j + 1] = v.y; val[4 * j + 2] = v.z; val[4 * j + 3] = v.w;
-      dig[4 * j] = dig[4 * j + 1] = dig[4 * j + 2] = dig[4 * j + 3] = d;
-      if (lane == 0) atomicAdd(&hist_s[d], MS_CHUNK);
-      continue;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int32_t x = ms_striped(v, k, lane);
-      int dk = cb + k * 32 + lane < n ? (class_of(S, x) >> shift) & 255 : 256;
-      val[4 * j + k] = x;
-      dig[4 * j + k] = dk;
-      uint32_t peers = __match_any_sync(0xffffffffu, dk);
-      if (dk < 256 && lane == __ffs(peers) - 1) atomicAdd(&hist_s[dk], __popc(peers));
-    }
-  }
-  __syncthreads();
-  // ---- publish this tile's aggregate as early as possible
-  const int d = threadIdx.x;   // MS_THREADS == 256 digits
-  const int32_t agg = hist_s[d];
-  unsigned long long* st = O.status + tile * 256 + d;
-  atomicExch(st, os_pack(O.epoch, tile == 0 ? 2u : 1u, (unsigned long long)agg));
-  // ---- phase 2: stable ranking within the tile (overlaps the predecessors' publishing)
-  for (int i = lane; i < 256; i += 32) sm.cnt[warp][i] = 0;
-  __syncwarp();
-#pragma unroll
-  for (int j = 0; j < MS_CHUNKS; ++j) {
-    if (fast & (1u << j)) {
-      int dj = dig[4 * j];
-      int32_t before = sm.cnt[warp][dj];
-      __syncwarp();
-      if (lane == 0) sm.cnt[warp][dj] = before + MS_CHUNK;
-      __syncwarp();
-      int32_t r = before + 4 * lane;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) dig[4 * j + k] = dj | ((r + k) << 9);
-      continue;
-    }
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int dk = dig[4 * j + k];
-      uint32_t peers = __match_any_sync(0xffffffffu, dk);
-      int32_t before = dk < 256 ? sm.cnt[warp][dk] : 0;
-      __syncwarp();
-      if (dk < 256 && lane == __ffs(peers) - 1) sm.cnt[warp][dk] = before + __popc(peers);
-      __syncwarp();
-      dig[4 * j + k] = dk | ((before + __popc(peers & lt)) << 9);
-    }
-  }
-  __syncthreads();
-  // ---- phase 3: warp prefix per digit, decoupled look-back, global base
+  SegView S = ms_load_table(T, sm);
+  // digit totals -> global digit bases and the list of present digits
   {
-    int32_t acc = 0;
-    for (int w = 0; w < MS_THREADS / 32; ++w) { int32_t t = sm.cnt[w][d]; sm.cnt[w][d] = acc; acc += t; }
-    unsigned long long prefix = 0;
-    int64_t j = tile - 1;
-    while (j >= 0) {
-      unsigned long long w[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k)
-        w[k] = j - k >= 0 ? *reinterpret_cast<volatile unsigned long long*>(O.status + (j - k) * 256 + d)
-                          : os_pack(O.epoch, 2u, 0ull);
-      bool done = false;
-      int k = 0;
-      for (; k < 8; ++k) {
-        if ((uint32_t)(w[k] >> 48) != O.epoch || ((w[k] >> 46) & 3) == 0) break;   // not ready: re-poll
-        prefix += w[k] & ((1ull << 46) - 1);
-        if (((w[k] >> 46) & 3) == 2) { done = true; break; }
-      }
-      if (done) break;
-      j -= k;
-    }
-    if (tile > 0) atomicExch(st, os_pack(O.epoch, 2u, prefix + agg));
+    const int d = tid;
     unsigned long long td = O.tot[d] + (d == 0 ? (unsigned long long)n - O.tot[256] : 0ull);
     unsigned long long x = td;
 #pragma unroll
@@ -818,18 +712,380 @@ __global__ void __launch_bounds__(MS_THREADS, 4) k_ms_onesweep(const int32_t* __
       unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
       if (lane >= o) x += y;
     }
-    if (lane == 31) warp_tot_s[warp] = (int64_t)x;
+    uint32_t present = __ballot_sync(0xffffffffu, td != 0);
+    if (lane == 31) { sm.gbase[warp] = (int64_t)x; sm.agg[warp] = __popc(present); }
     __syncthreads();
     int64_t wp = 0;
-    for (int w2 = 0; w2 < warp; ++w2) wp += warp_tot_s[w2];
-    base_s[d] = wp + (int64_t)(x - td) + (int64_t)prefix;
+    int32_t ap = 0;
+    for (int w = 0; w < warp; ++w) { wp += sm.gbase[w]; ap += sm.agg[w]; }
+    __syncthreads();
+    sm.gbase[d] = wp + (int64_t)(x - td);
+    if (td) sm.act[ap + __popc(present & lt)] = d;
+    if (d == MS_THREADS - 1) sm.nact = ap + __popc(present);
+  }
+  const int64_t ntiles = (n + MS_TILE - 1) / MS_TILE;
+  int32_t c_lo = 1, c_hi = 0, c_d = 0;   // warp's cached constant-class interval
+  for (;;) {
+    if (tid == 0) sm.tile = atomicAdd(O.tile_ctr, 1);
+    for (int i = lane; i < 256; i += 32) sm.cnt[warp][i] = 0;
+    __syncthreads();
+    const int64_t tile = sm.tile;
+    if (tile >= ntiles) break;
+    const int64_t wbase = tile * MS_TILE + warp * (MS_CHUNKS * MS_CHUNK);
+    // ---- phase 1: load, classify and rank (per warp, in array order)
+    int32_t val[MS_ITEMS];
+    int32_t dig[MS_ITEMS];   // digit | rank-within-warp << 9; digit 256 = past the end
+    uint32_t fast = 0;       // bit j: chunk j is one run of one digit (val[4j] = first id)
+#pragma unroll
+    for (int j = 0; j < MS_CHUNKS; ++j) {
+      const int64_t cb = wbase + j * MS_CHUNK;
+      int32_t x[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int64_t i = cb + 32 * k + lane;
+        x[k] = i < n ? __ldg(src + i) : 0;
+      }
+      const int32_t v0 = __shfl_sync(0xffffffffu, x[0], 0);
+      bool ok = cb + MS_CHUNK <= n;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ok = ok && x[k] == v0 + 32 * k + lane;
+      int d = -1;
+      if (__all_sync(0xffffffffu, ok)) {
+        if (!(v0 >= c_lo && v0 + (MS_CHUNK - 1) < c_hi)) {
+          Span s = seg_find(S, v0);
+          c_lo = s.lo; c_hi = s.hi; c_d = (s.cls >> shift) & 255;
+        }
+        if (v0 + (MS_CHUNK - 1) < c_hi) d = c_d;
+      }
+      if (d >= 0) {
+        fast |= 1u << j;
+        int32_t before = sm.cnt[warp][d];
+        __syncwarp();
+        if (lane == 0) sm.cnt[warp][d] = before + MS_CHUNK;
+        __syncwarp();
+        val[4 * j] = v0;
+        dig[4 * j] = d | (before << 9);
+        continue;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int dk = 256;
+        if (cb + 32 * k + lane < n) {
+          if (x[k] >= c_lo && x[k] < c_hi) dk = c_d;
+          else dk = (seg_find(S, x[k]).cls >> shift) & 255;
+        }
+        uint32_t peers = __match_any_sync(0xffffffffu, dk);
+        int32_t before = dk < 256 ? sm.cnt[warp][dk] : 0;
+        __syncwarp();
+        if (dk < 256 && lane == __ffs(peers) - 1) sm.cnt[warp][dk] = before + __popc(peers);
+        __syncwarp();
+        val[4 * j + k] = x[k];
+        dig[4 * j + k] = dk | ((before + __popc(peers & lt)) << 9);
+      }
+    }
+    __syncthreads();
+    // ---- tile aggregate per digit; exclusive warp offsets; publish
+    {
+      const int d = tid;
+      int32_t acc = 0;
+#pragma unroll
+      for (int w = 0; w < MS_WARPS; ++w) { int32_t t = sm.cnt[w][d]; sm.cnt[w][d] = acc; acc += t; }
+      sm.agg[d] = acc;
+      if (O.tot[d] + (d == 0 ? (unsigned long long)n - O.tot[256] : 0ull))
+        atomicExch(O.status + d * O.stride + tile, os_pack(O.epoch, tile == 0 ? 2u : 1u, (unsigned long long)acc));
+    }
+    __syncthreads();
+    // ---- decoupled look-back: one warp per present digit, 32 tiles per step
+    for (int a = warp; a < sm.nact; a += MS_WARPS) {
+      const int d = sm.act[a];
+      const unsigned long long* row = O.status + d * O.stride;
+      unsigned long long prefix = 0;
+      int64_t j = tile - 1;
+      while (j >= 0) {
+        int64_t t = j - lane;
+        unsigned long long w = t >= 0 ? *reinterpret_cast<const volatile unsigned long long*>(row + t)
+                                      : os_pack(O.epoch, 2u, 0ull);
+        bool ready = (uint32_t)(w >> 48) == O.epoch && ((w >> 46) & 3) != 0;
+        uint32_t nr = __ballot_sync(0xffffffffu, !ready);
+        uint32_t inc = __ballot_sync(0xffffffffu, ready && ((w >> 46) & 3) == 2);
+        int lim = nr ? __ffs(nr) - 1 : 32;      // lanes [0, lim) are ready
+        int fi = inc ? __ffs(inc) - 1 : 32;     // nearest inclusive
+        int take = fi < lim ? fi + 1 : lim;
+        unsigned long long v = lane < take ? (w & ((1ull << 46) - 1)) : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (fi < lim) break;
+        j -= take;
+      }
+      if (lane == 0) {
+        if (tile > 0) atomicExch(O.status + d * O.stride + tile, os_pack(O.epoch, 2u, prefix + sm.agg[d]));
+        sm.base[d] = sm.gbase[d] + (int64_t)prefix;
+      }
+    }
+    __syncthreads();
+    // ---- scatter
+#pragma unroll
+    for (int j = 0; j < MS_CHUNKS; ++j) {
+      if (fast & (1u << j)) {
+        const int d = dig[4 * j] & 511;
+        int64_t p = sm.base[d] + sm.cnt[warp][d] + (dig[4 * j] >> 9) + lane;
+        const int32_t v = val[4 * j] + lane;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dst[p + 32 * k] = v + 32 * k;
+        continue;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int dd = dig[4 * j + k] & 511, r = dig[4 * j + k] >> 9;
+        if (dd < 256) dst[sm.base[dd] + sm.cnt[warp][dd] + r] = val[4 * j + k];
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// On-chip multisplit (one cooperative launch per pass, one grid barrier).
+//
+// One 1024-thread CTA per SM owns a contiguous slice of the list; each of its
+// 32 warps owns a contiguous run of 128-entry chunks inside it.  Phase 1
+// reads every entry once (four coalesced 128-byte loads per chunk per warp),
+// classifies chunks — a chunk that is one run of consecutive ids inside one
+// constant-class interval is recorded as (first id, digit) and never read
+// again — and counts digits per warp; entries of the other chunks are kept in
+// shared memory (or re-read later if the slice is larger than the cache).
+// The CTA's digit histogram goes to global memory; after the grid barrier
+// every CTA reads the whole histogram matrix (148 x 256 counters, from L2) to
+// get its digit bases, so no look-back and no separate totals kernel exist.
+// Phase 3 replays the chunks in the same order and writes: run chunks as
+// computed ids with coalesced stores, the others ranked with match_any in
+// array order (stable).  Traffic: 4 B read + 4 B written per entry.
+constexpr int MC_THREADS = 1024;
+constexpr int MC_WARPS = MC_THREADS / 32;
+constexpr int MC_SMEM = 224 * 1024;
+constexpr int MC_FIXED = 3 * MS_SMEM_SEGS * 4 + MC_WARPS * 256 * 4 + 256 * 8 + 2 * 4 * 256 * 4 + 64 + 8 + 16;
+
+struct McArgs {
+  const int32_t* src; int64_t n; SegTab T; int shift; int32_t* dst;
+  int32_t* hist;       // [gridDim.x][256] per-CTA digit counts
+  int32_t* bar;        // grid barrier counter (zero at launch)
+  int64_t E;           // entries per CTA (multiple of 128)
+  int32_t vcap;        // entries per CTA kept in shared memory
+  int32_t nch_cap;     // chunk records per CTA
+};
+
+// TMA bulk copy global -> shared, completion counted on an mbarrier.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "MBAR_WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+
+__device__ __forceinline__ void grid_barrier(int32_t* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(bar, 1);
+    while (*reinterpret_cast<volatile int32_t*>(bar) < (int32_t)gridDim.x) __nanosleep(64);
+    __threadfence();
   }
   __syncthreads();
-  // ---- phase 4: scatter
+}
+
+__device__ __forceinline__ int ms_digit(const SegView& S, int32_t x, int32_t c_lo, int32_t c_hi, int c_d, int shift) {
+  if (x >= c_lo && x < c_hi) return c_d;
+  return (seg_find(S, x).cls >> shift) & 255;
+}
+
+__global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
+  extern __shared__ __align__(16) unsigned char mc_raw[];
+  int32_t* lo32 = reinterpret_cast<int32_t*>(mc_raw);
+  int32_t* hi32 = lo32 + MS_SMEM_SEGS;
+  int32_t* cls32 = hi32 + MS_SMEM_SEGS;
+  int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(cls32 + MS_SMEM_SEGS);
+  int64_t* base = reinterpret_cast<int64_t*>(cnt + MC_WARPS);
+  int32_t* red = reinterpret_cast<int32_t*>(base + 256);          // [2][4][256]
+  int64_t* misc = reinterpret_cast<int64_t*>(red + 2 * 4 * 256);  // 8 x int64: warp totals; [7] = mbarrier
+  int2* info = reinterpret_cast<int2*>(misc + 8);                 // nch_cap chunk records
+  int32_t* cache = reinterpret_cast<int32_t*>(info + ((A.nch_cap + 1) & ~1));   // 16-B aligned, vcap + 4
+  uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 7);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int shift = A.shift;
+  const int64_t r0 = (int64_t)blockIdx.x * A.E;
+  const int64_t r1 = r0 + A.E < A.n ? r0 + A.E : A.n;
+  const int64_t len = r1 > r0 ? r1 - r0 : 0;
+  // stage the first m entries of the slice in shared memory with one TMA bulk
+  // copy (16-byte aligned window; entry i lands at cache[delta + i])
+  const int64_t m = len < A.vcap ? len : A.vcap;
+  const uintptr_t g0 = reinterpret_cast<uintptr_t>(A.src + r0);
+  const int32_t delta = (int32_t)((g0 & 15) >> 2);
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    if (m > 0) {
+      uintptr_t gs = g0 & ~uintptr_t(15);
+      uintptr_t ge = (reinterpret_cast<uintptr_t>(A.src + r0 + m) + 15) & ~uintptr_t(15);
+      uint32_t bytes = (uint32_t)(ge - gs);
+      mbar_expect_tx(bar, bytes);
+      tma_bulk_g2s(cache, reinterpret_cast<const void*>(gs), bytes, bar);
+    }
+  }
+  // class table -> smem while the copy is in flight
+  SegView S;
+  {
+    int64_t nn = *A.T.n;
+    S.n = (int32_t)nn;
+    S.steps = nn > 1 ? 64 - __clzll(nn - 1) : 0;
+    S.small = nn <= MS_SMEM_SEGS;
+    S.lo = A.T.lo; S.hi = A.T.hi; S.cls = A.T.cls;
+    S.lo32 = lo32; S.hi32 = hi32; S.cls32 = cls32;
+    if (S.small)
+      for (int64_t i = tid; i < nn; i += MC_THREADS) {
+        lo32[i] = (int32_t)A.T.lo[i]; hi32[i] = (int32_t)A.T.hi[i]; cls32[i] = A.T.cls[i];
+      }
+  }
+  for (int i = lane; i < 256; i += 32) cnt[warp][i] = 0;
+  __syncthreads();
+  if (m > 0) mbar_wait(bar, 0);
+  const int32_t nch = (int32_t)((len + MS_CHUNK - 1) / MS_CHUNK);
+  const int32_t ch0 = (int32_t)((int64_t)nch * warp / MC_WARPS);
+  const int32_t ch1 = (int32_t)((int64_t)nch * (warp + 1) / MC_WARPS);
+  int32_t c_lo = 1, c_hi = 0, c_d = 0;   // the warp's cached constant-class interval
+  // ---- phase 1: classify and count
+  for (int32_t ch = ch0; ch < ch1; ++ch) {
+    const int64_t cb = r0 + (int64_t)ch * MS_CHUNK;
+    int32_t x[4];
 #pragma unroll
-  for (int i = 0; i < MS_ITEMS; ++i) {
-    int dd = dig[i] & 511, r = dig[i] >> 9;
-    if (dd < 256) dst[base_s[dd] + sm.cnt[warp][dd] + r] = val[i];
+    for (int k = 0; k < 4; ++k) {
+      const int32_t off = ch * MS_CHUNK + 32 * k + lane;
+      const int64_t i = cb + 32 * k + lane;
+      x[k] = i < r1 ? (off < m ? cache[delta + off] : __ldcs(A.src + i)) : 0;
+    }
+    const int32_t v0 = __shfl_sync(0xffffffffu, x[0], 0);
+    bool ok = cb + MS_CHUNK <= r1;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) ok = ok && x[k] == v0 + 32 * k + lane;
+    int d = -1;
+    if (__all_sync(0xffffffffu, ok)) {
+      if (!(v0 >= c_lo && v0 + (MS_CHUNK - 1) < c_hi)) {
+        Span sp = seg_find(S, v0);
+        c_lo = sp.lo; c_hi = sp.hi; c_d = (sp.cls >> shift) & 255;
+      }
+      if (v0 + (MS_CHUNK - 1) < c_hi) d = c_d;
+    }
+    if (d >= 0) {
+      if (lane == 0) { info[ch] = make_int2(v0, d); cnt[warp][d] += MS_CHUNK; }
+      __syncwarp();
+      continue;
+    }
+    if (lane == 0) info[ch] = make_int2(0, -1);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      int dk = cb + 32 * k + lane < r1 ? ms_digit(S, x[k], c_lo, c_hi, c_d, shift) : 256;
+      uint32_t peers = __match_any_sync(0xffffffffu, dk);
+      if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] += __popc(peers);
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  // ---- CTA histogram; exclusive warp offsets
+  if (tid < 256) {
+    int32_t acc = 0;
+#pragma unroll 8
+    for (int w = 0; w < MC_WARPS; ++w) { int32_t t = cnt[w][tid]; cnt[w][tid] = acc; acc += t; }
+    __stcg(A.hist + (int64_t)blockIdx.x * 256 + tid, acc);
+  }
+  grid_barrier(A.bar);
+  // ---- phase 2: digit bases from the histogram matrix (prefix over CTAs + digit totals)
+  {
+    const int d = tid & 255, g = tid >> 8;
+    const int G = (int)gridDim.x, me = (int)blockIdx.x;
+    int32_t pre = 0, all = 0;
+    for (int c0 = g; c0 < G; c0 += 64) {
+      int32_t v[16];
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        int c = c0 + 4 * u;
+        v[u] = c < G ? __ldcg(A.hist + (int64_t)c * 256 + d) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        all += v[u];
+        if (c0 + 4 * u < me) pre += v[u];
+      }
+    }
+    red[g * 256 + d] = pre;
+    red[1024 + g * 256 + d] = all;
+  }
+  __syncthreads();
+  {
+    int64_t pre = 0, tot = 0, x = 0;
+    if (tid < 256) {
+      pre = (int64_t)red[tid] + red[256 + tid] + red[512 + tid] + red[768 + tid];
+      tot = (int64_t)red[1024 + tid] + red[1280 + tid] + red[1536 + tid] + red[1792 + tid];
+      x = tot;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) misc[warp] = x;
+    }
+    __syncthreads();
+    if (tid < 256) {
+      int64_t wp = 0;
+      for (int w = 0; w < warp; ++w) wp += misc[w];
+      base[tid] = wp + (x - tot) + pre;
+    }
+  }
+  __syncthreads();
+  // ---- phase 3: replay the chunks in order and scatter
+  for (int32_t ch = ch0; ch < ch1; ++ch) {
+    const int64_t cb = r0 + (int64_t)ch * MS_CHUNK;
+    const int2 rec = info[ch];
+    if (rec.y >= 0) {
+      const int d = rec.y;
+      const int32_t before = cnt[warp][d];
+      const int64_t p = base[d] + before + lane;
+      const int32_t v = rec.x + lane;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) A.dst[p + 32 * k] = v + 32 * k;
+      __syncwarp();
+      if (lane == 0) cnt[warp][d] = before + MS_CHUNK;
+      __syncwarp();
+      continue;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int32_t off = ch * MS_CHUNK + 32 * k + lane;
+      const int64_t i = cb + 32 * k + lane;
+      int32_t xv = 0;
+      if (i < r1) xv = off < m ? cache[delta + off] : __ldcs(A.src + i);
+      int dk = i < r1 ? ms_digit(S, xv, c_lo, c_hi, c_d, shift) : 256;
+      uint32_t peers = __match_any_sync(0xffffffffu, dk);
+      int32_t before = dk < 256 ? cnt[warp][dk] : 0;
+      __syncwarp();
+      if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] = before + __popc(peers);
+      __syncwarp();
+      if (dk < 256) A.dst[base[dk] + before + __popc(peers & lt)] = xv;
+    }
   }
 }
 
@@ -886,6 +1142,7 @@ void scan_flags(Ctx& c, const int32_t* in, int64_t n, int64_t* out) { scan_i32_t
 static void multisplit(Ctx& c, const SegTab& T, int passes) {
   int64_t n = c.len;
   if (n == 0 || passes <= 0) return;
+  if (passes > MS_MAX_PASSES) throw Error(MSG_E_INVAL, "too many reorder classes");
   int64_t ntiles = (n + MS_TILE - 1) / MS_TILE;
   if ((int64_t)c.ms_status.n < 256 * ntiles) {
     c.ms_status.exact(256 * ntiles);
@@ -894,14 +1151,43 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
   }
   if (!c.ms_ctr.p) {
     c.ms_ctr.exact(1 << 16);
-    c.ms_tot.exact(257 * 4);
+    c.ms_tot.exact(257 * MS_MAX_PASSES);
   }
+  static int grid_cap = 0, coop_grid = 0;
+  if (!grid_cap) {
+    int per_sm = 0, sms = 0, coop_per_sm = 0;
+    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ms_onesweep, MS_THREADS, 0));
+    MSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    MSG_CUDA(cudaFuncSetAttribute(k_ms_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MC_SMEM));
+    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&coop_per_sm, k_ms_coop, MC_THREADS, MC_SMEM));
+    grid_cap = std::max(1, per_sm) * std::max(1, sms);
+    coop_grid = coop_per_sm * sms;
+  }
+  // on-chip cooperative path when every CTA's chunk records fit in shared memory
+  int64_t E = 0, vcap = -1, nch = 0;
+  if (coop_grid > 0) {
+    E = (n + coop_grid - 1) / coop_grid;
+    E = (E + MS_CHUNK - 1) / MS_CHUNK * MS_CHUNK;
+    nch = E / MS_CHUNK;
+    vcap = ((int64_t)MC_SMEM - MC_FIXED - 8 * nch) / 4 - 8;   // + 4 alignment slack entries
+    vcap = std::min<int64_t>(vcap, E) & ~int64_t(31);
+  }
+  const bool coop = vcap >= 0 && !(c.debug & 8);
   cudaEvent_t e0, e1;
   MSG_CUDA(cudaEventCreate(&e0));
   MSG_CUDA(cudaEventCreate(&e1));
   c.ev_pool.push_back(e0);
   c.ev_pool.push_back(e1);
   MSG_CUDA(cudaEventRecord(e0, c.st));
+  unsigned long long* tot = c.ms_tot.p;
+  if (!coop) {
+    // digit totals of all passes from the resident bitmap (one launch)
+    MSG_CUDA(cudaMemsetAsync(tot, 0, 257 * passes * 8, c.st));
+    k_ms_digit_totals<<<296, 256, 0, c.st>>>(T, c.bits.p, passes, tot);
+    add_launches(1);
+  } else if ((int64_t)c.ms_hist.n < 256 * (int64_t)coop_grid) {
+    c.ms_hist.exact(256 * (int64_t)coop_grid);
+  }
   for (int pass = 0; pass < passes; ++pass) {
     if (++c.ms_epoch >= (1u << 16)) {   // epochs wrap: clear the status words
       MSG_CUDA(cudaMemsetAsync(c.ms_status.p, 0, c.ms_status.n * 8, c.st));
@@ -910,13 +1196,19 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     if (c.ms_epoch == 1) MSG_CUDA(cudaMemsetAsync(c.ms_ctr.p, 0, (1 << 16) * 4, c.st));
     const int32_t* src = c.order[c.cur].p + c.head;
     int32_t* dst = c.order[c.cur ^ 1].p;
-    unsigned long long* tot = reinterpret_cast<unsigned long long*>(c.ms_tot.p) + 257 * (pass & 3);
-    MSG_CUDA(cudaMemsetAsync(tot, 0, 257 * 8, c.st));
-    k_ms_digit_totals<<<296, 256, 0, c.st>>>(T, c.bits.p, 8 * pass, tot);
-    Onesweep O{c.ms_status.p, c.ms_ctr.p + c.ms_epoch, tot, c.ms_epoch};
-    k_ms_onesweep<<<ntiles, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, dst, O);
+    if (coop) {
+      McArgs A{src, n, T, 8 * pass, dst, c.ms_hist.p, c.ms_ctr.p + c.ms_epoch, E, (int32_t)vcap, (int32_t)nch};
+      void* args[] = {&A};
+      MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS),
+                                           args, MC_SMEM, c.st));
+    } else {
+      Onesweep O{c.ms_status.p, (int64_t)(c.ms_status.n / 256), c.ms_ctr.p + c.ms_epoch, tot + 257 * pass,
+                 c.ms_epoch};
+      int grid = (int)std::min<int64_t>(ntiles, grid_cap);
+      k_ms_onesweep<<<grid, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, dst, O);
+    }
     MSG_CHECK_LAUNCH();
-    add_launches(2);
+    add_launches(1);
     c.cur ^= 1;
     c.head = 0;
   }
@@ -1388,7 +1680,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     poplist.resize(std::max<int64_t>(pop, 1), st);
     if (pop) units_fill(c, R, c.s.uofs.p, &c.dstate->populate, poplist.p);
     int64_t* mig = mig_buf(c, ev + pop);
-    if (c.debug) {
+    if (c.debug & 3) {
       dump_dense(c, c.order[c.cur].p + c.head, ev, c.dbg[1]);
       dump_dense(c, poplist.p, pop, c.dbg[2]);
     }
@@ -1436,11 +1728,11 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
       if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     }
     ev_done = std::min(evict, c.len);
-    if (c.debug) dump_dense(c, c.order[c.cur].p + c.head, ev_done, c.dbg[1]);
+    if (c.debug & 3) dump_dense(c, c.order[c.cur].p + c.head, ev_done, c.dbg[1]);
     evict_head_n(c, ev_done, mig);
     out->evicted = ev_done;
   }
-  if (c.debug) {
+  if (c.debug & 3) {
     if (evict <= 0) c.dbg[1].clear();
     dump_dense(c, c.s.miss.p, n, c.dbg[2]);
   }
@@ -1685,7 +1977,7 @@ void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out
       int64_t over = c.len + n - c.C;
       touch_slow(c, task, cmd, over > 0 ? over : 0, nullptr, 0, cmd + 1, t.kind[cmd] == MSG_CMD_H2D, &o, nullptr);
       evicted_out[cmd - c0] = o.evicted;
-      if (c.debug) {  // [cmd, nmiss, miss..., nev, ev...] per faulting command
+      if (c.debug & 3) {  // [cmd, nmiss, miss..., nev, ev...] per faulting command
         auto& u = c.dbg[3];
         u.push_back(cmd);
         u.push_back((int64_t)c.dbg[2].size());

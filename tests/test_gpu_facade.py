@@ -104,13 +104,15 @@ def test_reorder_realizes_next_use_order():                   # :179-191
     assert ev2.pages_in_order()[:2] == [7, 9]
 
 
-def test_multi_window_reorder_matches_oracle():
+@pytest.mark.parametrize("path", [0, 8], ids=["coop", "onesweep"])
+def test_multi_window_reorder_matches_oracle(path):
     """reorder_for_opt over several windows (one multisplit on the GPU) ==
     the reference's per-run madvise sequence (oracle run list)."""
     rng = random.Random(11)
     for _ in range(40):
         pages = rng.sample(range(3000), 600)
         ev = make_list([], domain=4096)
+        ev.ctx.debug(path)
         rl = port.RunList()
         runs = port.norm_runs([(p, p + 1) for p in pages])
         # append in a shuffled run order to get a non-sorted list
@@ -133,10 +135,67 @@ def test_multi_window_reorder_matches_oracle():
         assert ev.pages_in_order() == rl.order()
 
 
-def test_randomized_list_ops_match_oracle():
+def _closed_form_reorder(order, wins):
+    """the reorder is a stable sort of the list by the
+    tuple (class in window 0, ..., class in window W-1), class = K_w - r for
+    the r-th first-access run of window w (0 if absent).  A numpy statement
+    of it for list sizes the per-run madvise oracle cannot replay in time;
+    the small randomized tests above pin it to the oracle."""
+    import numpy as np
+
+    order = np.asarray(order, dtype=np.int64)
+    keys = []
+    for runs in wins:
+        k = len(runs)
+        st = np.array([a for a, _ in runs], dtype=np.int64)
+        en = np.array([b for _, b in runs], dtype=np.int64)
+        srt = np.argsort(st, kind="stable")
+        st, en, rank = st[srt], en[srt], srt
+        i = np.searchsorted(st, order, side="right") - 1
+        ok = (i >= 0) & (order < en[np.maximum(i, 0)])
+        keys.append(np.where(ok, k - rank[np.maximum(i, 0)], 0))
+    idx = np.lexsort(tuple(reversed(keys)) + ()) if keys else np.arange(len(order))
+    return order[idx].tolist()
+
+
+@pytest.mark.parametrize("path", [0, 8], ids=["coop", "onesweep"])
+def test_large_reorder_matches_closed_form(path):
+    """~1.2 M resident pages in ~68 K runs of varied length (both the
+    run-chunk and the per-entry paths fire), > 2048 class segments (the class
+    table is searched in global memory) and > 256 classes (two passes)."""
+    rng = random.Random(5)
+    D = 2_000_000
+    ev = memman.EvictionList(domain_pages=D)
+    ev.ctx.debug(path)
+    starts = sorted(rng.sample(range(0, D, 8), 150_000))
+    runs = port.norm_runs([(s, s + rng.choice((1, 3, 8, 8, 8))) for s in starts] +
+                          [(a, a + rng.randrange(500, 20000)) for a in rng.sample(range(0, D - 20000), 60)])
+    order = list(runs)
+    rng.shuffle(order)
+    ev.append_tail(order)
+    cur = [p for a, b in order for p in range(a, b)]
+    assert ev.pages_in_order() == cur
+    for it in range(3):
+        wins = []
+        for w in range(4):
+            seen, wr = (), []
+            for _ in range(1500 if w == 0 else 40):
+                a = rng.randrange(0, D - 30000)
+                new = port.runs_sub(((a, a + rng.randint(1, 30000 if w else 300)),), seen)
+                wr.extend(new)
+                seen = port.runs_or(seen, new)
+            wins.append(wr)
+        memman.reorder_for_opt(ev, (), {}, [memman.Window("t", wr, wr, PageSet(wr), 0) for wr in wins])
+        cur = _closed_form_reorder(cur, wins)
+        assert ev.pages_in_order() == cur, it
+
+
+@pytest.mark.parametrize("path", [0, 8], ids=["coop", "onesweep"])
+def test_randomized_list_ops_match_oracle(path):
     rng = random.Random(7)
     for _ in range(20):
         ev = memman.EvictionList(domain_pages=20000)
+        ev.ctx.debug(path)
         rl = port.RunList()
         for _ in range(25):
             op = rng.random()
