@@ -448,11 +448,310 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P, int
   if (threadIdx.x == 0) { *P.nseg_out = nc; *P.ncls_out = ndist; }
 }
 
+// ---------------------------------------------------------------------------
+// K3 fast path: every window's first-access runs, the cross-window class
+// table and window 0's demand runs in ONE single-CTA launch (memman.py:174-206
+// + the reorder classes of DESIGN.md section 3 + engine.py:310-313).  Used
+// when the windows hold <= 512 predicted intervals in total (all configs
+// here: <= 168), so every sort is one element per thread: a 1024-wide
+// bitonic network with shuffles for strides < 32 and shared memory above.
+// Descriptors travel as kernel parameters; all searches run in shared memory.
+
+constexpr int FW_MAX_WIN = 16;
+constexpr int FW_MAX_IV = 512;
+constexpr int FW_MAX_SPANS = 1024;
+constexpr uint64_t FW_POS = (1ull << 48) - 1;
+
+struct FusedWinParams {
+  WinDesc wd[FW_MAX_WIN];
+  int32_t nwin;
+  WinOut out;
+  const int64_t* span_first; const int64_t* span_dense; int32_t nspans;
+  int64_t* seg_lo; int64_t* seg_hi; int32_t* seg_cls; int64_t* nseg_out; int64_t* ncls_out;
+  RangeOut R;            // window 0 demand runs (R.nr == nullptr: not wanted)
+};
+
+struct FwSmem {
+  int64_t ia[FW_MAX_IV], ib[FW_MAX_IV];
+  int32_t iw[FW_MAX_IV], icmd[FW_MAX_IV];
+  uint64_t E[1024];             // unique window-tagged endpoints
+  int32_t L[1024];              // first-access command per segment
+  uint64_t xk[1024], xk2[1024]; // bitonic exchange
+  int32_t xv[1024];
+  int64_t ra[1024], rb[1024];   // runs by id (start order), abs
+  int32_t rl[1024], rsk[1024], rek[1024];
+  int64_t sa[1024], sb[1024];   // runs in first-access order (window, label, start)
+  int32_t sl[1024], sw[1024], scls[1024];
+  uint8_t isb[1024];
+  uint64_t E2[1024];            // unique run boundaries (abs)
+  unsigned __int128 skey[1024]; // mixed-radix class tuple per elementary segment
+  int32_t cls_of[1024];
+  uint16_t wcls[FW_MAX_WIN * 1024];   // class of each elementary segment per window
+  int64_t span_first[FW_MAX_SPANS], span_dense[FW_MAX_SPANS];
+  int64_t ws[32];
+  int64_t ioff[FW_MAX_WIN + 1], coff[FW_MAX_WIN + 1];
+  int32_t wfirst[FW_MAX_WIN], K[FW_MAX_WIN];
+  unsigned long long pages[FW_MAX_WIN];
+  unsigned __int128 M[FW_MAX_WIN];
+  int32_t nu, R, nu2;
+};
+
+// Bitonic sort of the first n triples (n a power of two <= 1024), one
+// (hi, lo, payload) triple per thread, ordered lexicographically; on return
+// thread t < n holds the triple of rank t.  Triples must be distinct (the
+// payload is a unique index) and threads count..n-1 must hold padding that
+// sorts last.  Strides < 32 use shuffles; wider ones exchange through shared
+// memory (every thread reaches the barriers; only t < max(n, 32) computes).
+__device__ __forceinline__ void fw_sort2(uint64_t& hi, uint64_t& lo, int32_t& v, FwSmem& s, int n) {
+  const int t = threadIdx.x;
+  const bool act = t < (n < 32 ? 32 : n);
+  for (int kk = 2; kk <= n; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      uint64_t ph = 0, pl = 0; int32_t pv = 0;
+      if (j >= 32) {
+        if (act) { s.xk[t] = hi; s.xk2[t] = lo; s.xv[t] = v; }
+        __syncthreads();
+        if (act) { ph = s.xk[t ^ j]; pl = s.xk2[t ^ j]; pv = s.xv[t ^ j]; }
+        __syncthreads();
+      } else if (act) {
+        ph = __shfl_xor_sync(0xffffffffu, hi, j);
+        pl = __shfl_xor_sync(0xffffffffu, lo, j);
+        pv = __shfl_xor_sync(0xffffffffu, v, j);
+      }
+      if (act) {
+        const bool up = (t & kk) == 0, lower = (t & j) == 0;
+        const bool less = ph < hi || (ph == hi && (pl < lo || (pl == lo && pv < v)));
+        if (lower == up ? less : !less) { hi = ph; lo = pl; v = pv; }
+      }
+    }
+  }
+}
+
+__device__ __forceinline__ void fw_sort(uint64_t& k, int32_t& v, FwSmem& s, int n) {
+  uint64_t z = 0;
+  fw_sort2(k, z, v, s, n);
+}
+
+__device__ __forceinline__ int fw_pow2(int n) {
+  int p = 1;
+  while (p < n) p <<= 1;
+  return p;
+}
+
+__device__ __forceinline__ int32_t fw_lb(const uint64_t* a, int32_t n, uint64_t x) {
+  int32_t lo = 0, hi = n;
+  while (lo < hi) { int32_t mid = (lo + hi) >> 1; if (a[mid] < x) lo = mid + 1; else hi = mid; }
+  return lo;
+}
+
+__global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
+  extern __shared__ __align__(16) unsigned char fw_raw[];
+  FwSmem& s = *reinterpret_cast<FwSmem*>(fw_raw);
+  const int t = threadIdx.x, lane = t & 31;
+  const int W = P.nwin;
+  if (t == 0) {
+    s.ioff[0] = 0; s.coff[0] = 0;
+    for (int w = 0; w < W; ++w) {
+      s.ioff[w + 1] = s.ioff[w] + (P.wd[w].pool_hi - P.wd[w].pool_lo);
+      s.coff[w + 1] = s.coff[w] + (P.wd[w].c1 - P.wd[w].c0);
+    }
+  }
+  if (t < FW_MAX_WIN) { s.wfirst[t] = 0x7fffffff; s.K[t] = 0; s.pages[t] = 0; }
+  for (int i = t; i < P.nspans; i += 1024) { s.span_first[i] = P.span_first[i]; s.span_dense[i] = P.span_dense[i]; }
+  __syncthreads();
+  const int32_t N = (int32_t)s.ioff[W];
+  const int64_t NC = s.coff[W];
+  // ---- intervals and their commands
+  for (int64_t k = t; k < NC; k += 1024) {
+    int w = 0;
+    while (k >= s.coff[w + 1]) ++w;
+    const WinDesc& D = P.wd[w];
+    int32_t c = D.c0 + (int32_t)(k - s.coff[w]);
+    int64_t j0 = D.cmd_off[c], j1 = D.cmd_off[c + 1];
+    for (int64_t j = j0; j < j1; ++j) s.icmd[s.ioff[w] + (j - D.pool_lo)] = c;
+  }
+  if (t < N) {
+    int w = 0;
+    while (t >= s.ioff[w + 1]) ++w;
+    const Iv v = P.wd[w].pool[P.wd[w].pool_lo + (t - s.ioff[w])];
+    s.ia[t] = v.a; s.ib[t] = v.b; s.iw[t] = w;
+  }
+  __syncthreads();
+  // ---- unique window-tagged endpoints
+  {
+    uint64_t k = ~0ull;
+    int32_t v = t;
+    if (t < 2 * N) {
+      int i = t >> 1;
+      k = ((uint64_t)s.iw[i] << 48) | (uint64_t)((t & 1) ? s.ib[i] : s.ia[i]);
+    }
+    fw_sort(k, v, s, fw_pow2(2 * N));
+    s.xk[t] = k;
+    __syncthreads();
+    bool f = t < 2 * N && (t == 0 || s.xk[t - 1] != k);
+    int64_t tot;
+    int64_t pos = block_scan_excl_i64(f ? 1 : 0, s.ws, &tot);
+    if (f) s.E[pos] = k;
+    if (t == 0) s.nu = (int32_t)tot;
+  }
+  s.L[t] = kNone;
+  s.isb[t] = 0;
+  __syncthreads();
+  const int32_t nu = s.nu;
+  // ---- first-access label per elementary segment (memman.py:187-193)
+  if (t < N) {
+    uint64_t tag = (uint64_t)s.iw[t] << 48;
+    int32_t s0 = fw_lb(s.E, nu, tag | (uint64_t)s.ia[t]), s1 = fw_lb(s.E, nu, tag | (uint64_t)s.ib[t]);
+    for (int32_t k = s0; k < s1; ++k) atomicMin(&s.L[k], s.icmd[t]);
+  }
+  __syncthreads();
+  // ---- maximal runs of one label (consecutive covered segments share a window)
+  {
+    const int32_t k = t;
+    const bool in = k < nu - 1 && s.L[k] != kNone;
+    const bool st = in && (k == 0 || s.L[k - 1] != s.L[k]);
+    const bool en = in && (k == nu - 2 || s.L[k + 1] != s.L[k]);
+    int64_t tot;
+    int64_t ex = block_scan_excl_i64(st ? 1 : 0, s.ws, &tot);
+    int32_t rid = (int32_t)(ex + (st ? 1 : 0)) - 1;
+    if (st) { s.ra[rid] = (int64_t)(s.E[k] & FW_POS); s.rl[rid] = s.L[k]; s.rsk[rid] = k; }
+    if (en) { s.rb[rid] = (int64_t)(s.E[k + 1] & FW_POS); s.rek[rid] = k + 1; }
+    if (t == 0) s.R = (int32_t)tot;
+  }
+  __syncthreads();
+  const int32_t R = s.R;
+  // ---- runs in first-access order per window: (window, label, start)
+  {
+    uint64_t k = ~0ull;
+    int32_t v = t;
+    if (t < R) k = ((s.E[s.rsk[t]] >> 48) << 52) | ((uint64_t)(uint32_t)s.rl[t] << 20) | (uint64_t)t;
+    fw_sort(k, v, s, fw_pow2(R));
+    if (t < R) {
+      int w = (int)(k >> 52);
+      atomicMin(&s.wfirst[w], t);
+      atomicAdd(&s.K[w], 1);
+    }
+    __syncthreads();
+    if (t < R) {
+      int w = (int)(k >> 52);
+      int32_t rid = (int32_t)(k & 0xfffff);
+      int32_t r = t - s.wfirst[w];
+      int64_t a = s.ra[rid], b = s.rb[rid];
+      s.sa[t] = a; s.sb[t] = b; s.sl[t] = s.rl[rid]; s.sw[t] = w; s.scls[t] = s.K[w] - r;
+      int64_t o = P.wd[w].scratch + r;
+      P.out.run_a[o] = a; P.out.run_b[o] = b; P.out.run_lab[o] = s.rl[rid];
+      atomicAdd(&s.pages[w], (unsigned long long)(b - a));
+      s.isb[s.rsk[rid]] = 1;   // run boundaries, marked on the endpoint list
+      s.isb[s.rek[rid]] = 1;
+    }
+  }
+  __syncthreads();
+  if (t < W) {
+    P.out.nruns[t] = s.K[t];
+    P.out.pages[t] = (int64_t)s.pages[t];
+    P.out.run_base[t] = P.wd[t].scratch;
+  }
+  auto dense_of = [&](int64_t a) -> int64_t {
+    int32_t lo = 0, hi = P.nspans;
+    while (lo < hi) { int32_t mid = (lo + hi) >> 1; if (s.span_first[mid] <= a) lo = mid + 1; else hi = mid; }
+    return s.span_dense[lo - 1] + (a - s.span_first[lo - 1]);
+  };
+  // ---- window 0 demand runs: not self-populating, dense, first-access order
+  if (P.R.nr) {
+    const int32_t K0 = W > 0 ? s.K[0] : 0;
+    const int32_t r = t;   // window 0 runs are ranks [0, K0)
+    bool keep = false;
+    int64_t dlo = 0, dlen = 0;
+    if (r < K0) {
+      keep = !P.wd[0].selfpop[s.sl[r]];
+      dlo = dense_of(s.sa[r]);
+      dlen = s.sb[r] - s.sa[r];
+    }
+    int64_t words = keep ? ((dlo + dlen + 31) >> 5) - (dlo >> 5) : 0;
+    int64_t tot, utot;
+    int64_t ex = block_scan_excl_i64(keep ? 1 : 0, s.ws, &tot);
+    int64_t uex = block_scan_excl_i64(words, s.ws, &utot);
+    if (keep) {
+      P.R.lo[ex] = dlo; P.R.len[ex] = dlen; P.R.tag[ex] = s.sl[r] - P.wd[0].c0; P.R.uoff[ex] = uex;
+    }
+    if (t == 0) { *P.R.nr = tot; P.R.uoff[tot] = utot; }
+  }
+  // ---- cross-window class table: elementary segments of all run boundaries
+  {
+    uint64_t k = ~0ull;
+    int32_t v = t;
+    if (t < nu && s.isb[t]) k = s.E[t] & FW_POS;
+    fw_sort(k, v, s, fw_pow2(nu));
+    s.xk[t] = k;
+    __syncthreads();
+    bool f = k != ~0ull && (t == 0 || s.xk[t - 1] != k);
+    int64_t tot;
+    int64_t pos = block_scan_excl_i64(f ? 1 : 0, s.ws, &tot);
+    if (f) s.E2[pos] = k;
+    if (t == 0) {
+      s.nu2 = (int32_t)tot;
+      unsigned __int128 m = 1;
+      for (int w = W - 1; w >= 0; --w) { s.M[w] = m; m *= (unsigned __int128)(s.K[w] + 1); }
+    }
+    s.skey[t] = 0;
+  }
+  __syncthreads();
+  const int32_t nu2 = s.nu2;
+  // paint each window's class over the elementary segments (all windows in
+  // parallel: runs of one window are disjoint), then fold to the mixed radix
+  for (int i = t; i < W * 1024; i += 1024) s.wcls[i] = 0;
+  __syncthreads();
+  if (t < R) {
+    int32_t s0 = fw_lb(s.E2, nu2, (uint64_t)s.sa[t]), s1 = fw_lb(s.E2, nu2, (uint64_t)s.sb[t]);
+    uint16_t c = (uint16_t)s.scls[t];
+    for (int32_t k = s0; k < s1; ++k) s.wcls[s.sw[t] * 1024 + k] = c;
+  }
+  __syncthreads();
+  if (t < nu2 - 1) {
+    unsigned __int128 key = 0;
+    for (int w = 0; w < W; ++w) key += (unsigned __int128)s.wcls[w * 1024 + t] * s.M[w];
+    s.skey[t] = key;
+  }
+  __syncthreads();
+  // dense rank of the distinct tuples over covered segments
+  {
+    const int32_t k = t;
+    const bool cov = k < nu2 - 1 && s.skey[k] != 0;
+    uint64_t hi = cov ? (uint64_t)(s.skey[k] >> 64) : ~0ull;   // valid tuples are < 2^97
+    uint64_t lo = cov ? (uint64_t)s.skey[k] : ~0ull;
+    int32_t v = k;
+    fw_sort2(hi, lo, v, s, fw_pow2(nu2 > 1 ? nu2 - 1 : 1));
+    s.xk[t] = hi; s.xk2[t] = lo;
+    __syncthreads();
+    const bool valid = hi != ~0ull;
+    const bool first = valid && (t == 0 || s.xk[t - 1] != hi || s.xk2[t - 1] != lo);
+    int64_t tot;
+    int64_t ex = block_scan_excl_i64(first ? 1 : 0, s.ws, &tot);
+    if (valid) s.cls_of[v] = (int32_t)(ex + (first ? 1 : 0));
+    if (t == 0) *P.ncls_out = tot;
+  }
+  __syncthreads();
+  // ---- covered segments in position order, dense
+  {
+    const int32_t k = t;
+    const bool cov = k < nu2 - 1 && s.skey[k] != 0;
+    int64_t tot;
+    int64_t ci = block_scan_excl_i64(cov ? 1 : 0, s.ws, &tot);
+    if (cov) {
+      int64_t a = (int64_t)s.E2[k], b = (int64_t)s.E2[k + 1];
+      int64_t d = dense_of(a);
+      P.seg_lo[ci] = d; P.seg_hi[ci] = d + (b - a); P.seg_cls[ci] = s.cls_of[k];
+    }
+    if (t == 0) *P.nseg_out = tot;
+  }
+}
+
 static void win_kernels_init() {
   static bool done = false;
   if (done) return;
   MSG_CUDA(cudaFuncSetAttribute(k_window_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
   MSG_CUDA(cudaFuncSetAttribute(k_window_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
+  MSG_CUDA(cudaFuncSetAttribute(k_windows_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwSmem)));
   done = true;
 }
 
@@ -848,31 +1147,40 @@ k_ms_onesweep(const int32_t* __restrict__ src, int64_t n, SegTab T, int shift, i
 // ---------------------------------------------------------------------------
 // On-chip multisplit (one cooperative launch per pass, one grid barrier).
 //
-// One 1024-thread CTA per SM owns a contiguous slice of the list; each of its
-// 32 warps owns a contiguous run of 128-entry chunks inside it.  Phase 1
-// reads every entry once (four coalesced 128-byte loads per chunk per warp),
-// classifies chunks — a chunk that is one run of consecutive ids inside one
-// constant-class interval is recorded as (first id, digit) and never read
-// again — and counts digits per warp; entries of the other chunks are kept in
-// shared memory (or re-read later if the slice is larger than the cache).
-// The CTA's digit histogram goes to global memory; after the grid barrier
-// every CTA reads the whole histogram matrix (148 x 256 counters, from L2) to
-// get its digit bases, so no look-back and no separate totals kernel exist.
-// Phase 3 replays the chunks in the same order and writes: run chunks as
-// computed ids with coalesced stores, the others ranked with match_any in
-// array order (stable).  Traffic: 4 B read + 4 B written per entry.
+// One 1024-thread CTA per SM owns a contiguous slice of the list, staged in
+// shared memory by one TMA bulk copy (slices are cut on 16-byte boundaries of
+// the underlying buffer, so every 512-entry block is 16-byte aligned in both
+// global and shared memory).  Each of the 32 warps owns a contiguous run of
+// blocks.  The eviction list is made of long runs of consecutive page ids
+// (pages are appended run by run, and every multisplit keeps relative
+// order), so phase 1 checks a whole block with four 16-byte shared loads per
+// lane: a block that is one run inside one constant-class interval is
+// recorded as (first id, digit) and never looked at again.  Other blocks are
+// split into 128-entry chunks (run chunk or per-entry, ranked with match_any
+// in array order, so the split is stable).  The CTA's digit histogram goes
+// to global memory (totals by atomics); after the grid barrier each CTA sums
+// the rows of the CTAs before it, so there is no look-back and no separate
+// totals kernel.  Phase 3 replays the blocks in order: run blocks are written
+// as computed ids with aligned 16-byte stores.  Traffic: 4 B read + 4 B
+// written per entry.
 constexpr int MC_THREADS = 1024;
 constexpr int MC_WARPS = MC_THREADS / 32;
+constexpr int MC_BLOCK = 512;                       // entries per fast block (16 per lane)
 constexpr int MC_SMEM = 224 * 1024;
-constexpr int MC_FIXED = 3 * MS_SMEM_SEGS * 4 + MC_WARPS * 256 * 4 + 256 * 8 + 2 * 4 * 256 * 4 + 64 + 8 + 16;
+constexpr int MC_FIXED = 3 * MS_SMEM_SEGS * 4 + MC_WARPS * 256 * 4 + 256 * 8 + 16 * 256 * 4 + 64 + 16;
 
 struct McArgs {
-  const int32_t* src; int64_t n; SegTab T; int shift; int32_t* dst;
-  int32_t* hist;       // [gridDim.x][256] per-CTA digit counts
-  int32_t* bar;        // grid barrier counter (zero at launch)
-  int64_t E;           // entries per CTA (multiple of 128)
-  int32_t vcap;        // entries per CTA kept in shared memory
-  int32_t nch_cap;     // chunk records per CTA
+  const int32_t* srcA;   // 16-byte aligned base: list entry i is srcA[i + a]
+  int64_t nA;            // n + a
+  int32_t a;             // leading pad entries (0..3)
+  SegTab T; int shift; int32_t* dst;
+  int32_t* hist;         // [gridDim.x][256] per-CTA digit counts
+  int32_t* tot;          // [256] digit totals (zero at launch)
+  int32_t* tot_next;     // [256] zeroed here for the next launch
+  int32_t* bar;          // grid barrier counter (zero at launch)
+  int64_t E;             // aligned entries per CTA (multiple of MC_BLOCK)
+  int32_t vcap;          // entries per CTA kept in shared memory (multiple of MC_BLOCK)
+  int32_t nch_cap;       // chunk records per CTA
 };
 
 // TMA bulk copy global -> shared, completion counted on an mbarrier.
@@ -921,30 +1229,24 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   int32_t* cls32 = hi32 + MS_SMEM_SEGS;
   int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(cls32 + MS_SMEM_SEGS);
   int64_t* base = reinterpret_cast<int64_t*>(cnt + MC_WARPS);
-  int32_t* red = reinterpret_cast<int32_t*>(base + 256);          // [2][4][256]
-  int64_t* misc = reinterpret_cast<int64_t*>(red + 2 * 4 * 256);  // 8 x int64: warp totals; [7] = mbarrier
-  int2* info = reinterpret_cast<int2*>(misc + 8);                 // nch_cap chunk records
-  int32_t* cache = reinterpret_cast<int32_t*>(info + ((A.nch_cap + 1) & ~1));   // 16-B aligned, vcap + 4
+  int32_t* red = reinterpret_cast<int32_t*>(base + 256);          // [16][256]
+  int64_t* misc = reinterpret_cast<int64_t*>(red + 16 * 256);     // 8 x int64: warp totals; [7] = mbarrier
+  int2* info = reinterpret_cast<int2*>(misc + 8);                 // chunk records
+  int32_t* cache = reinterpret_cast<int32_t*>(info + ((A.nch_cap + 1) & ~1));   // 16-B aligned
   uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 7);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = (1u << lane) - 1u;
   const int shift = A.shift;
-  const int64_t r0 = (int64_t)blockIdx.x * A.E;
-  const int64_t r1 = r0 + A.E < A.n ? r0 + A.E : A.n;
-  const int64_t len = r1 > r0 ? r1 - r0 : 0;
-  // stage the first m entries of the slice in shared memory with one TMA bulk
-  // copy (16-byte aligned window; entry i lands at cache[delta + i])
-  const int64_t m = len < A.vcap ? len : A.vcap;
-  const uintptr_t g0 = reinterpret_cast<uintptr_t>(A.src + r0);
-  const int32_t delta = (int32_t)((g0 & 15) >> 2);
+  const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
+  const int64_t cEnd = cE + A.E < A.nA ? cE + A.E : A.nA;
+  const int64_t lenA = cEnd > cE ? cEnd - cE : 0;
+  const int32_t m = (int32_t)(lenA < A.vcap ? lenA : A.vcap);      // staged entries
   if (tid == 0) {
     mbar_init(bar, 1);
     if (m > 0) {
-      uintptr_t gs = g0 & ~uintptr_t(15);
-      uintptr_t ge = (reinterpret_cast<uintptr_t>(A.src + r0 + m) + 15) & ~uintptr_t(15);
-      uint32_t bytes = (uint32_t)(ge - gs);
+      uint32_t bytes = (uint32_t)(((int64_t)m * 4 + 15) & ~int64_t(15));
       mbar_expect_tx(bar, bytes);
-      tma_bulk_g2s(cache, reinterpret_cast<const void*>(gs), bytes, bar);
+      tma_bulk_g2s(cache, A.srcA + cE, bytes, bar);
     }
   }
   // class table -> smem while the copy is in flight
@@ -964,82 +1266,121 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   for (int i = lane; i < 256; i += 32) cnt[warp][i] = 0;
   __syncthreads();
   if (m > 0) mbar_wait(bar, 0);
-  const int32_t nch = (int32_t)((len + MS_CHUNK - 1) / MS_CHUNK);
-  const int32_t ch0 = (int32_t)((int64_t)nch * warp / MC_WARPS);
-  const int32_t ch1 = (int32_t)((int64_t)nch * (warp + 1) / MC_WARPS);
+  auto valid = [&](int32_t off) { int64_t ia = cE + off; return ia >= A.a && ia < A.nA; };
+  auto fetch = [&](int32_t off) -> int32_t { return off < m ? cache[off] : __ldcs(A.srcA + cE + off); };
+  const int32_t nblk = (int32_t)((lenA + MC_BLOCK - 1) / MC_BLOCK);
+  const int32_t b0 = (int32_t)((int64_t)nblk * warp / MC_WARPS);
+  const int32_t b1 = (int32_t)((int64_t)nblk * (warp + 1) / MC_WARPS);
   int32_t c_lo = 1, c_hi = 0, c_d = 0;   // the warp's cached constant-class interval
+  // digit of a run [v, v + len) if it lies in one constant-class interval, else -1
+  auto run_digit = [&](int32_t v, int32_t len) -> int {
+    if (!(v >= c_lo && v + (len - 1) < c_hi)) {
+      Span sp = seg_find(S, v);
+      c_lo = sp.lo; c_hi = sp.hi; c_d = (sp.cls >> shift) & 255;
+    }
+    return v + (len - 1) < c_hi ? c_d : -1;
+  };
   // ---- phase 1: classify and count
-  for (int32_t ch = ch0; ch < ch1; ++ch) {
-    const int64_t cb = r0 + (int64_t)ch * MS_CHUNK;
-    int32_t x[4];
+  for (int32_t b = b0; b < b1; ++b) {
+    const int32_t boff = b * MC_BLOCK;
+    const bool full = cE + boff >= A.a && cE + boff + MC_BLOCK <= A.nA;
+    int4 q[4];
+    if (boff + MC_BLOCK <= m) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int32_t off = ch * MS_CHUNK + 32 * k + lane;
-      const int64_t i = cb + 32 * k + lane;
-      x[k] = i < r1 ? (off < m ? cache[delta + off] : __ldcs(A.src + i)) : 0;
-    }
-    const int32_t v0 = __shfl_sync(0xffffffffu, x[0], 0);
-    bool ok = cb + MS_CHUNK <= r1;
+      for (int t = 0; t < 4; ++t) q[t] = *reinterpret_cast<const int4*>(cache + boff + 16 * lane + 4 * t);
+    } else if (cE + boff + MC_BLOCK <= A.nA) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) ok = ok && x[k] == v0 + 32 * k + lane;
-    int d = -1;
-    if (__all_sync(0xffffffffu, ok)) {
-      if (!(v0 >= c_lo && v0 + (MS_CHUNK - 1) < c_hi)) {
-        Span sp = seg_find(S, v0);
-        c_lo = sp.lo; c_hi = sp.hi; c_d = (sp.cls >> shift) & 255;
+      for (int t = 0; t < 4; ++t)
+        q[t] = __ldcs(reinterpret_cast<const int4*>(A.srcA + cE + boff + 16 * lane + 4 * t));
+    } else {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        int32_t o = boff + 16 * lane + 4 * t;
+        q[t].x = valid(o) ? fetch(o) : 0; q[t].y = valid(o + 1) ? fetch(o + 1) : 0;
+        q[t].z = valid(o + 2) ? fetch(o + 2) : 0; q[t].w = valid(o + 3) ? fetch(o + 3) : 0;
       }
-      if (v0 + (MS_CHUNK - 1) < c_hi) d = c_d;
     }
+    const int32_t v0 = __shfl_sync(0xffffffffu, q[0].x, 0);
+    bool ok = full;
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      int32_t e = v0 + 16 * lane + 4 * t;
+      ok = ok && q[t].x == e && q[t].y == e + 1 && q[t].z == e + 2 && q[t].w == e + 3;
+    }
+    int d = __all_sync(0xffffffffu, ok) ? run_digit(v0, MC_BLOCK) : -1;
     if (d >= 0) {
-      if (lane == 0) { info[ch] = make_int2(v0, d); cnt[warp][d] += MS_CHUNK; }
+      if (lane < 4) info[4 * b + lane] = make_int2(v0 + MS_CHUNK * lane, d);
+      if (lane == 0) cnt[warp][d] += MC_BLOCK;
       __syncwarp();
       continue;
     }
-    if (lane == 0) info[ch] = make_int2(0, -1);
+    // mixed block: per 128-entry chunk, entries striped (32k + lane)
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {
+      const int32_t coff = boff + MS_CHUNK * j;
+      int32_t x[4];
+      bool okc = true;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      int dk = cb + 32 * k + lane < r1 ? ms_digit(S, x[k], c_lo, c_hi, c_d, shift) : 256;
-      uint32_t peers = __match_any_sync(0xffffffffu, dk);
-      if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] += __popc(peers);
-      __syncwarp();
+      for (int k = 0; k < 4; ++k) {
+        int32_t o = coff + 32 * k + lane;
+        bool vk = valid(o);
+        x[k] = vk ? fetch(o) : 0;
+        okc = okc && vk;
+      }
+      const int32_t c0 = __shfl_sync(0xffffffffu, x[0], 0);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) okc = okc && x[k] == c0 + 32 * k + lane;
+      int dc = __all_sync(0xffffffffu, okc) ? run_digit(c0, MS_CHUNK) : -1;
+      if (dc >= 0) {
+        if (lane == 0) { info[4 * b + j] = make_int2(c0, dc); cnt[warp][dc] += MS_CHUNK; }
+        __syncwarp();
+        continue;
+      }
+      if (lane == 0) info[4 * b + j] = make_int2(0, -1);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        int dk = valid(coff + 32 * k + lane) ? ms_digit(S, x[k], c_lo, c_hi, c_d, shift) : 256;
+        uint32_t peers = __match_any_sync(0xffffffffu, dk);
+        if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] += __popc(peers);
+        __syncwarp();
+      }
     }
   }
   __syncthreads();
-  // ---- CTA histogram; exclusive warp offsets
+  // ---- CTA histogram; exclusive warp offsets; digit totals by atomics
   if (tid < 256) {
     int32_t acc = 0;
 #pragma unroll 8
     for (int w = 0; w < MC_WARPS; ++w) { int32_t t = cnt[w][tid]; cnt[w][tid] = acc; acc += t; }
     __stcg(A.hist + (int64_t)blockIdx.x * 256 + tid, acc);
+    if (acc) atomicAdd(A.tot + tid, acc);
   }
   grid_barrier(A.bar);
-  // ---- phase 2: digit bases from the histogram matrix (prefix over CTAs + digit totals)
+  // ---- phase 2: digit bases = totals scan + this CTA's prefix over the
+  // histogram rows of the CTAs before it (16-byte loads, 16 row groups)
   {
-    const int d = tid & 255, g = tid >> 8;
-    const int G = (int)gridDim.x, me = (int)blockIdx.x;
-    int32_t pre = 0, all = 0;
-    for (int c0 = g; c0 < G; c0 += 64) {
-      int32_t v[16];
+    const int qd = tid & 63, g = tid >> 6;      // digits 4qd..4qd+3, rows g, g+16, ...
+    int4 pre = make_int4(0, 0, 0, 0);
+    const int me = (int)blockIdx.x;
+    for (int r0 = g; r0 < me; r0 += 64) {
+      int4 v[4];
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        int c = c0 + 4 * u;
-        v[u] = c < G ? __ldcg(A.hist + (int64_t)c * 256 + d) : 0;
+      for (int u = 0; u < 4; ++u) {
+        int c = r0 + 16 * u;
+        v[u] = c < me ? __ldcg(reinterpret_cast<const int4*>(A.hist + (int64_t)c * 256) + qd) : make_int4(0, 0, 0, 0);
       }
 #pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        all += v[u];
-        if (c0 + 4 * u < me) pre += v[u];
-      }
+      for (int u = 0; u < 4; ++u) { pre.x += v[u].x; pre.y += v[u].y; pre.z += v[u].z; pre.w += v[u].w; }
     }
-    red[g * 256 + d] = pre;
-    red[1024 + g * 256 + d] = all;
+    reinterpret_cast<int4*>(red + g * 256)[qd] = pre;
   }
   __syncthreads();
   {
     int64_t pre = 0, tot = 0, x = 0;
     if (tid < 256) {
-      pre = (int64_t)red[tid] + red[256 + tid] + red[512 + tid] + red[768 + tid];
-      tot = (int64_t)red[1024 + tid] + red[1280 + tid] + red[1536 + tid] + red[1792 + tid];
+#pragma unroll
+      for (int g = 0; g < 16; ++g) pre += red[g * 256 + tid];
+      tot = __ldcg(A.tot + tid);
       x = tot;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -1053,38 +1394,63 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       int64_t wp = 0;
       for (int w = 0; w < warp; ++w) wp += misc[w];
       base[tid] = wp + (x - tot) + pre;
+      if (blockIdx.x == 0) A.tot_next[tid] = 0;   // the next launch's totals start at zero
     }
   }
   __syncthreads();
-  // ---- phase 3: replay the chunks in order and scatter
-  for (int32_t ch = ch0; ch < ch1; ++ch) {
-    const int64_t cb = r0 + (int64_t)ch * MS_CHUNK;
-    const int2 rec = info[ch];
-    if (rec.y >= 0) {
-      const int d = rec.y;
-      const int32_t before = cnt[warp][d];
-      const int64_t p = base[d] + before + lane;
-      const int32_t v = rec.x + lane;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) A.dst[p + 32 * k] = v + 32 * k;
+  // ---- phase 3: replay the blocks in order and scatter
+  int32_t* __restrict__ dst = A.dst;
+  for (int32_t b = b0; b < b1; ++b) {
+    const int32_t boff = b * MC_BLOCK;
+    int2 r = lane < 4 ? info[4 * b + lane] : make_int2(0, -1);
+    const int32_t v0 = __shfl_sync(0xffffffffu, r.x, 0);
+    const int d0 = __shfl_sync(0xffffffffu, r.y, 0);
+    const bool same = lane >= 4 || (r.y == d0 && r.x == v0 + MS_CHUNK * lane);
+    if (d0 >= 0 && __all_sync(0xffffffffu, same)) {
+      const int32_t before = cnt[warp][d0];
+      const int64_t p = base[d0] + before;
+      const int32_t ph = (int32_t)((4 - (p & 3)) & 3);          // entries before a 16-B boundary
+      if (lane < ph) dst[p + lane] = v0 + lane;
+      const int32_t nb = (MC_BLOCK - ph) >> 2;
+      for (int32_t k = lane; k < nb; k += 32) {
+        int32_t t = ph + 4 * k;
+        *reinterpret_cast<int4*>(dst + p + t) = make_int4(v0 + t, v0 + t + 1, v0 + t + 2, v0 + t + 3);
+      }
+      const int32_t ts = ph + 4 * nb;
+      if (lane < MC_BLOCK - ts) dst[p + ts + lane] = v0 + ts + lane;
       __syncwarp();
-      if (lane == 0) cnt[warp][d] = before + MS_CHUNK;
+      if (lane == 0) cnt[warp][d0] = before + MC_BLOCK;
       __syncwarp();
       continue;
     }
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {
+      const int32_t rx = __shfl_sync(0xffffffffu, r.x, j);
+      const int ry = __shfl_sync(0xffffffffu, r.y, j);
+      const int32_t coff = boff + MS_CHUNK * j;
+      if (ry >= 0) {
+        const int32_t before = cnt[warp][ry];
+        const int64_t p = base[ry] + before + lane;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const int32_t off = ch * MS_CHUNK + 32 * k + lane;
-      const int64_t i = cb + 32 * k + lane;
-      int32_t xv = 0;
-      if (i < r1) xv = off < m ? cache[delta + off] : __ldcs(A.src + i);
-      int dk = i < r1 ? ms_digit(S, xv, c_lo, c_hi, c_d, shift) : 256;
-      uint32_t peers = __match_any_sync(0xffffffffu, dk);
-      int32_t before = dk < 256 ? cnt[warp][dk] : 0;
-      __syncwarp();
-      if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] = before + __popc(peers);
-      __syncwarp();
-      if (dk < 256) A.dst[base[dk] + before + __popc(peers & lt)] = xv;
+        for (int k = 0; k < 4; ++k) dst[p + 32 * k] = rx + lane + 32 * k;
+        __syncwarp();
+        if (lane == 0) cnt[warp][ry] = before + MS_CHUNK;
+        __syncwarp();
+        continue;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int32_t o = coff + 32 * k + lane;
+        const bool vk = valid(o);
+        const int32_t xv = vk ? fetch(o) : 0;
+        int dk = vk ? ms_digit(S, xv, c_lo, c_hi, c_d, shift) : 256;
+        uint32_t peers = __match_any_sync(0xffffffffu, dk);
+        int32_t before = dk < 256 ? cnt[warp][dk] : 0;
+        __syncwarp();
+        if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] = before + __popc(peers);
+        __syncwarp();
+        if (dk < 256) dst[base[dk] + before + __popc(peers & lt)] = xv;
+      }
     }
   }
 }
@@ -1164,13 +1530,16 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     coop_grid = coop_per_sm * sms;
   }
   // on-chip cooperative path when every CTA's chunk records fit in shared memory
+  const int32_t* src0 = c.order[c.cur].p + c.head;
+  const int32_t apad = (int32_t)((reinterpret_cast<uintptr_t>(src0) & 15) >> 2);
+  const int64_t nA = n + apad;
   int64_t E = 0, vcap = -1, nch = 0;
   if (coop_grid > 0) {
-    E = (n + coop_grid - 1) / coop_grid;
-    E = (E + MS_CHUNK - 1) / MS_CHUNK * MS_CHUNK;
+    E = (nA + coop_grid - 1) / coop_grid;
+    E = (E + MC_BLOCK - 1) / MC_BLOCK * MC_BLOCK;
     nch = E / MS_CHUNK;
-    vcap = ((int64_t)MC_SMEM - MC_FIXED - 8 * nch) / 4 - 8;   // + 4 alignment slack entries
-    vcap = std::min<int64_t>(vcap, E) & ~int64_t(31);
+    vcap = ((int64_t)MC_SMEM - MC_FIXED - 8 * (nch + 1)) / 4 - 4;   // + 16-B over-read slack
+    vcap = std::min<int64_t>(vcap, E) & ~int64_t(3);
   }
   const bool coop = vcap >= 0 && !(c.debug & 8);
   cudaEvent_t e0, e1;
@@ -1185,8 +1554,10 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     MSG_CUDA(cudaMemsetAsync(tot, 0, 257 * passes * 8, c.st));
     k_ms_digit_totals<<<296, 256, 0, c.st>>>(T, c.bits.p, passes, tot);
     add_launches(1);
-  } else if ((int64_t)c.ms_hist.n < 256 * (int64_t)coop_grid) {
-    c.ms_hist.exact(256 * (int64_t)coop_grid);
+  } else if ((int64_t)c.ms_hist.n < 256 * ((int64_t)coop_grid + 2)) {
+    c.ms_hist.exact(256 * ((int64_t)coop_grid + 2));   // rows + two digit-total buffers
+    MSG_CUDA(cudaMemsetAsync(c.ms_hist.p, 0, c.ms_hist.n * 4, c.st));
+    c.ms_tot_par = 0;
   }
   for (int pass = 0; pass < passes; ++pass) {
     if (++c.ms_epoch >= (1u << 16)) {   // epochs wrap: clear the status words
@@ -1197,7 +1568,11 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     const int32_t* src = c.order[c.cur].p + c.head;
     int32_t* dst = c.order[c.cur ^ 1].p;
     if (coop) {
-      McArgs A{src, n, T, 8 * pass, dst, c.ms_hist.p, c.ms_ctr.p + c.ms_epoch, E, (int32_t)vcap, (int32_t)nch};
+      int32_t* totb = c.ms_hist.p + 256 * (int64_t)coop_grid;
+      const int32_t a = (int32_t)((reinterpret_cast<uintptr_t>(src) & 15) >> 2);
+      McArgs A{src - a, n + a, a, T, 8 * pass, dst, c.ms_hist.p, totb + 256 * c.ms_tot_par,
+               totb + 256 * (c.ms_tot_par ^ 1), c.ms_ctr.p + c.ms_epoch, E, (int32_t)vcap, (int32_t)nch};
+      c.ms_tot_par ^= 1;
       void* args[] = {&A};
       MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS),
                                            args, MC_SMEM, c.st));
@@ -1316,7 +1691,7 @@ struct WinBuild {
   std::vector<int64_t> win_base;
 };
 
-static void build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild& wb) {
+static bool build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild& wb, const RangeOut* dem = nullptr) {
   std::vector<WinDesc> wd(nwin);
   int64_t off = 0;
   for (int w = 0; w < nwin; ++w) {
@@ -1342,22 +1717,25 @@ static void build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
   c.s.i64b.resize(off, st);                 // vals
   c.s.i32a.resize(off, st);                 // labels / run labels
   c.s.i64c.resize(3 * off + 4 * nwin + 8, st);   // run_a | run_b | run_d | run_base | nruns | pages
-  DVec<WinDesc>& dwd = *reinterpret_cast<DVec<WinDesc>*>(&c.s.iv);  // reuse Iv buffer as raw bytes
-  size_t need_iv = (nwin * sizeof(WinDesc) + sizeof(Iv) - 1) / sizeof(Iv);
-  c.s.iv.resize(need_iv, st);
-  MSG_CUDA(cudaMemcpyAsync(c.s.iv.p, wd.data(), nwin * sizeof(WinDesc), cudaMemcpyHostToDevice, st));
-  (void)dwd;
   int64_t* rbuf = c.s.i64c.p;
   WinOut o;
   o.run_a = rbuf; o.run_b = rbuf + off; o.run_d = rbuf + 2 * off;
   o.run_base = rbuf + 3 * off; o.nruns = o.run_base + nwin; o.pages = o.nruns + nwin;
   c.s.i32b.resize(off, st);
   o.run_lab = c.s.i32b.p;
-  win_kernels_init();
-  k_window_runs<<<nwin, 1024, kWinSmem, st>>>(reinterpret_cast<const WinDesc*>(c.s.iv.p),
-                                              c.s.i64a.p, c.s.i64b.p, c.s.i32a.p, o, kWinSmem);
-  MSG_CHECK_LAUNCH();
-  add_launches(1);
+  const bool fused = wb.total_iv <= FW_MAX_IV && nwin <= FW_MAX_WIN && (int64_t)c.span_first.size() <= FW_MAX_SPANS;
+  if (!fused) {
+    DVec<WinDesc>& dwd = *reinterpret_cast<DVec<WinDesc>*>(&c.s.iv);  // reuse Iv buffer as raw bytes
+    size_t need_iv = (nwin * sizeof(WinDesc) + sizeof(Iv) - 1) / sizeof(Iv);
+    c.s.iv.resize(need_iv, st);
+    MSG_CUDA(cudaMemcpyAsync(c.s.iv.p, wd.data(), nwin * sizeof(WinDesc), cudaMemcpyHostToDevice, st));
+    (void)dwd;
+    win_kernels_init();
+    k_window_runs<<<nwin, 1024, kWinSmem, st>>>(reinterpret_cast<const WinDesc*>(c.s.iv.p),
+                                                c.s.i64a.p, c.s.i64b.p, c.s.i32a.p, o, kWinSmem);
+    MSG_CHECK_LAUNCH();
+    add_launches(1);
+  }
   // combine scratch: key[mp] | val[mp] | E[2mp] | idx[2M] | seg_lo[2M] | seg_hi[2M] | nseg | ncls
   int64_t M = 2 * wb.total_iv + 2;    // >= total runs
   int64_t mp = pow2_at_least(2 * M);
@@ -1382,9 +1760,23 @@ static void build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
   P.nseg_out = P.seg_hi + 2 * M;
   P.ncls_out = P.nseg_out + 1;
   win_kernels_init();
+  if (fused) {
+    FusedWinParams F{};
+    for (int w = 0; w < nwin; ++w) F.wd[w] = wd[w];
+    F.nwin = nwin;
+    F.out = o;
+    F.span_first = c.d_span_first.p; F.span_dense = c.d_span_dense.p; F.nspans = (int32_t)c.span_first.size();
+    F.seg_lo = P.seg_lo; F.seg_hi = P.seg_hi; F.seg_cls = P.seg_cls; F.nseg_out = P.nseg_out; F.ncls_out = P.ncls_out;
+    if (dem) F.R = *dem; else F.R.nr = nullptr;
+    k_windows_fused<<<1, 1024, sizeof(FwSmem), st>>>(F);
+    MSG_CHECK_LAUNCH();
+    add_launches(1);
+    return dem != nullptr;
+  }
   k_window_combine<<<1, 1024, kWinSmem, st>>>(P, kWinSmem);
   MSG_CHECK_LAUNCH();
   add_launches(1);
+  return false;
 }
 
 // pointers into the build outputs (must mirror build_windows)
@@ -1622,13 +2014,14 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   int32_t c0 = win[0].c0, c1 = win[0].c1, ncw = c1 - c0;
   c.hbuf.reserve(4 * (int64_t)nwin + 2 * (int64_t)ncw + 64);
   // ---- phase A: windows, class table, window-0 demand vs residency
-  WinBuild wb;
-  build_windows(c, win, nwin, wb);
-  WinPtrs wp = win_ptrs(c, nwin, wb);
   int64_t niv0 = t0.pred_off[c1] - t0.pred_off[c0];
   int64_t nrun_cap = std::max<int64_t>(2 * niv0 + 2, 2);
   int64_t units_cap = t0.pred_units[c1] - t0.pred_units[c0] + 2 * nrun_cap + 2;
   c.s.rdem.reserve(nrun_cap, st);
+  RangeOut dem_out = c.s.rdem.out();
+  WinBuild wb;
+  const bool dem_done = build_windows(c, win, nwin, wb, &dem_out);
+  WinPtrs wp = win_ptrs(c, nwin, wb);
   c.s.ucnt.resize(units_cap, st);
   c.s.uofs.resize(units_cap, st);
   c.s.uscr.resize(512 + ncw, st);
@@ -1644,9 +2037,11 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   D.R = c.s.rdem.out();
   RangeSet R = c.s.rdem.set();
   if (ncw) MSG_CUDA(cudaMemsetAsync(pref_d, 0, ncw * sizeof(int64_t), st));
-  k_demand_collect<<<1, 1024, 0, st>>>(D);
-  MSG_CHECK_LAUNCH();
-  add_launches(1);
+  if (!dem_done) {
+    k_demand_collect<<<1, 1024, 0, st>>>(D);
+    MSG_CHECK_LAUNCH();
+    add_launches(1);
+  }
   units_count(c, R, c.s.ucnt.p, pref_d, nullptr);
   units_scan(c, R, c.s.ucnt.p, c.s.uofs.p, total_d, c.s.uscr.p);
   k_plan_scalars<<<1, 1, 0, st>>>(total_d, c.dstate, c.C, c.len);
