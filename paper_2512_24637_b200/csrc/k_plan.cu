@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P, int
 // Descriptors travel as kernel parameters; all searches run in shared memory.
 
 constexpr int FW_MAX_WIN = 16;
-constexpr int FW_MAX_IV = 512;
+constexpr int FW_MAX_IV = 512;   // 2 x 512 endpoints: one per thread of a 1024-thread CTA
 constexpr int FW_MAX_SPANS = 1024;
 constexpr uint64_t FW_POS = (1ull << 48) - 1;
 
@@ -502,34 +502,44 @@ struct FwSmem {
 // payload is a unique index) and threads count..n-1 must hold padding that
 // sorts last.  Strides < 32 use shuffles; wider ones exchange through shared
 // memory (every thread reaches the barriers; only t < max(n, 32) computes).
-__device__ __forceinline__ void fw_sort2(uint64_t& hi, uint64_t& lo, int32_t& v, FwSmem& s, int n) {
+template <bool HI, bool PAY>
+__device__ __forceinline__ void fw_sortT(uint64_t& hi, uint64_t& lo, int32_t& v, FwSmem& s, int n) {
   const int t = threadIdx.x;
   const bool act = t < (n < 32 ? 32 : n);
   for (int kk = 2; kk <= n; kk <<= 1) {
     for (int j = kk >> 1; j > 0; j >>= 1) {
       uint64_t ph = 0, pl = 0; int32_t pv = 0;
       if (j >= 32) {
-        if (act) { s.xk[t] = hi; s.xk2[t] = lo; s.xv[t] = v; }
+        if (act) { if (HI) s.xk[t] = hi; s.xk2[t] = lo; if (PAY) s.xv[t] = v; }
         __syncthreads();
-        if (act) { ph = s.xk[t ^ j]; pl = s.xk2[t ^ j]; pv = s.xv[t ^ j]; }
+        if (act) { if (HI) ph = s.xk[t ^ j]; pl = s.xk2[t ^ j]; if (PAY) pv = s.xv[t ^ j]; }
         __syncthreads();
       } else if (act) {
-        ph = __shfl_xor_sync(0xffffffffu, hi, j);
+        if (HI) ph = __shfl_xor_sync(0xffffffffu, hi, j);
         pl = __shfl_xor_sync(0xffffffffu, lo, j);
-        pv = __shfl_xor_sync(0xffffffffu, v, j);
+        if (PAY) pv = __shfl_xor_sync(0xffffffffu, v, j);
       }
       if (act) {
         const bool up = (t & kk) == 0, lower = (t & j) == 0;
-        const bool less = ph < hi || (ph == hi && (pl < lo || (pl == lo && pv < v)));
-        if (lower == up ? less : !less) { hi = ph; lo = pl; v = pv; }
+        bool less;
+        if (HI) less = ph < hi || (ph == hi && (pl < lo || (PAY && pl == lo && pv < v)));
+        else less = pl < lo || (PAY && pl == lo && pv < v);
+        if (lower == up ? less : !less) { if (HI) hi = ph; lo = pl; if (PAY) v = pv; }
       }
     }
   }
 }
 
-__device__ __forceinline__ void fw_sort(uint64_t& k, int32_t& v, FwSmem& s, int n) {
+// (hi, lo, payload) triples, lexicographic; payloads unique
+__device__ __forceinline__ void fw_sort2(uint64_t& hi, uint64_t& lo, int32_t& v, FwSmem& s, int n) {
+  fw_sortT<true, true>(hi, lo, v, s, n);
+}
+
+// plain 64-bit keys (duplicates allowed)
+__device__ __forceinline__ void fw_sort(uint64_t& k, FwSmem& s, int n) {
   uint64_t z = 0;
-  fw_sort2(k, z, v, s, n);
+  int32_t v = 0;
+  fw_sortT<false, false>(z, k, v, s, n);
 }
 
 __device__ __forceinline__ int fw_pow2(int n) {
@@ -557,12 +567,12 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     }
   }
   if (t < FW_MAX_WIN) { s.wfirst[t] = 0x7fffffff; s.K[t] = 0; s.pages[t] = 0; }
-  for (int i = t; i < P.nspans; i += 1024) { s.span_first[i] = P.span_first[i]; s.span_dense[i] = P.span_dense[i]; }
+  for (int i = t; i < P.nspans; i += blockDim.x) { s.span_first[i] = P.span_first[i]; s.span_dense[i] = P.span_dense[i]; }
   __syncthreads();
   const int32_t N = (int32_t)s.ioff[W];
   const int64_t NC = s.coff[W];
   // ---- intervals and their commands
-  for (int64_t k = t; k < NC; k += 1024) {
+  for (int64_t k = t; k < NC; k += blockDim.x) {
     int w = 0;
     while (k >= s.coff[w + 1]) ++w;
     const WinDesc& D = P.wd[w];
@@ -580,12 +590,11 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   // ---- unique window-tagged endpoints
   {
     uint64_t k = ~0ull;
-    int32_t v = t;
     if (t < 2 * N) {
       int i = t >> 1;
       k = ((uint64_t)s.iw[i] << 48) | (uint64_t)((t & 1) ? s.ib[i] : s.ia[i]);
     }
-    fw_sort(k, v, s, fw_pow2(2 * N));
+    fw_sort(k, s, fw_pow2(2 * N));
     s.xk[t] = k;
     __syncthreads();
     bool f = t < 2 * N && (t == 0 || s.xk[t - 1] != k);
@@ -623,9 +632,8 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   // ---- runs in first-access order per window: (window, label, start)
   {
     uint64_t k = ~0ull;
-    int32_t v = t;
     if (t < R) k = ((s.E[s.rsk[t]] >> 48) << 52) | ((uint64_t)(uint32_t)s.rl[t] << 20) | (uint64_t)t;
-    fw_sort(k, v, s, fw_pow2(R));
+    fw_sort(k, s, fw_pow2(R));
     if (t < R) {
       int w = (int)(k >> 52);
       atomicMin(&s.wfirst[w], t);
@@ -679,9 +687,8 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   // ---- cross-window class table: elementary segments of all run boundaries
   {
     uint64_t k = ~0ull;
-    int32_t v = t;
     if (t < nu && s.isb[t]) k = s.E[t] & FW_POS;
-    fw_sort(k, v, s, fw_pow2(nu));
+    fw_sort(k, s, fw_pow2(nu));
     s.xk[t] = k;
     __syncthreads();
     bool f = k != ~0ull && (t == 0 || s.xk[t - 1] != k);
@@ -699,7 +706,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   const int32_t nu2 = s.nu2;
   // paint each window's class over the elementary segments (all windows in
   // parallel: runs of one window are disjoint), then fold to the mixed radix
-  for (int i = t; i < W * 1024; i += 1024) s.wcls[i] = 0;
+  for (int i = t; i < W * nu2; i += blockDim.x) s.wcls[(i / nu2) * 1024 + i % nu2] = 0;
   __syncthreads();
   if (t < R) {
     int32_t s0 = fw_lb(s.E2, nu2, (uint64_t)s.sa[t]), s1 = fw_lb(s.E2, nu2, (uint64_t)s.sb[t]);
@@ -720,10 +727,13 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     uint64_t hi = cov ? (uint64_t)(s.skey[k] >> 64) : ~0ull;   // valid tuples are < 2^97
     uint64_t lo = cov ? (uint64_t)s.skey[k] : ~0ull;
     int32_t v = k;
-    fw_sort2(hi, lo, v, s, fw_pow2(nu2 > 1 ? nu2 - 1 : 1));
+    const int ns = fw_pow2(nu2 > 1 ? nu2 - 1 : 1);
+    if (__syncthreads_or(cov && hi != 0)) fw_sort2(hi, lo, v, s, ns);
+    else fw_sortT<false, true>(hi, lo, v, s, ns);
+    const bool valid = t < ns && v < nu2 - 1 && s.skey[v] != 0;
+    if (valid) { hi = (uint64_t)(s.skey[v] >> 64); lo = (uint64_t)s.skey[v]; }
     s.xk[t] = hi; s.xk2[t] = lo;
     __syncthreads();
-    const bool valid = hi != ~0ull;
     const bool first = valid && (t == 0 || s.xk[t - 1] != hi || s.xk2[t - 1] != lo);
     int64_t tot;
     int64_t ex = block_scan_excl_i64(first ? 1 : 0, s.ws, &tot);
@@ -1768,7 +1778,10 @@ static bool build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
     F.span_first = c.d_span_first.p; F.span_dense = c.d_span_dense.p; F.nspans = (int32_t)c.span_first.size();
     F.seg_lo = P.seg_lo; F.seg_hi = P.seg_hi; F.seg_cls = P.seg_cls; F.nseg_out = P.nseg_out; F.ncls_out = P.ncls_out;
     if (dem) F.R = *dem; else F.R.nr = nullptr;
-    k_windows_fused<<<1, 1024, sizeof(FwSmem), st>>>(F);
+    // one element per thread in every phase: 2N endpoints bound them all
+    int threads = 64;
+    while (threads < 2 * wb.total_iv) threads <<= 1;
+    k_windows_fused<<<1, threads, sizeof(FwSmem), st>>>(F);
     MSG_CHECK_LAUNCH();
     add_launches(1);
     return dem != nullptr;
