@@ -1618,41 +1618,75 @@ struct Epochs {
   int* dep;   // [0] max inst_ep over evicted frames, [1] max free_ep over reused free frames
 };
 
-__global__ void k_evict_head(const int32_t* order, int64_t n, uint32_t* bits, int32_t* frame, int32_t* fifo,
-                             int64_t fifo_tail, int64_t C, int64_t* mig, Epochs ep) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-    int32_t p = order[e];
-    atomicAnd(&bits[p >> 5], ~(1u << (p & 31)));
-    int32_t f = frame[p];
-    frame[p] = -1;
-    fifo[(fifo_tail + e) % C] = f;
-    if (mig) mig[e] = ((int64_t)p << 32) | (uint32_t)f;
-    if (ep.inst_ep) {
-      int32_t w = ep.inst_ep[f];
-      if (w >= 0) atomicMax(&ep.dep[0], w);
-      ep.free_ep[f] = ep.batch;
-    }
+// Warp-aggregated residency-bit update: lanes whose pages share a bitmap word
+// combine their bits and one lane issues the atomic (list runs put 32
+// consecutive pages in one word, which would otherwise serialise 32 atomics).
+__device__ __forceinline__ void bits_update(uint32_t* bits, int32_t p, bool valid, bool set) {
+  const unsigned act = __ballot_sync(0xffffffffu, valid);
+  if (!valid) return;
+  const int32_t wd = p >> 5;
+  const unsigned peers = __match_any_sync(act, wd);
+  const unsigned m = __reduce_or_sync(peers, 1u << (p & 31));
+  if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) {
+    if (set) atomicOr(&bits[wd], m); else atomicAnd(&bits[wd], ~m);
   }
 }
 
-__global__ void k_install(const int32_t* pages, const int64_t* np_dev, int64_t np_host, uint32_t* bits,
-                          int32_t* frame, const int32_t* fifo, int64_t fifo_head, int64_t C, int32_t* order_tail,
-                          int64_t* mig, Epochs ep, int64_t old_free) {
-  int64_t n = np_dev ? *np_dev : np_host;
-  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x) {
-    int32_t p = pages[j];
-    atomicOr(&bits[p >> 5], 1u << (p & 31));
-    int32_t f = fifo[(fifo_head + j) % C];
+__global__ void k_evict_head(const int32_t* __restrict__ order, int64_t n, uint32_t* bits, int32_t* frame,
+                             int32_t* fifo, int64_t fifo_tail, int64_t C, int64_t* mig, Epochs ep) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int dep = -1;
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < n; e0 += stride) {
+    const int64_t e = e0 + threadIdx.x;
+    const bool valid = e < n;
+    const int32_t p = valid ? order[e] : 0;
+    bits_update(bits, p, valid, false);
+    if (!valid) continue;
+    const int32_t f = frame[p];
+    frame[p] = -1;
+    int64_t q = fifo_tail + e;
+    if (q >= C) q -= C;
+    if (q >= C) q -= C;
+    fifo[q] = f;
+    if (mig) mig[e] = ((int64_t)p << 32) | (uint32_t)f;
+    if (ep.inst_ep) {
+      dep = max(dep, ep.inst_ep[f]);
+      ep.free_ep[f] = ep.batch;
+    }
+  }
+  if (ep.inst_ep) {
+    dep = __reduce_max_sync(0xffffffffu, dep);
+    if ((threadIdx.x & 31) == 0 && dep >= 0) atomicMax(&ep.dep[0], dep);
+  }
+}
+
+__global__ void k_install(const int32_t* __restrict__ pages, const int64_t* np_dev, int64_t np_host, uint32_t* bits,
+                          int32_t* frame, const int32_t* __restrict__ fifo, int64_t fifo_head, int64_t C,
+                          int32_t* order_tail, int64_t* mig, Epochs ep, int64_t old_free) {
+  const int64_t n = np_dev ? *np_dev : np_host;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int dep = -1;
+  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
+    const int64_t j = j0 + threadIdx.x;
+    const bool valid = j < n;
+    const int32_t p = valid ? pages[j] : 0;
+    bits_update(bits, p, valid, true);
+    if (!valid) continue;
+    int64_t q = fifo_head + j;
+    if (q >= C) q -= C;
+    if (q >= C) q -= C;
+    const int32_t f = fifo[q];
     frame[p] = f;
     order_tail[j] = p;
     if (mig) mig[j] = ((int64_t)p << 32) | (uint32_t)f;
     if (ep.inst_ep) {
-      if (j < old_free) {
-        int32_t r = ep.free_ep[f];
-        if (r >= 0) atomicMax(&ep.dep[1], r);
-      }
+      if (j < old_free) dep = max(dep, ep.free_ep[f]);
       ep.inst_ep[f] = ep.batch;
     }
+  }
+  if (ep.inst_ep) {
+    dep = __reduce_max_sync(0xffffffffu, dep);
+    if ((threadIdx.x & 31) == 0 && dep >= 0) atomicMax(&ep.dep[1], dep);
   }
 }
 
@@ -1881,18 +1915,6 @@ static void install_pages(Ctx& c, const int32_t* pages, int64_t n, int64_t* mig)
   c.len += n;
 }
 
-static void reorder_with_windows(Ctx& c, const msg_window* win, int32_t nwin, int64_t* win_pages) {
-  WinBuild wb;
-  build_windows(c, win, nwin, wb);
-  WinPtrs wp = win_ptrs(c, nwin, wb);
-  int64_t* hb = c.hbuf.p;
-  MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, c.st));
-  MSG_CUDA(cudaMemcpyAsync(hb + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, c.st));
-  MSG_CUDA(cudaStreamSynchronize(c.st));
-  for (int w = 0; w < nwin; ++w) win_pages[w] = hb[w];
-  multisplit(c, wp.tab, passes_for(hb[nwin]));
-}
-
 static int64_t abs_of(const Ctx& c, int64_t d) {
   auto it = std::upper_bound(c.span_dense.begin(), c.span_dense.end(), d);
   int64_t s = (it - c.span_dense.begin()) - 1;
@@ -1997,25 +2019,6 @@ static void touch_counts(Ctx& c, TaskTab& t, int32_t lo, int32_t hi) {
   units_count(c, c.s.ract.set(), nullptr, c.s.tc.p, nullptr);
 }
 
-// the missing pages of one command in page order, into c.s.miss; returns n
-static int64_t missing_list(Ctx& c, TaskTab& t, int32_t cmd) {
-  int64_t nu = t.act_units[cmd + 1] - t.act_units[cmd];
-  if (t.act_off[cmd + 1] == t.act_off[cmd]) return 0;
-  ranges_from_actual(c, t, cmd, cmd + 1, c.s.ract);
-  c.s.ucnt.resize(std::max<int64_t>(nu, 1), c.st);
-  c.s.uofs.resize(std::max<int64_t>(nu, 1), c.st);
-  c.s.uscr.resize(512, c.st);
-  RangeSet R = c.s.ract.set();
-  units_count(c, R, c.s.ucnt.p, nullptr, nullptr);
-  units_scan(c, R, c.s.ucnt.p, c.s.uofs.p, c.s.uscr.p + 400, c.s.uscr.p);
-  MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, c.s.uscr.p + 400, 8, cudaMemcpyDeviceToHost, c.st));
-  MSG_CUDA(cudaStreamSynchronize(c.st));
-  int64_t n = c.hbuf.p[0];
-  c.s.miss.resize(std::max<int64_t>(n, 1), c.st);
-  units_fill(c, R, c.s.uofs.p, nullptr, c.s.miss.p);
-  return n;
-}
-
 void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_always, msg_switch_out* out,
                  int64_t* win_pages, int64_t* prefix, int64_t* touch_cnt) {
   if (nwin < 1) throw Error(MSG_E_INVAL, "need at least one window");
@@ -2077,16 +2080,18 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   out->populate = out->evict = out->truncated = 0;
   // ---- phase B: reorder (multisplit), plan, apply, migrate
   if (!out->early_exit) {
-    multisplit(c, wp.tab, passes_for(ncls));
-    if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
-    out->free_before = c.C - c.len;
     int64_t pop = S.populate, ev = S.evict;
     out->populate = pop; out->evict = ev; out->truncated = S.truncated;
     if (pop > c.C - c.len + ev) throw Error(MSG_E_CAPACITY, "migration plan overflowed HBM capacity");
-    // populate list against pre-apply residency, truncated at capacity
+    // populate list against pre-apply residency, truncated at capacity (the
+    // reorder does not touch residency, so this runs first and keeps the
+    // stream busy while the host launches the multisplit)
     DVec<int32_t>& poplist = c.s.poplist;
     poplist.resize(std::max<int64_t>(pop, 1), st);
     if (pop) units_fill(c, R, c.s.uofs.p, &c.dstate->populate, poplist.p);
+    multisplit(c, wp.tab, passes_for(ncls));
+    if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
+    out->free_before = c.C - c.len;
     int64_t* mig = mig_buf(c, ev + pop);
     if (c.debug & 3) {
       dump_dense(c, c.order[c.cur].p + c.head, ev, c.dbg[1]);
@@ -2122,16 +2127,50 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   if (cmd < 0 || cmd >= t.ncmd || scan_end > t.ncmd) throw Error(MSG_E_INVAL, "bad command index");
   cudaStream_t st = c.st;
   c.hbuf.reserve(4 * (int64_t)nwin + (scan_end - cmd) + 64);
-  // missing list of cmd against current residency (before any eviction)
-  int64_t n = missing_list(c, t, cmd);
+  // One host round trip for both the missing count of cmd (against current
+  // residency, before any eviction) and, when a refresh reorder follows, the
+  // window class table; then the missing list is filled while the host
+  // launches the reorder, so the multisplit starts on a busy stream.
+  const bool has_iv = t.act_off[cmd + 1] != t.act_off[cmd];
+  const bool refresh = evict > 0 && nwin > 0;
+  RangeSet R{};
+  int64_t* hb = c.hbuf.p;
+  if (has_iv) {
+    int64_t nu = t.act_units[cmd + 1] - t.act_units[cmd];
+    ranges_from_actual(c, t, cmd, cmd + 1, c.s.ract);
+    c.s.ucnt.resize(std::max<int64_t>(nu, 1), st);
+    c.s.uofs.resize(std::max<int64_t>(nu, 1), st);
+    c.s.uscr.resize(512, st);
+    R = c.s.ract.set();
+    units_count(c, R, c.s.ucnt.p, nullptr, nullptr);
+    units_scan(c, R, c.s.ucnt.p, c.s.uofs.p, c.s.uscr.p + 400, c.s.uscr.p);
+    MSG_CUDA(cudaMemcpyAsync(hb, c.s.uscr.p + 400, 8, cudaMemcpyDeviceToHost, st));
+  }
+  WinBuild wb;
+  WinPtrs wp{};
+  if (refresh) {
+    build_windows(c, win, nwin, wb);
+    wp = win_ptrs(c, nwin, wb);
+    MSG_CUDA(cudaMemcpyAsync(hb + 1, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    MSG_CUDA(cudaMemcpyAsync(hb + 1 + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  }
+  if (has_iv || refresh) MSG_CUDA(cudaStreamSynchronize(st));
+  const int64_t n = has_iv ? hb[0] : 0;
+  const int64_t ncls = refresh ? hb[1 + nwin] : 0;
+  if (refresh)
+    for (int w = 0; w < nwin; ++w) win_pages[w] = hb[1 + w];
+  if (n) {
+    c.s.miss.resize(n, st);
+    units_fill(c, R, c.s.uofs.p, nullptr, c.s.miss.p);
+  }
   out->missing = n;
   out->refreshed = 0;
   out->evicted = 0;
   int64_t* mig = mig_buf(c, std::max<int64_t>(evict, 0) + n);
   int64_t ev_done = 0;
   if (evict > 0) {
-    if (nwin > 0) {
-      reorder_with_windows(c, win, nwin, win_pages);
+    if (refresh) {
+      multisplit(c, wp.tab, passes_for(ncls));
       out->refreshed = 1;
       if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     }
