@@ -71,6 +71,7 @@ extern "C" {
 #define MSG_F_MIGRATE 1u       /* perform real host<->HBM copies of planned pages */
 #define MSG_F_VERIFY_TAGS 2u   /* stamp page ids into payloads so migration is checkable */
 #define MSG_F_LOOSE_DOMAIN 4u  /* predictor-only contexts: pages outside the map are allowed (no residency) */
+#define MSG_F_EXECUTE 8u       /* msg_run_command: executed commands also wait for their own in-flight pages */
 
 typedef struct msg_ctx msg_ctx;
 
@@ -164,6 +165,11 @@ typedef struct {
   int64_t ms_passes;
   double ms_ms;
   int64_t ms_bytes;
+  /* executed commands (msg_run_command): count, pages read from the HBM
+   * arena, pages whose payload tag did not match (MSG_F_VERIFY_TAGS), pages
+   * found non-resident, and the consumer stream's busy time (CUDA events) */
+  int64_t run_cmds, run_pages, run_bad_tags, run_missing;
+  double run_ms;
 } msg_stats;
 
 /* Forget all residency (bitmap, list, frames); keep the task tables and the
@@ -216,6 +222,22 @@ int msg_touch(msg_ctx *ctx, int32_t task, int32_t cmd, int64_t evict, const msg_
 /* Demand-paging slice (Mode.um): commands [c0, c1) of `task` processed in
  * order on the device; per command: missing count and capacity evictions. */
 int msg_um_slice(msg_ctx *ctx, int32_t task, int32_t c0, int32_t c1, int64_t *missing_out, int64_t *evicted_out);
+
+/* Execute command `cmd` of `task` on the device (the paper's early-start
+ * gating made real, engine.py:139-158, 342-361, 373-378): on a dedicated
+ * stream, wait until the populate copies of the current switch have landed
+ * up to `need_pages` (the command's gating prefix: demand pages first
+ * accessed by commands <= cmd, in populate order) — and, if this command's
+ * own touch installed pages, until that batch has landed; with MSG_F_EXECUTE
+ * also until every page of its actual set that this switch populates has
+ * landed (a page predicted for a later command but touched by this one is
+ * in flight, and the hardware would stall on it) — then launch a
+ * kernel that reads every page of the command's actual set from its HBM
+ * frame (16-byte loads) and checks the payload tags when the context
+ * verifies them.  Pass need_pages = populate count to wait for the whole
+ * batch (Mode.early_start = False).  Later migrations wait for the executed
+ * commands before they evict or overwrite frames.  Needs MSG_F_MIGRATE. */
+int msg_run_command(msg_ctx *ctx, int32_t task, int32_t cmd, int64_t need_pages);
 
 /* Release a task: drop its pages (absolute page spans) from the list. */
 int msg_release_task(msg_ctx *ctx, const int64_t *span_first, const int64_t *span_end, int32_t nspans,

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "libmsched_b200.so")
 MSG_OK, MSG_E_INVAL, MSG_E_DOMAIN, MSG_E_CAPACITY, MSG_E_OOM, MSG_E_CUDA = 0, -1, -2, -3, -4, -5
 PRED_TEMPLATE, PRED_ALLOCATION, PRED_TRUTH = 0, 1, 2
 CMD_KERNEL, CMD_H2D, CMD_D2H = 0, 1, 2
-F_MIGRATE, F_VERIFY_TAGS, F_LOOSE_DOMAIN = 1, 2, 4
+F_MIGRATE, F_VERIFY_TAGS, F_LOOSE_DOMAIN, F_EXECUTE = 1, 2, 4, 8
 
 EXPORTS = [
     "msg_create", "msg_destroy", "msg_last_error", "msg_stream", "msg_set_domain", "msg_add_task",
@@ -27,6 +27,7 @@ EXPORTS = [
     "msg_um_slice", "msg_release_task", "msg_list_append", "msg_list_madvise", "msg_list_evict_head",
     "msg_list_len", "msg_list_read", "msg_sync", "msg_get_stats", "msg_verify_residency",
     "msg_flush_l2", "msg_list_reorder", "msg_debug", "msg_debug_read", "msg_window_runs", "msg_list_plan", "msg_reset",
+    "msg_run_command",
 ]
 
 
@@ -63,7 +64,8 @@ class Stats(C.Structure):
                 ("h2d_segments", C.c_int64), ("d2h_segments", C.c_int64), ("ce_batches", C.c_int64),
                 ("sm_batches", C.c_int64), ("h2d_busy_ms", C.c_double), ("d2h_busy_ms", C.c_double),
                 ("plan_ms", C.c_double), ("ms_passes", C.c_int64), ("ms_ms", C.c_double),
-                ("ms_bytes", C.c_int64)]
+                ("ms_bytes", C.c_int64), ("run_cmds", C.c_int64), ("run_pages", C.c_int64),
+                ("run_bad_tags", C.c_int64), ("run_missing", C.c_int64), ("run_ms", C.c_double)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}
@@ -121,6 +123,7 @@ def load():
         "msg_get_stats": ([vp, C.POINTER(Stats)], C.c_int),
         "msg_verify_residency": ([vp, C.POINTER(i64)], C.c_int),
         "msg_flush_l2": ([vp], C.c_int),
+        "msg_run_command": ([vp, i32, i32, i64], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -349,6 +352,11 @@ class Context:
         self.check(self.lib.msg_touch(self.h, idx, cmd, evict, warr if nw else None, nw, scan_end,
                                       int(write_tags), C.byref(out), _p(win_pages)))
         return out, win_pages[:nw]
+
+    def run_command(self, idx, cmd, need_pages):
+        """Execute a command on the device once `need_pages` of the current
+        switch's populate have landed (early-start gating)."""
+        self.check(self.lib.msg_run_command(self.h, idx, cmd, int(need_pages)))
 
     def um_slice(self, idx, c0, c1):
         n = c1 - c0

@@ -13,6 +13,8 @@
 //      writing mapped pinned memory with 16-byte accesses.
 #include "msched_internal.cuh"
 
+#include <cuda.h>   // stream memory-op types only; the entry points come from cudaGetDriverEntryPoint
+
 #include <algorithm>
 #include <cstdlib>
 
@@ -22,7 +24,7 @@ constexpr int64_t kTagMagic = 0x5a17c0de00000000ll;
 constexpr int64_t kSegCeMax = 1 << 16;   // CE path limit on segments per batch
 constexpr int64_t kMinCePages = 8;       // average segment size for the CE path (pages)
 
-__device__ __forceinline__ int64_t tag_of(int64_t page) { return kTagMagic ^ page; }
+__host__ __device__ __forceinline__ int64_t tag_of(int64_t page) { return kTagMagic ^ page; }
 
 __global__ void k_seg_mark(const int64_t* list, int64_t n, int64_t n_d2h, int64_t pool_pages, int32_t* flag) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
@@ -88,6 +90,30 @@ __global__ void k_verify(const uint32_t* bits, const int32_t* frame, int64_t D, 
   if (nb) atomicAdd(bad, nb);
 }
 
+// Stream memory operations (populate progress counter written by the H2D
+// stream, waited on by the command stream).  Resolved through the runtime so
+// the library does not link libcuda directly.
+typedef CUresult (*PfnWait64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+typedef CUresult (*PfnWrite64)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+static PfnWait64 p_wait64 = nullptr;
+static PfnWrite64 p_write64 = nullptr;
+
+static void stream_memops_init() {
+  if (p_wait64 && p_write64) return;
+  cudaDriverEntryPointQueryResult q1, q2;
+  MSG_CUDA(cudaGetDriverEntryPoint("cuStreamWaitValue64", reinterpret_cast<void**>(&p_wait64), cudaEnableDefault, &q1));
+  MSG_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue64", reinterpret_cast<void**>(&p_write64), cudaEnableDefault, &q2));
+  if (q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess || !p_wait64 || !p_write64)
+    throw Error(MSG_E_CUDA, "cuStreamWaitValue64 / cuStreamWriteValue64 unavailable");
+}
+
+static void write_progress(Ctx& c, cudaStream_t st, int64_t value) {
+  if (!c.d_progress) return;
+  CUresult r = p_write64(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.d_progress), (cuuint64_t)value,
+                         CU_STREAM_WRITE_VALUE_DEFAULT);
+  if (r != CUDA_SUCCESS) throw Error(MSG_E_CUDA, "cuStreamWriteValue64 failed (" + std::to_string((int)r) + ")");
+}
+
 void migration_init(Ctx& c) {
   MSG_CUDA(cudaStreamCreateWithFlags(&c.st_d2h, cudaStreamNonBlocking));
   MSG_CUDA(cudaStreamCreateWithFlags(&c.st_h2d, cudaStreamNonBlocking));
@@ -118,6 +144,13 @@ void migration_init(Ctx& c) {
   }
   MSG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&c.pool_dev), c.pool, 0));
   if (c.cfg.flags & MSG_F_MIGRATE) {
+    stream_memops_init();
+    MSG_CUDA(cudaStreamCreateWithFlags(&c.st_run, cudaStreamNonBlocking));
+    MSG_CUDA(cudaEventCreateWithFlags(&c.ev_run_last, cudaEventDisableTiming));
+    MSG_CUDA(cudaMalloc(&c.d_progress, 8));
+    MSG_CUDA(cudaMalloc(&c.d_run_acc, 4 * 8));
+    MSG_CUDA(cudaMemsetAsync(c.d_progress, 0, 8, c.st));
+    MSG_CUDA(cudaMemsetAsync(c.d_run_acc, 0, 4 * 8, c.st));
     c.inst_ep.exact(std::max<int64_t>(c.C, 1));
     c.free_ep.exact(std::max<int64_t>(c.C, 1));
     MSG_CUDA(cudaMemsetAsync(c.inst_ep.p, 0xff, c.C * 4, c.st));
@@ -163,6 +196,9 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     c.mig_par ^= 1;
     return;
   }
+  const int64_t base = c.installed_total;   // populate progress before this batch
+  c.installed_total = base + n_h2d;
+  if (c.run_used) run_wait_before_copies(c);
   // 1. segments
   c.s.mflag.resize(n, c.st);
   c.s.moff.resize(n, c.st);
@@ -204,6 +240,7 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     }
     MSG_CHECK_LAUNCH();
     add_launches(2);
+    write_progress(c, c.st_h2d, base + n_h2d);
     MSG_CUDA(cudaEventRecord(h2d_end, c.st_h2d));
     MSG_CUDA(cudaEventRecord(c.ev_h2d_done, c.st_h2d));
     MSG_CUDA(cudaEventRecord(c.ev_d2h_prev, c.st_h2d));
@@ -261,6 +298,18 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     MSG_CUDA(cudaEventRecord(h2d_start, c.st_h2d));
     size_t waited = 0;
     bool any_wait = false;
+    // installs go in populate order; after every flushed copy batch the H2D
+    // stream publishes how many of them have landed (the early-start progress
+    // that executed commands wait on), at least every 1/16 of the batch
+    const int64_t h2d_chunk = std::max<int64_t>((n_h2d + 15) / 16, 256);
+    int64_t issued = 0, published = 0;
+    auto flush_h2d = [&]() {
+      ce_batch(dd, ss, zz, c.st_h2d);
+      if (copy_h2d && issued > published) {
+        write_progress(c, c.st_h2d, base + issued);
+        published = issued;
+      }
+    };
     for (; k < nseg; ++k) {
       int64_t i0, len, page, frame;
       seg_at(k, &i0, &len, &page, &frame);
@@ -269,12 +318,14 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
         size_t need = 0;
         while (need + 1 < done.size() && done[need].first <= e_idx) ++need;
         if (!any_wait || need > waited) {
-          ce_batch(dd, ss, zz, c.st_h2d);
+          flush_h2d();
           MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, done[need].second, 0));
           waited = need;
           any_wait = true;
         }
       }
+      if (copy_h2d && issued - published >= h2d_chunk) flush_h2d();
+      issued = (i0 - n_d2h) + len;
       if (copy_h2d) {
         dd.push_back(c.arena + frame * c.P);
         ss.push_back(c.pool + (page % c.pool_pages) * c.P);
@@ -283,7 +334,7 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
         c.stats.h2d_segments++;
       }
     }
-    ce_batch(dd, ss, zz, c.st_h2d);
+    flush_h2d();
     if (!copy_h2d && (c.cfg.flags & MSG_F_VERIFY_TAGS) && n_h2d) {
       // installs that carry their own data (memcpy): stamp the frames instead
       MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, d2h_end, 0));
@@ -293,6 +344,7 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
       add_launches(1);
       MSG_CUDA(cudaEventRecord(c.ev_mig[par], c.st_h2d));
     }
+    write_progress(c, c.st_h2d, base + n_h2d);
     MSG_CUDA(cudaEventRecord(h2d_end, c.st_h2d));
     MSG_CUDA(cudaEventRecord(c.ev_h2d_done, c.st_h2d));
     MSG_CUDA(cudaEventRecord(c.ev_d2h_prev, c.st_d2h));
@@ -303,6 +355,103 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
   c.mig_batch++;
   c.busy_h2d.push_back({h2d_start, h2d_end});
   c.mig_par ^= 1;
+}
+
+// ---------------------------------------------------------------------------
+// Executed commands: the slice's kernels, started as soon as the populate
+// prefix they need has landed (the paper's GPU trackers + events,
+// PAPER.md:1000-1009; the early-start model of engine.py:139-158, 373-378).
+// Each reads every page of its actual set from its HBM frame.
+
+__global__ void k_consume(const Iv* __restrict__ iv, int64_t n_iv, const int32_t* __restrict__ frame,
+                          const char* __restrict__ arena, int64_t P, int verify, unsigned long long* acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t v16 = P / 16;
+  unsigned long long pages = 0, bad = 0, miss = 0;
+  int4 x = make_int4(0, 0, 0, 0);
+  int64_t skip = 0;
+  for (int64_t r = 0; r < n_iv; ++r) {
+    const Iv v = iv[r];
+    const int64_t np = v.b - v.a;
+    // this warp's first page in range r: global page index = skip + k
+    int64_t k0 = warp - skip % nwarps;
+    if (k0 < 0) k0 += nwarps;
+    for (int64_t k = k0; k < np; k += nwarps) {
+      const int64_t d = v.d + k;
+      const int32_t f = frame[d];
+      if (f < 0) { if (lane == 0) ++miss; continue; }
+      const int4* src = reinterpret_cast<const int4*>(arena + (int64_t)f * P);
+      for (int64_t q = lane; q < v16; q += 32) {
+        int4 y = __ldcs(src + q);
+        x.x ^= y.x; x.y ^= y.y; x.z ^= y.z; x.w ^= y.w;
+      }
+      if (lane == 0) {
+        ++pages;
+        if (verify && *reinterpret_cast<const int64_t*>(arena + (int64_t)f * P) != tag_of(d)) ++bad;
+      }
+    }
+    skip += np;
+  }
+  pages = __reduce_add_sync(0xffffffffu, (unsigned)pages);
+  bad = __reduce_add_sync(0xffffffffu, (unsigned)bad);
+  miss = __reduce_add_sync(0xffffffffu, (unsigned)miss);
+  unsigned sig = __reduce_xor_sync(0xffffffffu, (unsigned)(x.x ^ x.y ^ x.z ^ x.w));
+  if (lane == 0) {
+    if (pages) atomicAdd(&acc[0], pages);
+    if (bad) atomicAdd(&acc[1], bad);
+    if (miss) atomicAdd(&acc[2], miss);
+    atomicXor(&acc[3], (unsigned long long)sig);
+  }
+}
+
+// copies of a new batch must not evict or overwrite frames that executed
+// commands may still be reading
+void run_wait_before_copies(Ctx& c) {
+  MSG_CUDA(cudaStreamWaitEvent(c.st_d2h, c.ev_run_last, 0));
+  MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_run_last, 0));
+}
+
+void run_command(Ctx& c, int32_t task, int32_t cmd, int64_t need_pages) {
+  if (!(c.cfg.flags & MSG_F_MIGRATE) || !c.st_run) throw Error(MSG_E_INVAL, "executing commands needs MSG_F_MIGRATE");
+  if (task < 0 || task >= (int32_t)c.tasks.size() || !c.tasks[task]) throw Error(MSG_E_INVAL, "unknown task");
+  TaskTab& t = *c.tasks[task];
+  if (cmd < 0 || cmd >= t.ncmd) throw Error(MSG_E_INVAL, "bad command index");
+  if (need_pages < 0) throw Error(MSG_E_INVAL, "negative gating prefix");
+  if (c.gate_task == task && cmd >= c.gate_c0 && cmd - c.gate_c0 < (int64_t)c.gate_need.size())
+    need_pages = std::max<int64_t>(need_pages, c.gate_need[cmd - c.gate_c0]);
+  int64_t want = c.switch_base + need_pages;
+  if (c.fault_task == task && c.fault_cmd == cmd) want = std::max(want, c.fault_total);
+  // a wait on a value no issued copy will ever publish would hang the stream
+  if (want > c.installed_total) throw Error(MSG_E_INVAL, "gating prefix beyond the issued populate copies");
+  // the frame table of the plan that made the pages resident
+  cudaEvent_t planned = new_event(c, false);
+  MSG_CUDA(cudaEventRecord(planned, c.st));
+  MSG_CUDA(cudaStreamWaitEvent(c.st_run, planned, 0));
+  if (want > 0) {
+    CUresult r = p_wait64(reinterpret_cast<CUstream>(c.st_run), reinterpret_cast<CUdeviceptr>(c.d_progress),
+                          (cuuint64_t)want, CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) throw Error(MSG_E_CUDA, "cuStreamWaitValue64 failed (" + std::to_string((int)r) + ")");
+  }
+  cudaEvent_t e0 = new_event(c, true), e1 = new_event(c, true);
+  MSG_CUDA(cudaEventRecord(e0, c.st_run));
+  int64_t i0 = t.act_off[cmd], niv = t.act_off[cmd + 1] - i0;
+  int64_t pages = 0;
+  if (niv) {
+    // bitmap-word units bound the page count (enough to size the grid)
+    pages = (t.act_units[cmd + 1] - t.act_units[cmd]) * 32;
+    int blocks = (int)std::min<int64_t>(std::max<int64_t>((pages + 7) / 8, 1), 148 * 8);
+    k_consume<<<blocks, 256, 0, c.st_run>>>(t.act_pool.p + i0, niv, c.frame.p, c.arena, c.P,
+                                             (c.cfg.flags & MSG_F_VERIFY_TAGS) ? 1 : 0, c.d_run_acc);
+    MSG_CHECK_LAUNCH();
+    add_launches(1);
+  }
+  MSG_CUDA(cudaEventRecord(e1, c.st_run));
+  MSG_CUDA(cudaEventRecord(c.ev_run_last, c.st_run));
+  c.busy_run.push_back({e0, e1});
+  c.run_used = true;
+  c.stats.run_cmds++;
 }
 
 void verify_tags(Ctx& c, int64_t* bad) {
@@ -317,8 +466,16 @@ void verify_tags(Ctx& c, int64_t* bad) {
   add_launches(1);
   unsigned long long h = 0;
   MSG_CUDA(cudaMemcpyAsync(&h, d, 8, cudaMemcpyDeviceToHost, c.st));
+  // non-resident pages: their host slot must hold their own payload (an
+  // eviction that copied the wrong frame back would only show up here)
+  std::vector<uint32_t> words((c.D + 31) / 32 + 1);
+  MSG_CUDA(cudaMemcpyAsync(words.data(), c.bits.p, words.size() * 4, cudaMemcpyDeviceToHost, c.st));
   MSG_CUDA(cudaStreamSynchronize(c.st));
   cudaFree(d);
+  for (int64_t p = 0; p < c.D; ++p) {
+    if ((words[p >> 5] >> (p & 31)) & 1u) continue;
+    if (*reinterpret_cast<const int64_t*>(c.pool + p * c.P) != tag_of(p)) ++h;
+  }
   *bad = (int64_t)h;
 }
 

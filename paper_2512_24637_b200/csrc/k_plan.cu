@@ -1690,6 +1690,34 @@ __global__ void k_install(const int32_t* __restrict__ pages, const int64_t* np_d
   }
 }
 
+// MSG_F_EXECUTE: populate position of every page installed by this switch,
+// and per command of the slice the populate prefix its actual set needs
+__global__ void k_pos_scatter(const int32_t* __restrict__ pages, int64_t n, int64_t tag, int64_t* pos_of) {
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < n; j += (int64_t)gridDim.x * blockDim.x)
+    pos_of[pages[j]] = (tag << 32) | j;
+}
+
+__global__ void k_gate_need(const Iv* __restrict__ pool, const int64_t* __restrict__ off, int32_t c0, int32_t c1,
+                            const int64_t* __restrict__ pos_of, int64_t tag, unsigned long long* need) {
+  // one warp per (command, interval) pair, lanes over pages
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t i0 = off[c0], n = off[c1] - i0;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    int32_t a = c0, b = c1;   // command of interval i0 + i
+    while (a < b) { int32_t mid = (a + b) >> 1; if (off[mid + 1] <= i0 + i) a = mid + 1; else b = mid; }
+    const Iv v = pool[i0 + i];
+    unsigned long long m = 0;
+    for (int64_t k = lane; k < v.b - v.a; k += 32) {
+      int64_t x = pos_of[v.d + k];
+      if ((x >> 32) == tag) m = max(m, (unsigned long long)(x & 0xffffffff) + 1);
+    }
+    m = __reduce_max_sync(0xffffffffu, (unsigned)m);
+    if (lane == 0 && m) atomicMax(&need[a - c0], m);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // K8 touch scan: missing pages of each command's actual set (engine.py:396-397)
 
@@ -1893,6 +1921,10 @@ static Epochs epochs(Ctx& c, int64_t* mig) {
 static void evict_head_n(Ctx& c, int64_t n, int64_t* mig) {
   c.batch_old_free = c.fifo_len;   // frames already free before this batch's evictions
   if (n <= 0) return;
+  // executed commands read frames through the frame table: evictions (which
+  // unmap frames) come after every command executed so far, as the fault
+  // handler of a later command runs after the earlier ones finished
+  if (c.run_used) MSG_CUDA(cudaStreamWaitEvent(c.st, c.ev_run_last, 0));
   k_evict_head<<<grid_for(n, 256), 256, 0, c.st>>>(c.order[c.cur].p + c.head, n, c.bits.p, c.frame.p, c.fifo.p,
                                                   c.fifo_head + c.fifo_len, c.C, mig, epochs(c, mig));
   MSG_CHECK_LAUNCH();
@@ -1905,6 +1937,8 @@ static void evict_head_n(Ctx& c, int64_t n, int64_t* mig) {
 // install `n` pages (device list) at the tail
 static void install_pages(Ctx& c, const int32_t* pages, int64_t n, int64_t* mig) {
   if (n <= 0) return;
+  // remapping frames also waits for the commands executed so far (see evict_head_n)
+  if (c.run_used) MSG_CUDA(cudaStreamWaitEvent(c.st, c.ev_run_last, 0));
   k_install<<<grid_for(n, 256), 256, 0, c.st>>>(pages, nullptr, n, c.bits.p, c.frame.p, c.fifo.p, c.fifo_head, c.C,
                                                c.order[c.cur].p + c.head + c.len, mig, epochs(c, mig),
                                                c.batch_old_free);
@@ -2028,7 +2062,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   MSG_CUDA(cudaEventRecord(e0, st));
   TaskTab& t0 = *c.tasks[win[0].task];
   int32_t c0 = win[0].c0, c1 = win[0].c1, ncw = c1 - c0;
-  c.hbuf.reserve(4 * (int64_t)nwin + 2 * (int64_t)ncw + 64);
+  c.hbuf.reserve(4 * (int64_t)nwin + 3 * (int64_t)ncw + 64);
   // ---- phase A: windows, class table, window-0 demand vs residency
   int64_t niv0 = t0.pred_off[c1] - t0.pred_off[c0];
   int64_t nrun_cap = std::max<int64_t>(2 * niv0 + 2, 2);
@@ -2076,6 +2110,8 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   out->missing = S.missing;
   out->nwin = nwin;
   out->early_exit = S.missing == 0 && !reorder_always;
+  c.switch_base = c.installed_total;
+  c.fault_task = -1;
   out->free_before = c.C - c.len;
   out->populate = out->evict = out->truncated = 0;
   // ---- phase B: reorder (multisplit), plan, apply, migrate
@@ -2093,6 +2129,8 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     out->free_before = c.C - c.len;
     int64_t* mig = mig_buf(c, ev + pop);
+    c.switch_base = c.installed_total;   // executed commands gate on this switch's populate
+    c.fault_task = -1;
     if (c.debug & 3) {
       dump_dense(c, c.order[c.cur].p + c.head, ev, c.dbg[1]);
       dump_dense(c, poplist.p, pop, c.dbg[2]);
@@ -2101,6 +2139,29 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     compact_if_needed(c);
     install_pages(c, poplist.p, pop, mig ? mig + ev : nullptr);
     if (mig) migrate_batch(c, ev, pop, out->free_before, true);
+  }
+  // ---- MSG_F_EXECUTE: what each command of the slice physically needs landed
+  const bool gates = (c.cfg.flags & MSG_F_EXECUTE) && ncw > 0;
+  if (gates) {
+    if ((int64_t)c.pos_of.n < c.D) {
+      c.pos_of.exact(std::max<int64_t>(c.D, 1));
+      MSG_CUDA(cudaMemsetAsync(c.pos_of.p, 0xff, c.pos_of.n * 8, st));
+    }
+    ++c.switch_tag;
+    c.s.tb.resize(ncw, st);
+    unsigned long long* need = reinterpret_cast<unsigned long long*>(c.s.tb.p);
+    MSG_CUDA(cudaMemsetAsync(need, 0, ncw * 8, st));
+    if (!out->early_exit && out->populate) {
+      k_pos_scatter<<<grid_for(out->populate, 256), 256, 0, st>>>(c.s.poplist.p, out->populate, c.switch_tag,
+                                                                 c.pos_of.p);
+      int64_t niv = t0.act_off[c1] - t0.act_off[c0];
+      if (niv)
+        k_gate_need<<<grid_for(32 * niv, 256), 256, 0, st>>>(t0.act_pool.p, t0.d_act_off.p, c0, c1, c.pos_of.p,
+                                                            c.switch_tag, need);
+      MSG_CHECK_LAUNCH();
+      add_launches(2);
+    }
+    MSG_CUDA(cudaMemcpyAsync(hb + ncw, need, ncw * 8, cudaMemcpyDeviceToHost, st));
   }
   // ---- K8 touch scan of the slice (post-apply residency)
   touch_counts(c, t0, c0, c1);
@@ -2113,6 +2174,9 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     touch_cnt[k] = hb[k];
     if (hb[k] && out->first_missing < 0) { out->first_missing = c0 + k; out->first_missing_pages = hb[k]; }
   }
+  c.gate_task = gates ? win[0].task : -1;
+  c.gate_c0 = c0;
+  c.gate_need.assign(gates ? hb + ncw : hb, gates ? hb + 2 * ncw : hb);
   out->resident_after = c.len;
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
@@ -2167,6 +2231,9 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   out->refreshed = 0;
   out->evicted = 0;
   int64_t* mig = mig_buf(c, std::max<int64_t>(evict, 0) + n);
+  // frames free BEFORE this batch's evictions: installs beyond them reuse
+  // frames this batch evicts and must wait for those copies back to the host
+  const int64_t free_before = c.C - c.len;
   int64_t ev_done = 0;
   if (evict > 0) {
     if (refresh) {
@@ -2184,9 +2251,9 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     dump_dense(c, c.s.miss.p, n, c.dbg[2]);
   }
   compact_if_needed(c);
-  int64_t free_before = c.C - c.len;
   install_pages(c, c.s.miss.p, n, mig ? mig + ev_done : nullptr);
   if (mig) migrate_batch(c, ev_done, n, free_before, !write_tags);
+  if (n) { c.fault_task = task; c.fault_cmd = cmd; c.fault_total = c.installed_total; }
   out->resident_after = c.len;
   // rescan (cmd, scan_end)
   out->next_missing = -1;
@@ -2302,6 +2369,7 @@ void release_pages(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, 
   split_by_ranges(c, lo, len);   // members (class 1) now at the tail
   int64_t keep = c.len - k;
   const int32_t* gone = c.order[c.cur].p + c.head + keep;
+  if (c.run_used) MSG_CUDA(cudaStreamWaitEvent(c.st, c.ev_run_last, 0));
   k_release_pages<<<grid_for(k, 256), 256, 0, c.st>>>(gone, k, c.bits.p, c.frame.p, c.fifo.p,
                                                       c.fifo_head + c.fifo_len, c.C);
   MSG_CHECK_LAUNCH();

@@ -27,6 +27,7 @@ Ctx::~Ctx() {
   if (st) cudaStreamSynchronize(st);
   if (st_d2h) cudaStreamSynchronize(st_d2h);
   if (st_h2d) cudaStreamSynchronize(st_h2d);
+  if (st_run) cudaStreamSynchronize(st_run);
   for (auto* t : tasks) delete t;
   for (auto e : ev_pool) cudaEventDestroy(e);
   for (auto e : {ev_mig[0], ev_mig[1], ev_h2d_done, ev_plan_done, ev_d2h_prev})
@@ -35,6 +36,10 @@ Ctx::~Ctx() {
   if (pool) cudaFreeHost(pool);
   if (dstate) cudaFree(dstate);
   if (hstate) cudaFreeHost(hstate);
+  if (ev_run_last) cudaEventDestroy(ev_run_last);
+  if (d_progress) cudaFree(d_progress);
+  if (d_run_acc) cudaFree(d_run_acc);
+  if (st_run) cudaStreamDestroy(st_run);
   if (st_d2h) cudaStreamDestroy(st_d2h);
   if (st_h2d) cudaStreamDestroy(st_h2d);
   if (st) cudaStreamDestroy(st);
@@ -314,7 +319,12 @@ int msg_sync(msg_ctx* ctx) {
     MSG_CUDA(cudaStreamSynchronize(c.st));
     if (c.st_d2h) MSG_CUDA(cudaStreamSynchronize(c.st_d2h));
     if (c.st_h2d) MSG_CUDA(cudaStreamSynchronize(c.st_h2d));
+    if (c.st_run) MSG_CUDA(cudaStreamSynchronize(c.st_run));
   });
+}
+
+int msg_run_command(msg_ctx* ctx, int32_t task, int32_t cmd, int64_t need_pages) {
+  return guard(ctx, [&] { run_command(ctx->c, task, cmd, need_pages); });
 }
 
 int msg_get_stats(msg_ctx* ctx, msg_stats* out) {
@@ -323,8 +333,18 @@ int msg_get_stats(msg_ctx* ctx, msg_stats* out) {
     MSG_CUDA(cudaStreamSynchronize(c.st));
     if (c.st_d2h) MSG_CUDA(cudaStreamSynchronize(c.st_d2h));
     if (c.st_h2d) MSG_CUDA(cudaStreamSynchronize(c.st_h2d));
+    if (c.st_run) MSG_CUDA(cudaStreamSynchronize(c.st_run));
     msg_stats s = c.stats;
     s.kernels = kernel_launches();
+    if (c.d_run_acc) {
+      unsigned long long acc[4];
+      MSG_CUDA(cudaMemcpy(acc, c.d_run_acc, sizeof(acc), cudaMemcpyDeviceToHost));
+      s.run_pages = (int64_t)acc[0]; s.run_bad_tags = (int64_t)acc[1]; s.run_missing = (int64_t)acc[2];
+    }
+    double r = 0;
+    for (auto& pr : c.busy_run) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) r += ms; }
+    cudaGetLastError();
+    s.run_ms = r;
     double h = 0, d = 0;
     for (auto& pr : c.busy_h2d) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) h += ms; }
     for (auto& pr : c.busy_d2h) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) d += ms; }
@@ -345,6 +365,11 @@ int msg_reset(msg_ctx* ctx, int32_t keep_tasks) {
     MSG_CUDA(cudaStreamSynchronize(c.st));
     if (c.st_d2h) MSG_CUDA(cudaStreamSynchronize(c.st_d2h));
     if (c.st_h2d) MSG_CUDA(cudaStreamSynchronize(c.st_h2d));
+    if (c.st_run) MSG_CUDA(cudaStreamSynchronize(c.st_run));
+    c.installed_total = 0; c.switch_base = 0; c.fault_task = -1; c.run_used = false;
+    if (c.d_progress) MSG_CUDA(cudaMemsetAsync(c.d_progress, 0, 8, c.st));
+    if (c.d_run_acc) MSG_CUDA(cudaMemsetAsync(c.d_run_acc, 0, 4 * 8, c.st));
+    c.busy_run.clear();
     int64_t words = (std::max<int64_t>(c.D, 1) + 31) / 32 + 1;
     MSG_CUDA(cudaMemsetAsync(c.bits.p, 0, words * 4, c.st));
     k_fill_i32<<<1184, 256, 0, c.st>>>(c.frame.p, std::max<int64_t>(c.D, 1), -1);

@@ -178,6 +178,19 @@ struct Ctx {
   int device = 0;
   cudaStream_t st = nullptr;          // planner stream
   cudaStream_t st_d2h = nullptr, st_h2d = nullptr;
+  cudaStream_t st_run = nullptr;      // executed commands (msg_run_command)
+  unsigned long long* d_progress = nullptr;   // populate pages landed so far (written by the H2D stream)
+  unsigned long long* d_run_acc = nullptr;    // [0] pages read [1] bad tags [2] non-resident
+  int64_t installed_total = 0;        // populate pages whose copies have been issued
+  int64_t switch_base = 0;            // installed_total before the current switch's populate
+  int32_t fault_task = -1, fault_cmd = -1;   // last touch install and the total after its batch
+  int64_t fault_total = 0;
+  cudaEvent_t ev_run_last = nullptr;  // the last executed command
+  DVec<int64_t> pos_of;               // MSG_F_EXECUTE: (switch tag << 32 | populate position) per dense page
+  int32_t switch_tag = 0;
+  int32_t gate_task = -1, gate_c0 = 0;
+  std::vector<int64_t> gate_need;     // per command of the last switch's slice: populate pages its actual set needs
+  bool run_used = false;
   cudaEvent_t ev_plan_done = nullptr, ev_h2d_done = nullptr, ev_d2h_prev = nullptr;
   int64_t P = 4096, C = 0;            // page size, capacity pages
   // dense map
@@ -214,7 +227,7 @@ struct Ctx {
   cudaEvent_t ev_mig[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_pool;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_h2d, busy_d2h;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_plan, busy_ms;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_plan, busy_ms, busy_run;
   msg_stats stats{};
   // parity dumps
   int debug = 0;   // 1: plan lists, 2: full list orders
@@ -263,6 +276,8 @@ void scan_flags(Ctx& c, const int32_t* in, int64_t n, int64_t* out);   // exclus
 void migration_init(Ctx& c);
 void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bool copy_h2d);
 void verify_tags(Ctx& c, int64_t* bad);
+void run_command(Ctx& c, int32_t task, int32_t cmd, int64_t need_pages);
+void run_wait_before_copies(Ctx& c);
 
 int64_t kernel_launches();
 void add_launches(int64_t n);

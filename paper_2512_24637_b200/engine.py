@@ -199,12 +199,17 @@ class Simulator:
       device     CUDA device ordinal
       recorder   list receiving per-switch planner records (parity dumps)
       host_pool_pages  bound the pinned backing store (pages alias beyond it)
+      execute    run every executed command on the device as a kernel that
+                 reads its pages from HBM, gated by stream waits on the
+                 populate progress of the switch (early start when
+                 Mode.early_start, else after the whole batch); needs migrate
     """
 
     def __init__(self, tasks: Sequence[Task], hw: HwConfig, policy: Policy, mode: Mode,
                  feeder: Optional[Callable[["Simulator"], None]] = None, record_events: bool = False, *,
                  migrate: bool = False, verify: bool = False, device: int = 0, recorder: list | None = None,
-                 host_pool_pages: int = 0, descriptors: dict | None = None, order_every: int = 1):
+                 host_pool_pages: int = 0, descriptors: dict | None = None, order_every: int = 1,
+                 execute: bool = False):
         self.hw, self.policy, self.mode, self.feeder = hw, policy, mode, feeder
         self.page = hw.page_size_bytes
         self.capacity = hw.hbm_capacity_pages
@@ -213,6 +218,11 @@ class Simulator:
         self.recorder = recorder
         self.order_every = max(1, order_every)   # dump the full list order every k-th reorder
         self._descriptors = descriptors
+        if execute and not migrate:
+            raise ValueError("execute=True needs migrate=True (commands read their migrated pages)")
+        if execute and mode.name not in ("proactive", "ideal"):
+            raise ValueError("execute=True is defined for the proactive and ideal modes")
+        self.execute = execute
         self.ctx = None
         self._host_state()
         total_alloc = sum(a.size_bytes for t in self.tasks for a in t.allocations)
@@ -227,7 +237,8 @@ class Simulator:
             self._pred = _abi.PRED_ALLOCATION
         else:
             self._pred = _abi.PRED_TEMPLATE
-        flags = (_abi.F_MIGRATE if migrate else 0) | (_abi.F_VERIFY_TAGS if verify else 0)
+        flags = (_abi.F_MIGRATE if migrate else 0) | (_abi.F_VERIFY_TAGS if verify else 0) | \
+            (_abi.F_EXECUTE if execute else 0)
         self.ctx = _abi.Context(self.page, self.capacity, predictor=self._pred, device=device, flags=flags,
                                 host_pool_pages=host_pool_pages)
         self.ctx.set_domain(domain_spans(self.tasks, self.page))
@@ -393,7 +404,7 @@ class Simulator:
                    "windows": [[self.tasks[t].id, a, b] for t, a, b in windows], "missing": int(out.missing)}
             self.recorder.append(rec)
         state = {"windows": windows, "next_missing": out.first_missing,
-                 "next_missing_pages": out.first_missing_pages, "pending": None}
+                 "next_missing_pages": out.first_missing_pages, "pending": None, "gate": None}
         if out.early_exit:
             self._resident = out.resident_after
             return state
@@ -413,6 +424,17 @@ class Simulator:
             self.metrics.plan_truncations += 1
         self.metrics.migrated_in_pages += n_pop
         self.metrics.migrated_out_pages += n_ev
+        if self.execute:   # executed commands wait for their prefix, or the whole batch
+            c0, c1 = windows[0][1], windows[0][2]
+            if self.mode.pipelined and self.mode.early_start:
+                pop, cum, gate = self._selfpop[entry.task_id], 0, {}
+                for c in range(c0, c1):
+                    if not pop[c]:
+                        cum += int(prefix_cnt[c - c0])
+                    gate[c] = min(cum, n_pop)
+                state["gate"] = gate
+            else:
+                state["gate"] = {c: n_pop for c in range(c0, c1)}
         self._emit("migrate", entry.task_id, n_pop)
         if not self.mode.pipelined:
             self._charge(sequential_time(self.hw, n_ev, n_pop), "migration_s")
@@ -464,6 +486,9 @@ class Simulator:
                     self.metrics.migration_s += ready - offset
                     offset = ready
             offset += self._touch(task, cmd, cur, timeline, state, budget - elapsed, um)
+            if self.execute:
+                gate = state["gate"] if state else None
+                self.ctx.run_command(self._idx[task.id], cur, gate.get(cur, 0) if gate else 0)
             offset += cmd.latency_s
             elapsed += cmd.latency_s
             task.cursor = cur + 1
