@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-plan-only", action="store_true")
     ap.add_argument("--skip-large", action="store_true", help="skip the config-4-size multisplit roofline leg")
+    ap.add_argument("--skip-execute", action="store_true", help="skip the executed-commands (early-start) leg")
     return ap.parse_args()
 
 
@@ -398,6 +399,26 @@ def main():
         plan_only = {"value": pages_step / (p_ms / 1e3), "unit": UNIT, "ms_per_step": p_ms,
                      "multisplit_ms_per_step": pst["ms_ms"], "planner_ms_per_step": pst["plan_ms"],
                      "note": "replay with migration off: the reference's own work (plans + modeled timing)"}
+    # executed commands: every command of every slice runs on the device as a
+    # kernel reading its pages from HBM, gated by stream waits on the
+    # populate progress -- early start (prefix) vs the whole batch
+    execute = None
+    if not args.skip_execute and migrate:
+        execute = {}
+        for label, early in (("early_start", True), ("whole_batch", False)):
+            sim.close()
+            sim = engine.Simulator(tasks, hw, pol, engine.Mode.proactive(early_start=early), migrate=True,
+                                   device=local, descriptors=descs, host_pool_pages=pool_pages, execute=True)
+            stream = torch.cuda.ExternalStream(sim.ctx.stream(), device=dev)
+            one_step()
+            e_times = [one_step()[0] for _ in range(max(1, min(args.steps, 2)))]
+            est = sim.ctx.stats()
+            execute[label] = {"ms_per_step": max_over_ranks(torch, statistics.mean(e_times), ws, dev),
+                              "commands": est["run_cmds"], "pages_read": est["run_pages"],
+                              "consumer_busy_ms": est["run_ms"], "bad_payloads": est["run_bad_tags"],
+                              "non_resident_reads": est["run_missing"]}
+        execute["note"] = ("each executed command reads every page of its actual set from HBM after a "
+                           "cuStreamWaitValue64 on the populate progress the H2D stream publishes")
     if rank != 0:
         barrier_done = True  # noqa: F841
         sim.close()
@@ -458,6 +479,7 @@ def main():
         "migration": mig,
         "planner_ms_per_step": st["plan_ms"],
         "plan_only": plan_only,
+        "execute": execute,
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": int(launches),
