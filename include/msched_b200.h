@@ -236,7 +236,8 @@ int msg_um_slice(msg_ctx *ctx, int32_t task, int32_t c0, int32_t c1, int64_t *mi
  * frame (16-byte loads) and checks the payload tags when the context
  * verifies them.  Pass need_pages = populate count to wait for the whole
  * batch (Mode.early_start = False).  Later migrations wait for the executed
- * commands before they evict or overwrite frames.  Needs MSG_F_MIGRATE. */
+ * commands before they evict or overwrite frames.  Needs MSG_F_MIGRATE and
+ * MSG_F_EXECUTE (the H2D stream publishes populate progress only then). */
 int msg_run_command(msg_ctx *ctx, int32_t task, int32_t cmd, int64_t need_pages);
 
 /* Release a task: drop its pages (absolute page spans) from the list. */

@@ -108,7 +108,7 @@ static void stream_memops_init() {
 }
 
 static void write_progress(Ctx& c, cudaStream_t st, int64_t value) {
-  if (!c.d_progress) return;
+  if (!c.d_progress || !(c.cfg.flags & MSG_F_EXECUTE)) return;
   CUresult r = p_write64(reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(c.d_progress), (cuuint64_t)value,
                          CU_STREAM_WRITE_VALUE_DEFAULT);
   if (r != CUDA_SUCCESS) throw Error(MSG_E_CUDA, "cuStreamWriteValue64 failed (" + std::to_string((int)r) + ")");
@@ -301,11 +301,12 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     // installs go in populate order; after every flushed copy batch the H2D
     // stream publishes how many of them have landed (the early-start progress
     // that executed commands wait on), at least every 1/16 of the batch
-    const int64_t h2d_chunk = std::max<int64_t>((n_h2d + 15) / 16, 256);
+    const bool publish = (c.cfg.flags & MSG_F_EXECUTE) != 0;   // only executed commands read the progress
+    const int64_t h2d_chunk = publish ? std::max<int64_t>((n_h2d + 15) / 16, 256) : INT64_MAX;
     int64_t issued = 0, published = 0;
     auto flush_h2d = [&]() {
       ce_batch(dd, ss, zz, c.st_h2d);
-      if (copy_h2d && issued > published) {
+      if (publish && copy_h2d && issued > published) {
         write_progress(c, c.st_h2d, base + issued);
         published = issued;
       }
@@ -414,7 +415,8 @@ void run_wait_before_copies(Ctx& c) {
 }
 
 void run_command(Ctx& c, int32_t task, int32_t cmd, int64_t need_pages) {
-  if (!(c.cfg.flags & MSG_F_MIGRATE) || !c.st_run) throw Error(MSG_E_INVAL, "executing commands needs MSG_F_MIGRATE");
+  if (!(c.cfg.flags & MSG_F_MIGRATE) || !(c.cfg.flags & MSG_F_EXECUTE) || !c.st_run)
+    throw Error(MSG_E_INVAL, "executing commands needs MSG_F_MIGRATE | MSG_F_EXECUTE");
   if (task < 0 || task >= (int32_t)c.tasks.size() || !c.tasks[task]) throw Error(MSG_E_INVAL, "unknown task");
   TaskTab& t = *c.tasks[task];
   if (cmd < 0 || cmd >= t.ncmd) throw Error(MSG_E_INVAL, "bad command index");
