@@ -25,9 +25,12 @@ import math
 from dataclasses import dataclass, field
 from typing import Callable, Optional, Sequence
 
+import numpy as np
+
 from . import _abi
 from .analyzer import build_descriptors
 from .model import CommandKind, HwConfig, PageSet, Task
+from .tracebin import ColumnarTask, CommandColumns, encode_columns, kernel_ids_for
 from .scheduler import Policy, TimelineEntry, build_timeline, project_cursor
 
 __all__ = [
@@ -164,6 +167,9 @@ def um_command_duration(hw: HwConfig, cmd, missing_pages: int, prefetch_pages: i
 
 
 def _copy_task(t: Task) -> Task:
+    if isinstance(t.commands, CommandColumns):   # binary traces stay columnar (read-only columns)
+        return ColumnarTask(id=t.id, allocations=t.allocations, commands=t.commands, cursor=t.cursor,
+                            priority=t.priority, arrival_s=t.arrival_s)
     return Task(id=t.id, allocations=t.allocations, commands=list(t.commands), cursor=t.cursor,
                 priority=t.priority, arrival_s=t.arrival_s)
 
@@ -181,6 +187,9 @@ def domain_spans(tasks, page: int) -> list:
             lo, hi = _page_span(a, page)
             if hi > lo:
                 spans.append((lo, hi))
+        if isinstance(t.commands, CommandColumns):
+            spans.extend(_column_spans(t.commands, page))
+            continue
         for c in t.commands:
             for r in c.ground_truth_access:
                 spans.append((r.start_addr // page, (r.start_addr + r.length_bytes - 1) // page + 1))
@@ -188,6 +197,14 @@ def domain_spans(tasks, page: int) -> list:
                 d = c.device_range()
                 spans.append((d.start_addr // page, (d.end_addr - 1) // page + 1))
     return spans
+
+
+def _column_spans(cols: CommandColumns, page: int) -> list:
+    """domain_spans for a columnar task: ground-truth ranges and memcpy extents."""
+    out = [(a // page, (a + n - 1) // page + 1) for a, n in zip(cols.gts["start"].tolist(), cols.gts["len"].tolist())]
+    mem = cols.cmds[(cols.cmds["kind"] != _abi.CMD_KERNEL) & (cols.cmds["dev_len"] > 0)]
+    out.extend((a // page, (a + n - 1) // page + 1) for a, n in zip(mem["dev_addr"].tolist(), mem["dev_len"].tolist()))
+    return out
 
 
 class Simulator:
@@ -259,8 +276,14 @@ class Simulator:
         self.t = 0.0
         self.events: list = []
         self._idx = {t.id: i for i, t in enumerate(self.tasks)}
-        self._lat = {t.id: [c.latency_s for c in t.commands] for t in self.tasks}
-        self._selfpop = {t.id: [c.kind is CommandKind.MEMCPY_H2D for c in t.commands] for t in self.tasks}
+        self._lat, self._selfpop = {}, {}
+        for t in self.tasks:
+            if isinstance(t.commands, CommandColumns):
+                self._lat[t.id] = t.commands.lat.tolist()
+                self._selfpop[t.id] = (t.commands.kinds() == _abi.CMD_H2D).tolist()
+            else:
+                self._lat[t.id] = [c.latency_s for c in t.commands]
+                self._selfpop[t.id] = [c.kind is CommandKind.MEMCPY_H2D for c in t.commands]
         self._resident = 0
         self._nreorder = 0
         self._nrefresh = 0
@@ -275,7 +298,8 @@ class Simulator:
             self.ctx.add_task(i, [(a.base_addr, a.size_bytes) for a in t.allocations])
             kid, lossy = {}, []
             if self._pred == _abi.PRED_TEMPLATE and self.mode.name == "proactive":
-                descs = (self._descriptors or {}).get(t.id) or build_descriptors(t)
+                descs = (self._descriptors or {}).get(t.id) or getattr(t, "descriptors", None) or \
+                    build_descriptors(t)
                 names, rules, offs, lossy = _abi.lower_rules(descs)
                 kid = {n: k for k, n in enumerate(names)}
                 self.ctx.set_rules(i, rules, offs)
@@ -301,6 +325,13 @@ class Simulator:
         if not commands:
             return
         kid = self._kernel_ids[task.id]
+        if isinstance(commands, CommandColumns):   # binary trace: the columns are the ABI tables
+            comp = self.ctx.add_commands(self._idx[task.id], encode_columns(commands, kid))
+            k = kernel_ids_for(commands, kid)
+            lossy = np.asarray(list(self._lossy[task.id]) + [False], dtype=bool)
+            bad = (commands.kinds() == _abi.CMD_KERNEL) & (k >= 0) & lossy[np.where(k >= 0, k, len(lossy) - 1)]
+            self.complete[task.id].extend((comp.astype(bool) & ~bad).tolist())
+            return
         comp = self.ctx.add_commands(self._idx[task.id], _abi.encode_commands(commands, kid))
         lossy = self._lossy[task.id]
         for c, ok in zip(commands, comp):
@@ -311,6 +342,8 @@ class Simulator:
         task = self.by_id[task_id]
         if task.remaining() == 0 and task.commands:
             raise SimulationError(f"cannot append to completed task {task_id!r}")
+        if isinstance(task.commands, CommandColumns):
+            task.commands = list(task.commands)   # a fed task becomes a plain command list
         commands = list(commands)
         task.commands.extend(commands)
         self._lat[task_id].extend(c.latency_s for c in commands)
@@ -476,21 +509,21 @@ class Simulator:
                 raise
             if self.recorder is not None:
                 self._um_records(task.id, self.ctx.debug_read(3))
+        lat, selfpop = self._lat[task.id], self._selfpop[task.id]
         while task.cursor < len(task.commands) and elapsed < budget:
             cur = task.cursor
-            cmd = task.commands[cur]
             if pending is not None:
                 j = pending["prefix"].get(cur, 0)
                 ready = populate_ready(self.hw, j, pending["free"], pending["n_evict"])
                 if ready > offset:
                     self.metrics.migration_s += ready - offset
                     offset = ready
-            offset += self._touch(task, cmd, cur, timeline, state, budget - elapsed, um)
+            offset += self._touch(task, selfpop[cur], cur, timeline, state, budget - elapsed, um)
             if self.execute:
                 gate = state["gate"] if state else None
                 self.ctx.run_command(self._idx[task.id], cur, gate.get(cur, 0) if gate else 0)
-            offset += cmd.latency_s
-            elapsed += cmd.latency_s
+            offset += lat[cur]
+            elapsed += lat[cur]
             task.cursor = cur + 1
         if pending is not None and pending["evict_done"] > offset:
             self.metrics.migration_s += pending["evict_done"] - offset
@@ -514,7 +547,7 @@ class Simulator:
         if n > self.capacity:
             raise SimulationError(f"command working set ({n} pages) exceeds HBM capacity ({self.capacity} pages)")
 
-    def _touch(self, task, cmd, cur, timeline, state, remaining_budget, um) -> float:
+    def _touch(self, task, is_h2d, cur, timeline, state, remaining_budget, um) -> float:
         name = self.mode.name
         if name == "reference":
             return 0.0
@@ -525,7 +558,7 @@ class Simulator:
                 return 0.0
             self.metrics.evicted_capacity_pages += int(ev[cur - c0])
             stall = 0.0
-            if cmd.kind is CommandKind.MEMCPY_H2D:
+            if is_h2d:
                 self.metrics.memcpy_installed_pages += n
             else:
                 stall += self._fault(n)
@@ -549,8 +582,7 @@ class Simulator:
             dump_order = self._nrefresh % self.order_every == 0
             self._nrefresh += 1
             self.ctx.debug(3 if dump_order else 1)
-        out, win_pages = self.ctx.touch(self._idx[task.id], cur, max(over, 0), wins, scan_end,
-                                        cmd.kind is CommandKind.MEMCPY_H2D)
+        out, win_pages = self.ctx.touch(self._idx[task.id], cur, max(over, 0), wins, scan_end, bool(is_h2d))
         if over > 0:
             if self.recorder is not None:
                 r = {"ev": "refresh", "task": task.id, "cmd": cur,
@@ -564,7 +596,7 @@ class Simulator:
                 self.metrics.madvise_s += dt
                 stall += dt
             self.metrics.evicted_capacity_pages += int(out.evicted)
-        if cmd.kind is CommandKind.MEMCPY_H2D:
+        if is_h2d:
             self.metrics.memcpy_installed_pages += n
         else:
             stall += self._fault(n)
