@@ -260,10 +260,13 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
       *page = segs[2 * k + 1] >> 32;
       *frame = (int64_t)(uint32_t)(segs[2 * k + 1] & 0xffffffff);
     };
-    // evictions, in chunks; each chunk's completion is an event that gates
-    // the installs reusing its frames
-    static const int kChunks = getenv("MSG_MIG_CHUNKS") ? atoi(getenv("MSG_MIG_CHUNKS")) : 8;
-    int64_t chunk = std::max<int64_t>((n_d2h + kChunks - 1) / kChunks, 1);
+    // evictions, in chunks of ~64 MiB (8..128 per batch); each chunk's
+    // completion is an event that gates the installs reusing its frames.
+    // Segments are split at chunk boundaries, so one huge contiguous segment
+    // (2 MiB pages, whole GEMM operands) still pipelines.
+    static const int64_t kChunkBytes = getenv("MSG_MIG_CHUNK_MB") ? atoll(getenv("MSG_MIG_CHUNK_MB")) << 20 : 64ll << 20;
+    int64_t nchunks = std::min<int64_t>(std::max<int64_t>((n_d2h * c.P + kChunkBytes - 1) / kChunkBytes, 8), 128);
+    int64_t chunk = std::max<int64_t>((n_d2h + nchunks - 1) / nchunks, 1);
     std::vector<std::pair<int64_t, cudaEvent_t>> done;   // (evictions complete up to, event)
     std::vector<void*> dd, ss;
     std::vector<size_t> zz;
@@ -275,17 +278,21 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
       int64_t i0, len, page, frame;
       seg_at(k, &i0, &len, &page, &frame);
       if (i0 >= n_d2h) break;
-      dd.push_back(c.pool + (page % c.pool_pages) * c.P);
-      ss.push_back(c.arena + frame * c.P);
-      zz.push_back((size_t)(len * c.P));
-      c.stats.d2h_bytes += len * c.P;
-      c.stats.d2h_segments++;
-      if (i0 + len >= next_cut && i0 + len < n_d2h) {
-        ce_batch(dd, ss, zz, c.st_d2h);
-        cudaEvent_t e = new_event(c, false);
-        MSG_CUDA(cudaEventRecord(e, c.st_d2h));
-        done.push_back({i0 + len, e});
-        next_cut = ((i0 + len) / chunk + 1) * chunk;
+      for (int64_t pos = i0; pos < i0 + len;) {
+        int64_t take = std::min(i0 + len, next_cut) - pos;
+        dd.push_back(c.pool + ((page + (pos - i0)) % c.pool_pages) * c.P);
+        ss.push_back(c.arena + (frame + (pos - i0)) * c.P);
+        zz.push_back((size_t)(take * c.P));
+        c.stats.d2h_bytes += take * c.P;
+        c.stats.d2h_segments++;
+        pos += take;
+        if (pos == next_cut && pos < n_d2h) {
+          ce_batch(dd, ss, zz, c.st_d2h);
+          cudaEvent_t e = new_event(c, false);
+          MSG_CUDA(cudaEventRecord(e, c.st_d2h));
+          done.push_back({pos, e});
+          next_cut += chunk;
+        }
       }
     }
     ce_batch(dd, ss, zz, c.st_d2h);
@@ -314,25 +321,34 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     for (; k < nseg; ++k) {
       int64_t i0, len, page, frame;
       seg_at(k, &i0, &len, &page, &frame);
-      int64_t e_idx = (i0 - n_d2h) + len - 1 - free_before;   // last eviction this segment depends on
-      if (e_idx >= 0) {
-        size_t need = 0;
-        while (need + 1 < done.size() && done[need].first <= e_idx) ++need;
-        if (!any_wait || need > waited) {
-          flush_h2d();
-          MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, done[need].second, 0));
-          waited = need;
-          any_wait = true;
+      for (int64_t pos = i0; pos < i0 + len;) {
+        // install j = pos - n_d2h reuses the frame of eviction j - free_before;
+        // cut pieces where that eviction index crosses a chunk boundary
+        int64_t j = pos - n_d2h, take = i0 + len - pos;
+        int64_t e0 = j - free_before;
+        if (e0 < 0) take = std::min(take, -e0);                       // frames free before the batch
+        else take = std::min(take, (e0 / chunk + 1) * chunk - e0);   // up to the next chunk boundary
+        int64_t e_idx = e0 + take - 1;   // last eviction this piece depends on
+        if (e_idx >= 0) {
+          size_t need = 0;
+          while (need + 1 < done.size() && done[need].first <= e_idx) ++need;
+          if (!any_wait || need > waited) {
+            flush_h2d();
+            MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, done[need].second, 0));
+            waited = need;
+            any_wait = true;
+          }
         }
-      }
-      if (copy_h2d && issued - published >= h2d_chunk) flush_h2d();
-      issued = (i0 - n_d2h) + len;
-      if (copy_h2d) {
-        dd.push_back(c.arena + frame * c.P);
-        ss.push_back(c.pool + (page % c.pool_pages) * c.P);
-        zz.push_back((size_t)(len * c.P));
-        c.stats.h2d_bytes += len * c.P;
-        c.stats.h2d_segments++;
+        if (copy_h2d && issued - published >= h2d_chunk) flush_h2d();
+        issued = j + take;
+        if (copy_h2d) {
+          dd.push_back(c.arena + (frame + (pos - i0)) * c.P);
+          ss.push_back(c.pool + ((page + (pos - i0)) % c.pool_pages) * c.P);
+          zz.push_back((size_t)(take * c.P));
+          c.stats.h2d_bytes += take * c.P;
+          c.stats.h2d_segments++;
+        }
+        pos += take;
       }
     }
     flush_h2d();
