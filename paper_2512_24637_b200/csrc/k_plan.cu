@@ -1513,6 +1513,19 @@ static void scan_i32_to_i64(Ctx& c, const int32_t* in, int64_t n, int64_t* out) 
 
 void scan_flags(Ctx& c, const int32_t* in, int64_t n, int64_t* out) { scan_i32_to_i64(c, in, n, out); }
 
+int32_t* next_barrier(Ctx& c) {
+  if (!c.ms_ctr.p) {
+    c.ms_ctr.exact(1 << 16);
+    c.ms_tot.exact(257 * MS_MAX_PASSES);
+  }
+  if (++c.ms_epoch >= (1u << 16)) {   // epochs wrap: clear the look-back status words too
+    if (c.ms_status.p) MSG_CUDA(cudaMemsetAsync(c.ms_status.p, 0, c.ms_status.n * 8, c.st));
+    c.ms_epoch = 1;
+  }
+  if (c.ms_epoch == 1) MSG_CUDA(cudaMemsetAsync(c.ms_ctr.p, 0, (1 << 16) * 4, c.st));
+  return c.ms_ctr.p + c.ms_epoch;
+}
+
 // Stable multisplit of order[cur][head, head+len) by class digits; result
 // at order[cur^1][0, len) (one buffer swap per pass).  `passes` LSD passes.
 static void multisplit(Ctx& c, const SegTab& T, int passes) {
@@ -1570,24 +1583,20 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     c.ms_tot_par = 0;
   }
   for (int pass = 0; pass < passes; ++pass) {
-    if (++c.ms_epoch >= (1u << 16)) {   // epochs wrap: clear the status words
-      MSG_CUDA(cudaMemsetAsync(c.ms_status.p, 0, c.ms_status.n * 8, c.st));
-      c.ms_epoch = 1;
-    }
-    if (c.ms_epoch == 1) MSG_CUDA(cudaMemsetAsync(c.ms_ctr.p, 0, (1 << 16) * 4, c.st));
+    int32_t* bar = next_barrier(c);   // also the onesweep tile counter of this pass
     const int32_t* src = c.order[c.cur].p + c.head;
     int32_t* dst = c.order[c.cur ^ 1].p;
     if (coop) {
       int32_t* totb = c.ms_hist.p + 256 * (int64_t)coop_grid;
       const int32_t a = (int32_t)((reinterpret_cast<uintptr_t>(src) & 15) >> 2);
       McArgs A{src - a, n + a, a, T, 8 * pass, dst, c.ms_hist.p, totb + 256 * c.ms_tot_par,
-               totb + 256 * (c.ms_tot_par ^ 1), c.ms_ctr.p + c.ms_epoch, E, (int32_t)vcap, (int32_t)nch};
+               totb + 256 * (c.ms_tot_par ^ 1), bar, E, (int32_t)vcap, (int32_t)nch};
       c.ms_tot_par ^= 1;
       void* args[] = {&A};
       MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS),
                                            args, MC_SMEM, c.st));
     } else {
-      Onesweep O{c.ms_status.p, (int64_t)(c.ms_status.n / 256), c.ms_ctr.p + c.ms_epoch, tot + 257 * pass,
+      Onesweep O{c.ms_status.p, (int64_t)(c.ms_status.n / 256), bar, tot + 257 * pass,
                  c.ms_epoch};
       int grid = (int)std::min<int64_t>(ntiles, grid_cap);
       k_ms_onesweep<<<grid, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, dst, O);
@@ -2047,10 +2056,7 @@ void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_
 static void touch_counts(Ctx& c, TaskTab& t, int32_t lo, int32_t hi) {
   int32_t n = hi - lo;
   c.s.tc.resize(std::max(n, 1), c.st);
-  MSG_CUDA(cudaMemsetAsync(c.s.tc.p, 0, std::max(n, 1) * sizeof(int64_t), c.st));
-  if (n <= 0 || t.act_off[hi] == t.act_off[lo]) return;
-  ranges_from_actual(c, t, lo, hi, c.s.ract);
-  units_count(c, c.s.ract.set(), nullptr, c.s.tc.p, nullptr);
+  touch_counts_dev(c, t, lo, hi, c.s.tc.p);
 }
 
 void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_always, msg_switch_out* out,
@@ -2072,11 +2078,12 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   WinBuild wb;
   const bool dem_done = build_windows(c, win, nwin, wb, &dem_out);
   WinPtrs wp = win_ptrs(c, nwin, wb);
-  c.s.ucnt.resize(units_cap, st);
-  c.s.uofs.resize(units_cap, st);
   c.s.uscr.resize(512 + ncw, st);
   int64_t* pref_d = c.s.uscr.p + 512;   // per-command gating counts
   int64_t* total_d = c.s.uscr.p + 400;
+  // populate list (pre-apply residency, first-access order, capacity-capped)
+  DVec<int32_t>& poplist = c.s.poplist;
+  poplist.resize(std::max<int64_t>(std::min<int64_t>(32 * units_cap, c.C), 1), st);
   DemandParams D{};
   D.run_a = wp.run_a; D.run_b = wp.run_b; D.run_lab = wp.run_lab;
   D.run_base = 0;  // window 0's scratch region starts at offset 0
@@ -2086,17 +2093,13 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   D.nspans = (int32_t)c.span_first.size();
   D.R = c.s.rdem.out();
   RangeSet R = c.s.rdem.set();
-  if (ncw) MSG_CUDA(cudaMemsetAsync(pref_d, 0, ncw * sizeof(int64_t), st));
   if (!dem_done) {
     k_demand_collect<<<1, 1024, 0, st>>>(D);
     MSG_CHECK_LAUNCH();
     add_launches(1);
   }
-  units_count(c, R, c.s.ucnt.p, pref_d, nullptr);
-  units_scan(c, R, c.s.ucnt.p, c.s.uofs.p, total_d, c.s.uscr.p);
-  k_plan_scalars<<<1, 1, 0, st>>>(total_d, c.dstate, c.C, c.len);
-  MSG_CHECK_LAUNCH();
-  add_launches(1);
+  // missing = demand - resident, gating counts, plan scalars, populate list
+  units_plan(c, R, units_cap, ncw ? pref_d : nullptr, ncw, c.C, poplist.p, c.C, total_d);
   int64_t* hb = c.hbuf.p;
   MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -2119,12 +2122,6 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     int64_t pop = S.populate, ev = S.evict;
     out->populate = pop; out->evict = ev; out->truncated = S.truncated;
     if (pop > c.C - c.len + ev) throw Error(MSG_E_CAPACITY, "migration plan overflowed HBM capacity");
-    // populate list against pre-apply residency, truncated at capacity (the
-    // reorder does not touch residency, so this runs first and keeps the
-    // stream busy while the host launches the multisplit)
-    DVec<int32_t>& poplist = c.s.poplist;
-    poplist.resize(std::max<int64_t>(pop, 1), st);
-    if (pop) units_fill(c, R, c.s.uofs.p, &c.dstate->populate, poplist.p);
     multisplit(c, wp.tab, passes_for(ncls));
     if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     out->free_before = c.C - c.len;
@@ -2202,12 +2199,10 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   if (has_iv) {
     int64_t nu = t.act_units[cmd + 1] - t.act_units[cmd];
     ranges_from_actual(c, t, cmd, cmd + 1, c.s.ract);
-    c.s.ucnt.resize(std::max<int64_t>(nu, 1), st);
-    c.s.uofs.resize(std::max<int64_t>(nu, 1), st);
     c.s.uscr.resize(512, st);
+    c.s.miss.resize(std::max<int64_t>(32 * nu, 1), st);
     R = c.s.ract.set();
-    units_count(c, R, c.s.ucnt.p, nullptr, nullptr);
-    units_scan(c, R, c.s.ucnt.p, c.s.uofs.p, c.s.uscr.p + 400, c.s.uscr.p);
+    units_plan(c, R, nu, nullptr, 0, -1, c.s.miss.p, -1, c.s.uscr.p + 400);
     MSG_CUDA(cudaMemcpyAsync(hb, c.s.uscr.p + 400, 8, cudaMemcpyDeviceToHost, st));
   }
   WinBuild wb;
@@ -2223,10 +2218,6 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   const int64_t ncls = refresh ? hb[1 + nwin] : 0;
   if (refresh)
     for (int w = 0; w < nwin; ++w) win_pages[w] = hb[1 + w];
-  if (n) {
-    c.s.miss.resize(n, st);
-    units_fill(c, R, c.s.uofs.p, nullptr, c.s.miss.p);
-  }
   out->missing = n;
   out->refreshed = 0;
   out->evicted = 0;
@@ -2612,17 +2603,12 @@ void list_plan(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int6
   D.nspans = (int32_t)c.span_first.size();
   D.R = rb.out();
   RangeSet R = rb.set();
-  DVec<int32_t> ucnt; ucnt.exact(std::max<int64_t>(units, 1));
-  DVec<int64_t> uofs; uofs.exact(std::max<int64_t>(units, 1));
   DVec<int64_t> scr; scr.exact(512);
+  DVec<int32_t> pl; pl.exact(std::max<int64_t>(std::min<int64_t>(32 * units, std::max<int64_t>(capacity, 0)), 1));
   k_demand_collect<<<1, 1024, 0, st>>>(D);
   MSG_CHECK_LAUNCH();
   add_launches(1);
-  units_count(c, R, ucnt.p, nullptr, nullptr);
-  units_scan(c, R, ucnt.p, uofs.p, scr.p + 400, scr.p);
-  k_plan_scalars<<<1, 1, 0, st>>>(scr.p + 400, c.dstate, capacity, c.len);
-  MSG_CHECK_LAUNCH();
-  add_launches(1);
+  units_plan(c, R, units, nullptr, 0, std::max<int64_t>(capacity, 0), pl.p, capacity, scr.p + 400);
   MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaStreamSynchronize(st));
   DevState S = *c.hstate;
@@ -2630,8 +2616,6 @@ void list_plan(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int6
   *truncated = S.truncated;
   int64_t ev = std::min<int64_t>(S.evict, c.len);
   *nev = ev;
-  DVec<int32_t> pl; pl.exact(std::max<int64_t>(S.populate, 1));
-  if (S.populate) units_fill(c, R, uofs.p, &c.dstate->populate, pl.p);
   std::vector<int64_t> tmp;
   dump_dense(c, pl.p, S.populate, tmp);
   if (pop_out) std::copy(tmp.begin(), tmp.end(), pop_out);

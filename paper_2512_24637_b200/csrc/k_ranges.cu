@@ -201,6 +201,195 @@ void units_fill(Ctx& c, const RangeSet& R, const int64_t* uofs, const int64_t* c
   add_launches(1);
 }
 
+// ---- one cooperative launch: count, per-tag counts, scan, plan, fill ------
+//
+// The missing pages of an ordered range list against the resident bitmap,
+// in range order (memman.py:284-291, engine.py:310-313, 350-355): every CTA
+// owns a contiguous run of 32-page units; phase 1 counts (popcount of
+// ~resident & range mask) and accumulates per-tag counts in shared memory;
+// one grid barrier; phase 2 turns the per-CTA totals into offsets (and the
+// plan scalars, memman.py:284-299); phase 3 recounts each unit (the bitmap is
+// unchanged) and writes its pages at their offsets, capped.  Replaces the
+// count / 3-kernel scan / scalars / fill chain (six launches).
+
+struct UnitsPlan {
+  RangeSet R;
+  const uint32_t* bits;
+  int64_t* tag_cnt;      // per-tag totals (ntags), or nullptr
+  int32_t ntags;
+  int64_t cap;           // fill cap (pages), < 0: none
+  int32_t* out;          // fill output, or nullptr
+  DevState* S;           // plan scalars, or nullptr
+  int64_t C, len;        // capacity and resident pages (for the scalars)
+  int64_t* total_out;    // missing pages, or nullptr
+  int32_t* hist;         // [gridDim] CTA totals, then [gridDim][ntags] tag partials
+  int32_t* bar;          // grid barrier counter (zero at launch)
+};
+
+constexpr int UP_THREADS = 512;
+constexpr int UP_MAX_TAGS = 8192;
+
+__global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
+  __shared__ int64_t ws[32];
+  __shared__ int32_t tagc[UP_MAX_TAGS];
+  __shared__ int64_t carry_s;
+  const int t = threadIdx.x, G = gridDim.x, b = blockIdx.x;
+  const int64_t nr = *P.R.nr;
+  const int64_t nu = nr ? P.R.uoff[nr] : 0;
+  const int64_t U = (nu + G - 1) / G;
+  const int64_t u0 = (int64_t)b * U, u1 = u0 + U < nu ? u0 + U : nu;
+  for (int i = t; i < P.ntags; i += UP_THREADS) tagc[i] = 0;
+  __syncthreads();
+  auto unit = [&](int64_t u, int64_t* r_out, int64_t* w_out, uint32_t* m_out) {
+    int64_t a = 0, z = nr;   // largest r with uoff[r] <= u
+    while (z - a > 1) { int64_t mid = (a + z) >> 1; if (P.R.uoff[mid] <= u) a = mid; else z = mid; }
+    int64_t lo = P.R.lo[a], hi = lo + P.R.len[a];
+    int64_t w = (lo >> 5) + (u - P.R.uoff[a]);
+    int64_t p0 = w << 5;
+    uint32_t m = ~0u;
+    if (p0 < lo) m &= ~0u << (lo - p0);
+    if (p0 + 32 > hi) m &= (hi - p0) >= 32 ? ~0u : ((1u << (hi - p0)) - 1u);
+    *r_out = a; *w_out = w; *m_out = ~P.bits[w] & m;
+  };
+  // ---- phase 1: counts
+  int64_t acc = 0;
+  for (int64_t base = u0; base < u1; base += UP_THREADS) {
+    int64_t u = base + t, r = -1, w;
+    uint32_t m = 0;
+    if (u < u1) unit(u, &r, &w, &m);
+    int c = __popc(m);
+    acc += c;
+    if (P.tag_cnt) {
+      int tag = (r >= 0 && c) ? P.R.tag[r] : -1;
+      unsigned peers = __match_any_sync(0xffffffffu, tag);
+      int sum = __reduce_add_sync(peers, (unsigned)c);
+      if (tag >= 0 && (int)(t & 31) == __ffs(peers) - 1) atomicAdd(&tagc[tag], sum);
+    }
+  }
+  int64_t tot;
+  block_scan_excl_i64(acc, ws, &tot);
+  if (t == 0) __stcg(P.hist + b, (int32_t)tot);
+  __syncthreads();
+  if (P.tag_cnt)
+    for (int i = t; i < P.ntags; i += UP_THREADS) __stcg(P.hist + G + (int64_t)b * P.ntags + i, tagc[i]);
+  // ---- grid barrier
+  __syncthreads();
+  if (t == 0) {
+    __threadfence();
+    atomicAdd(P.bar, 1);
+    while (*reinterpret_cast<volatile int32_t*>(P.bar) < G) __nanosleep(32);
+    __threadfence();
+  }
+  __syncthreads();
+  // ---- phase 2: offsets, totals, scalars, per-tag totals
+  int64_t pre = 0, all = 0;
+  for (int i = t; i < G; i += UP_THREADS) {
+    int64_t v = __ldcg(P.hist + i);
+    all += v;
+    if (i < b) pre += v;
+  }
+  int64_t pre_tot, all_tot;
+  block_scan_excl_i64(pre, ws, &pre_tot);
+  block_scan_excl_i64(all, ws, &all_tot);
+  if (P.tag_cnt) {
+    for (int i = b * UP_THREADS + t; i < P.ntags; i += G * UP_THREADS) {
+      int64_t s = 0;
+      for (int c2 = 0; c2 < G; ++c2) s += __ldcg(P.hist + G + (int64_t)c2 * P.ntags + i);
+      P.tag_cnt[i] = s;
+    }
+  }
+  if (b == 0 && t == 0) {
+    if (P.total_out) *P.total_out = all_tot;
+    if (P.S) {
+      DevState* S = P.S;
+      S->missing = all_tot;
+      int64_t pop = all_tot < P.C ? all_tot : P.C;
+      S->populate = pop;
+      S->truncated = all_tot - pop;
+      S->free_before = P.C - P.len;
+      int64_t ev = pop - (P.C - P.len);
+      S->evict = ev > 0 ? ev : 0;
+      S->skip = all_tot == 0;
+    }
+  }
+  if (!P.out) return;
+  // ---- phase 3: fill in range order, capped
+  const int64_t cap = P.cap < 0 ? INT64_MAX : P.cap;
+  if (t == 0) carry_s = pre_tot;
+  __syncthreads();
+  for (int64_t base = u0; base < u1; base += UP_THREADS) {
+    int64_t u = base + t, r, w = 0;
+    uint32_t m = 0;
+    if (u < u1) unit(u, &r, &w, &m);
+    int64_t rt;
+    int64_t o = carry_s + block_scan_excl_i64(__popc(m), ws, &rt);
+    while (m && o < cap) {
+      int k = __ffs(m) - 1;
+      m &= m - 1;
+      P.out[o++] = (int32_t)((w << 5) + k);
+    }
+    __syncthreads();
+    if (t == 0) carry_s += rt;
+    __syncthreads();
+  }
+}
+
+// per command of [c0, c1) of a task: missing pages of its actual set against
+// the resident bitmap (engine.py:396-397), one CTA per command, no atomics
+__global__ void __launch_bounds__(256) k_touch_counts(const Iv* __restrict__ pool, const int64_t* __restrict__ off,
+                                                     int32_t c0, const uint32_t* __restrict__ bits,
+                                                     int64_t* __restrict__ out) {
+  __shared__ int64_t red[8];
+  const int32_t cmd = c0 + blockIdx.x;
+  const int64_t i0 = off[cmd], i1 = off[cmd + 1];
+  int64_t acc = 0;
+  for (int64_t i = i0; i < i1; ++i) {
+    const Iv v = pool[i];
+    const int64_t lo = v.d, hi = v.d + (v.b - v.a);
+    for (int64_t w = (lo >> 5) + threadIdx.x; w < ((hi + 31) >> 5); w += blockDim.x) {
+      int64_t p0 = w << 5;
+      uint32_t m = ~0u;
+      if (p0 < lo) m &= ~0u << (lo - p0);
+      if (p0 + 32 > hi) m &= (hi - p0) >= 32 ? ~0u : ((1u << (hi - p0)) - 1u);
+      acc += __popc(~bits[w] & m);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t s = 0;
+    for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+    out[blockIdx.x] = s;
+  }
+}
+
+void touch_counts_dev(Ctx& c, TaskTab& t, int32_t lo, int32_t hi, int64_t* out) {
+  if (hi <= lo) return;
+  k_touch_counts<<<hi - lo, 256, 0, c.st>>>(t.act_pool.p, t.d_act_off.p, lo, c.bits.p, out);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+}
+
+void units_plan(Ctx& c, const RangeSet& R, int64_t units_cap, int64_t* tag_cnt, int32_t ntags, int64_t cap,
+                int32_t* out, int64_t plan_capacity, int64_t* total_out) {
+  static int per_sm = -1, sms = 0;
+  if (per_sm < 0) {
+    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_units_plan, UP_THREADS, 0));
+    MSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+  }
+  if (ntags > UP_MAX_TAGS) throw Error(MSG_E_INVAL, "too many commands in one window for the units plan");
+  int G = (int)std::min<int64_t>(std::max<int64_t>((units_cap + 2047) / 2048, 1), (int64_t)std::max(per_sm, 1) * sms);
+  c.up_hist.resize((int64_t)G * (1 + std::max(ntags, 0)) + 1, c.st);
+  UnitsPlan P{R, c.bits.p, tag_cnt, tag_cnt ? ntags : 0, cap, out, plan_capacity >= 0 ? c.dstate : nullptr,
+              plan_capacity, c.len, total_out, c.up_hist.p, next_barrier(c)};
+  void* args[] = {&P};
+  MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_units_plan), dim3(G), dim3(UP_THREADS), args, 0,
+                                       c.st));
+  add_launches(1);
+}
+
 void ranges_from_actual(Ctx& c, TaskTab& t, int32_t c0, int32_t c1, RangeBuf& B) {
   int64_t n = t.act_off[c1] - t.act_off[c0];
   B.reserve(n, c.st);

@@ -35,5 +35,12 @@ void units_scan(Ctx& c, const RangeSet& R, const int32_t* ucnt, int64_t* uofs, i
 void units_fill(Ctx& c, const RangeSet& R, const int64_t* uofs, const int64_t* cap_ptr, int32_t* out);
 void ranges_from_actual(Ctx& c, TaskTab& t, int32_t c0, int32_t c1, RangeBuf& B);
 void units_scan_count(Ctx& c, const RangeSet& R, int32_t* ucnt, int64_t* uofs, int64_t* total, int64_t* scratch);
+// one cooperative launch: missing pages of R against residency, per-tag
+// counts (optional), plan scalars against plan_capacity into DevState
+// (optional), capped fill
+void units_plan(Ctx& c, const RangeSet& R, int64_t units_cap, int64_t* tag_cnt, int32_t ntags, int64_t cap,
+                int32_t* out, int64_t plan_capacity /* < 0: no plan scalars */, int64_t* total_out);
+void touch_counts_dev(Ctx& c, TaskTab& t, int32_t lo, int32_t hi, int64_t* out);
+int32_t* next_barrier(Ctx& c);   // a zeroed grid-barrier counter for one cooperative launch
 
 }  // namespace msg

@@ -237,6 +237,7 @@ struct Ctx {
   DVec<unsigned long long> ms_tot;      // digit totals (4 x 257)
   DVec<int32_t> ms_hist;                // per-CTA digit counts of the cooperative multisplit (+ 2 total rows)
   int ms_tot_par = 0;                   // which total row the next cooperative launch accumulates into
+  DVec<int32_t> up_hist;                // k_units_plan per-CTA totals and tag partials
   uint32_t ms_epoch = 0;
   std::vector<int64_t> dbg[4];
   ~Ctx();
