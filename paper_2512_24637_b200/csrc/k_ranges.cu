@@ -224,27 +224,42 @@ struct UnitsPlan {
   int64_t* total_out;    // missing pages, or nullptr
   int32_t* hist;         // [gridDim] CTA totals, then [gridDim][ntags] tag partials
   int32_t* bar;          // grid barrier counter (zero at launch)
+  int32_t stage;         // the range table fits the dynamic shared memory
 };
 
 constexpr int UP_THREADS = 512;
 constexpr int UP_MAX_TAGS = 8192;
+constexpr int UP_SMEM_RANGES = 4096;   // range tables up to this size are searched in shared memory
 
 __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
   __shared__ int64_t ws[32];
-  __shared__ int32_t tagc[UP_MAX_TAGS];
   __shared__ int64_t carry_s;
+  extern __shared__ __align__(16) unsigned char up_raw[];
+  int32_t* tagc = reinterpret_cast<int32_t*>(up_raw);                          // ntags
+  int64_t* r_uoff = reinterpret_cast<int64_t*>(up_raw + ((4 * (int64_t)P.ntags + 15) & ~int64_t(15)));
+  int64_t* r_lo = r_uoff + UP_SMEM_RANGES + 1;
   const int t = threadIdx.x, G = gridDim.x, b = blockIdx.x;
   const int64_t nr = *P.R.nr;
   const int64_t nu = nr ? P.R.uoff[nr] : 0;
   const int64_t U = (nu + G - 1) / G;
   const int64_t u0 = (int64_t)b * U, u1 = u0 + U < nu ? u0 + U : nu;
+  const bool staged = P.stage && nr <= UP_SMEM_RANGES;
   for (int i = t; i < P.ntags; i += UP_THREADS) tagc[i] = 0;
+  if (staged)
+    for (int64_t i = t; i <= nr; i += UP_THREADS) {
+      r_uoff[i] = P.R.uoff[i];
+      if (i < nr) r_lo[i] = P.R.lo[i];
+    }
   __syncthreads();
+  const int64_t* uoff = staged ? r_uoff : P.R.uoff;
+  const int64_t* rlo = staged ? r_lo : P.R.lo;
   auto unit = [&](int64_t u, int64_t* r_out, int64_t* w_out, uint32_t* m_out) {
     int64_t a = 0, z = nr;   // largest r with uoff[r] <= u
-    while (z - a > 1) { int64_t mid = (a + z) >> 1; if (P.R.uoff[mid] <= u) a = mid; else z = mid; }
-    int64_t lo = P.R.lo[a], hi = lo + P.R.len[a];
-    int64_t w = (lo >> 5) + (u - P.R.uoff[a]);
+    while (z - a > 1) { int64_t mid = (a + z) >> 1; if (uoff[mid] <= u) a = mid; else z = mid; }
+    // a range's units are the bitmap words it overlaps, so its end is the next range's start only
+    // as far as units go; the page extent needs len, read once per unit (cached in L1)
+    int64_t lo = rlo[a], hi = lo + P.R.len[a];
+    int64_t w = (lo >> 5) + (u - uoff[a]);
     int64_t p0 = w << 5;
     uint32_t m = ~0u;
     if (p0 < lo) m &= ~0u << (lo - p0);
@@ -292,10 +307,14 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
   block_scan_excl_i64(pre, ws, &pre_tot);
   block_scan_excl_i64(all, ws, &all_tot);
   if (P.tag_cnt) {
-    for (int i = b * UP_THREADS + t; i < P.ntags; i += G * UP_THREADS) {
-      int64_t s = 0;
-      for (int c2 = 0; c2 < G; ++c2) s += __ldcg(P.hist + G + (int64_t)c2 * P.ntags + i);
-      P.tag_cnt[i] = s;
+    // tag i's total over the CTAs' partials: CTA b sums tags b, b+G, ... with
+    // all its threads in parallel (one CTA row per thread)
+    for (int i = b; i < P.ntags; i += G) {
+      int64_t part = 0;
+      for (int c2 = t; c2 < G; c2 += UP_THREADS) part += __ldcg(P.hist + G + (int64_t)c2 * P.ntags + i);
+      int64_t sum;
+      block_scan_excl_i64(part, ws, &sum);
+      if (t == 0) P.tag_cnt[i] = sum;
     }
   }
   if (b == 0 && t == 0) {
@@ -313,8 +332,14 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
     }
   }
   if (!P.out) return;
-  // ---- phase 3: fill in range order, capped
+  // ---- phase 3: fill in range order, capped.  Offsets per unit (thread per
+  // unit, block scan), then one warp writes a unit's pages with one
+  // coalesced store (lane k writes page 32w+k when missing).
+  __shared__ int64_t uo_s[UP_THREADS];
+  __shared__ int64_t uw_s[UP_THREADS];
+  __shared__ uint32_t um_s[UP_THREADS];
   const int64_t cap = P.cap < 0 ? INT64_MAX : P.cap;
+  const int lane = t & 31, warp = t >> 5;
   if (t == 0) carry_s = pre_tot;
   __syncthreads();
   for (int64_t base = u0; base < u1; base += UP_THREADS) {
@@ -323,10 +348,14 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
     if (u < u1) unit(u, &r, &w, &m);
     int64_t rt;
     int64_t o = carry_s + block_scan_excl_i64(__popc(m), ws, &rt);
-    while (m && o < cap) {
-      int k = __ffs(m) - 1;
-      m &= m - 1;
-      P.out[o++] = (int32_t)((w << 5) + k);
+    uo_s[t] = o; uw_s[t] = w; um_s[t] = m;
+    __syncthreads();
+    for (int k = 0; k < 32; ++k) {
+      const int i = warp * 32 + k;
+      const uint32_t mk = um_s[i];
+      if (!mk) continue;
+      const int64_t ok = uo_s[i] + __popc(mk & ((1u << lane) - 1u));
+      if (((mk >> lane) & 1u) && ok < cap) P.out[ok] = (int32_t)((uw_s[i] << 5) + lane);
     }
     __syncthreads();
     if (t == 0) carry_s += rt;
@@ -336,10 +365,10 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
 
 // per command of [c0, c1) of a task: missing pages of its actual set against
 // the resident bitmap (engine.py:396-397), one CTA per command, no atomics
-__global__ void __launch_bounds__(256) k_touch_counts(const Iv* __restrict__ pool, const int64_t* __restrict__ off,
+__global__ void __launch_bounds__(1024) k_touch_counts(const Iv* __restrict__ pool, const int64_t* __restrict__ off,
                                                      int32_t c0, const uint32_t* __restrict__ bits,
                                                      int64_t* __restrict__ out) {
-  __shared__ int64_t red[8];
+  __shared__ int64_t red[32];
   const int32_t cmd = c0 + blockIdx.x;
   const int64_t i0 = off[cmd], i1 = off[cmd + 1];
   int64_t acc = 0;
@@ -367,7 +396,7 @@ __global__ void __launch_bounds__(256) k_touch_counts(const Iv* __restrict__ poo
 
 void touch_counts_dev(Ctx& c, TaskTab& t, int32_t lo, int32_t hi, int64_t* out) {
   if (hi <= lo) return;
-  k_touch_counts<<<hi - lo, 256, 0, c.st>>>(t.act_pool.p, t.d_act_off.p, lo, c.bits.p, out);
+  k_touch_counts<<<hi - lo, 1024, 0, c.st>>>(t.act_pool.p, t.d_act_off.p, lo, c.bits.p, out);
   MSG_CHECK_LAUNCH();
   add_launches(1);
 }
@@ -376,16 +405,20 @@ void units_plan(Ctx& c, const RangeSet& R, int64_t units_cap, int64_t* tag_cnt, 
                 int32_t* out, int64_t plan_capacity, int64_t* total_out) {
   static int per_sm = -1, sms = 0;
   if (per_sm < 0) {
-    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_units_plan, UP_THREADS, 0));
+    const int max_smem = 4 * UP_MAX_TAGS + 16 * (UP_SMEM_RANGES + 1) + 64;
+    MSG_CUDA(cudaFuncSetAttribute(k_units_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
+    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_units_plan, UP_THREADS, max_smem));
     MSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
   }
   if (ntags > UP_MAX_TAGS) throw Error(MSG_E_INVAL, "too many commands in one window for the units plan");
   int G = (int)std::min<int64_t>(std::max<int64_t>((units_cap + 2047) / 2048, 1), (int64_t)std::max(per_sm, 1) * sms);
   c.up_hist.resize((int64_t)G * (1 + std::max(ntags, 0)) + 1, c.st);
-  UnitsPlan P{R, c.bits.p, tag_cnt, tag_cnt ? ntags : 0, cap, out, plan_capacity >= 0 ? c.dstate : nullptr,
-              plan_capacity, c.len, total_out, c.up_hist.p, next_barrier(c)};
+  const int nt = tag_cnt ? ntags : 0;
+  const size_t smem = ((4 * (size_t)nt + 15) & ~size_t(15)) + 16 * ((size_t)UP_SMEM_RANGES + 1);
+  UnitsPlan P{R, c.bits.p, tag_cnt, nt, cap, out, plan_capacity >= 0 ? c.dstate : nullptr,
+              plan_capacity, c.len, total_out, c.up_hist.p, next_barrier(c), 1};
   void* args[] = {&P};
-  MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_units_plan), dim3(G), dim3(UP_THREADS), args, 0,
+  MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_units_plan), dim3(G), dim3(UP_THREADS), args, smem,
                                        c.st));
   add_launches(1);
 }
