@@ -179,12 +179,16 @@ def dist_init():
     return ws, rank, local
 
 
+def _coll_device(dist, dev):
+    return "cpu" if dist.get_backend() == "gloo" else dev
+
+
 def max_over_ranks(torch, x, ws, dev):
     if ws == 1:
         return x
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device(dist, dev))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -194,7 +198,7 @@ def sum_over_ranks(torch, x, ws, dev):
         return x
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    t = torch.tensor([x], dtype=torch.float64, device=_coll_device(dist, dev))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
@@ -322,12 +326,21 @@ def main():
     import torch
 
     ws, rank, local = dist_init()
+    # test hook: ranks share the visible GPU(s) and talk over gloo, so the
+    # multi-rank path can be exercised on a one-GPU box (the driver's N-GPU
+    # runs use one GPU per rank and NCCL)
+    shared = os.environ.get("MSG_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = local % max(torch.cuda.device_count(), 1)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     from paper_2512_24637_b200 import engine
     from paper_2512_24637_b200.analyzer import build_descriptors
 
