@@ -837,19 +837,6 @@ __global__ void __launch_bounds__(1024, 1) k_demand_collect(DemandParams P) {
   if (threadIdx.x == 0) { *P.R.nr = carry; P.R.uoff[carry] = ucarry; }
 }
 
-// plan scalars from the total missing count (memman.py:284-299)
-__global__ void k_plan_scalars(const int64_t* total_ptr, DevState* S, int64_t capacity, int64_t len) {
-  int64_t total = *total_ptr;
-  S->missing = total;
-  int64_t pop = total < capacity ? total : capacity;
-  S->populate = pop;
-  S->truncated = total - pop;
-  S->free_before = capacity - len;
-  int64_t ev = pop - (capacity - len);
-  S->evict = ev > 0 ? ev : 0;
-  S->skip = total == 0;
-}
-
 // ---------------------------------------------------------------------------
 // Multisplit of the eviction list (the reorder / madvise / remove kernel).
 

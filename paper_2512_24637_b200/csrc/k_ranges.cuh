@@ -30,11 +30,7 @@ __device__ __forceinline__ int64_t block_scan_excl_i64(int64_t v, int64_t* smem_
   return before;
 }
 
-void units_count(Ctx& c, const RangeSet& R, int32_t* ucnt, int64_t* tag_cnt, int64_t* range_cnt);
-void units_scan(Ctx& c, const RangeSet& R, const int32_t* ucnt, int64_t* uofs, int64_t* total, int64_t* scratch);
-void units_fill(Ctx& c, const RangeSet& R, const int64_t* uofs, const int64_t* cap_ptr, int32_t* out);
 void ranges_from_actual(Ctx& c, TaskTab& t, int32_t c0, int32_t c1, RangeBuf& B);
-void units_scan_count(Ctx& c, const RangeSet& R, int32_t* ucnt, int64_t* uofs, int64_t* total, int64_t* scratch);
 // one cooperative launch: missing pages of R against residency, per-tag
 // counts (optional), plan scalars against plan_capacity into DevState
 // (optional), capped fill
