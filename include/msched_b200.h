@@ -270,6 +270,34 @@ int msg_list_plan(msg_ctx *ctx, const int64_t *run_first, const int64_t *run_end
                   int64_t capacity, int64_t *populate_out, int64_t *npopulate, int64_t *evict_out,
                   int64_t *nevict, int64_t *truncated);
 
+/* Offline template inference, native (analyzer.py:185-441 of the reference:
+ * build_descriptors / build_descriptor / infer_rule / fit_linear_expr).
+ * Commands in the msg_cmd / msg_arg / blob / msg_range layout, with
+ * cmds[i].kernel = the index of the command's kernel name (0..nkernels-1,
+ * memcpys ignored) and latency[i] its latency.  Per kernel k: status[k] = 0
+ * when done here, 1 when a value lies outside the native arithmetic (values
+ * and slot values must be < 2^64) or argument counts are ragged — the host
+ * analyzer then does that kernel; latency_out[k] (mean over the records),
+ * unpredictable_out[k], and rules [rule_off[k], rule_off[k+1]) of rules_out.
+ * A rule's expression q (size for fixed/linear; stride, chunk, count for
+ * strided) is coeff * prod(slot[q][0..nslots[q])) with coeff = v0[q] divided
+ * by the product of those slots in the kernel's first record (the host forms
+ * the reduced fraction).  Returns MSG_E_INVAL if rules_cap is too small
+ * (rule_off[nkernels] has the count).  Needs no GPU and no context. */
+typedef struct {
+  int32_t ptr_arg;
+  int32_t kind;             /* 0 fixed, 1 linear, 2 strided */
+  int64_t offset;
+  int32_t nslots[3];
+  int32_t pad;
+  int64_t slot[3][3];       /* slot codes (see msg_expr) */
+  int64_t v0[3];
+} msg_arule;
+
+int msg_analyze(const msg_cmd *cmds, int32_t ncmd, const msg_arg *args, const uint8_t *blob, int64_t blob_len,
+                const msg_range *gt, const double *latency, int32_t nkernels, int32_t *status, double *latency_out,
+                double *unpredictable_out, msg_arule *rules_out, int32_t rules_cap, int32_t *rule_off);
+
 /* Parity dumps (the reference's promised but unimplemented SPEC.md:415-416
  * debug dump).  which: 0 list order after the last reorder, 1 last evicted
  * pages (head order), 2 last installed pages (install order).  enable is a

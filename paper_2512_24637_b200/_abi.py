@@ -27,7 +27,7 @@ EXPORTS = [
     "msg_um_slice", "msg_release_task", "msg_list_append", "msg_list_madvise", "msg_list_evict_head",
     "msg_list_len", "msg_list_read", "msg_sync", "msg_get_stats", "msg_verify_residency",
     "msg_flush_l2", "msg_list_reorder", "msg_debug", "msg_debug_read", "msg_window_runs", "msg_list_plan", "msg_reset",
-    "msg_run_command",
+    "msg_run_command", "msg_analyze",
 ]
 
 
@@ -77,6 +77,8 @@ CMD_DT = np.dtype([("kind", "<i4"), ("kernel", "<i4"), ("arg_off", "<i4"), ("nar
 RANGE_DT = np.dtype([("start", "<i8"), ("len", "<i8")])
 EXPR_DT = np.dtype([("num", "<i8"), ("den", "<i8"), ("nslots", "<i4"), ("pad", "<i4"), ("slot", "<i8", (3,))])
 RULE_DT = np.dtype([("kind", "<i4"), ("ptr_arg", "<i4"), ("offset", "<i8"), ("e", EXPR_DT, (3,))])
+ARULE_DT = np.dtype([("ptr_arg", "<i4"), ("kind", "<i4"), ("offset", "<i8"), ("nslots", "<i4", (3,)), ("pad", "<i4"),
+                     ("slot", "<i8", (3, 3)), ("v0", "<i8", (3,))])
 
 _lib = None
 
@@ -124,6 +126,7 @@ def load():
         "msg_verify_residency": ([vp, C.POINTER(i64)], C.c_int),
         "msg_flush_l2": ([vp], C.c_int),
         "msg_run_command": ([vp, i32, i32, i64], C.c_int),
+        "msg_analyze": ([vp, i32, vp, vp, i64, vp, vp, i32, vp, vp, vp, vp, i32, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
         f = getattr(lib, name)
@@ -169,6 +172,40 @@ def slot_code(name: str) -> int:
 
 
 _NEVER = 2 | (7 << 2)   # launch dim 7 does not exist: evaluates to None
+_DIM_NAMES = ("gx", "gy", "gz", "bx", "by", "bz")
+
+
+def slot_name(code: int) -> str:
+    """Inverse of slot_code."""
+    kind, idx = code & 3, (code >> 2) & 0xFFFF
+    if kind == 2:
+        return _DIM_NAMES[idx]
+    if kind == 0:
+        return f"a{idx}"
+    return f"a{idx}+{(code >> 18) & 0xFFFFFFFF}w{64 if (code >> 50) & 1 else 32}"
+
+
+def analyze(cmds_encoded, latency, nkernels: int):
+    """msg_analyze over encoded commands (cmds[i].kernel = kernel-name index).
+    Returns (status, latency_mean, unpredictable, rules ARULE_DT, rule_off)."""
+    lib = load()
+    carr, aarr, barr, blen, garr = cmds_encoded
+    lat = np.ascontiguousarray(latency, dtype=np.float64)
+    status = np.zeros(max(nkernels, 1), np.int32)
+    lat_out = np.zeros(max(nkernels, 1), np.float64)
+    unp = np.zeros(max(nkernels, 1), np.float64)
+    off = np.zeros(nkernels + 1, np.int32)
+    cap = max(4 * nkernels, 16)
+    while True:
+        rules = np.zeros(cap, ARULE_DT)
+        rc = lib.msg_analyze(_p(carr), len(carr), _p(aarr), _p(barr), blen, _p(garr), _p(lat), nkernels, _p(status),
+                             _p(lat_out), _p(unp), _p(rules), cap, _p(off))
+        if rc == MSG_OK:
+            return status[:nkernels], lat_out[:nkernels], unp[:nkernels], rules, off
+        if rc == MSG_E_INVAL and off[nkernels] > cap:
+            cap = int(off[nkernels])
+            continue
+        raise MsgError(rc, f"msg_analyze failed ({rc})")
 
 
 def _fits64(v: int) -> bool:
@@ -226,34 +263,39 @@ def _split128(v: int):
     return v & 0xFFFFFFFFFFFFFFFF, hi
 
 
+_KIND_CODE = {"KERNEL": CMD_KERNEL, "H2D": CMD_H2D, "D2H": CMD_D2H}
+
+
 def encode_commands(cmds, kernel_ids: dict):
-    """Columnarise Command objects into the C structs (one pass, host)."""
-    n = len(cmds)
-    carr = np.zeros(n, CMD_DT)
-    args, gts, blob = [], [], bytearray()
-    for i, c in enumerate(cmds):
-        row = carr[i]
+    """Columnarise Command objects into the C structs (one pass, host; rows
+    built as tuples and converted once)."""
+    rows, args, gts, blob = [], [], [], bytearray()
+    kid = kernel_ids.get
+    for c in cmds:
         kind = c.kind.value if hasattr(c.kind, "value") else c.kind
-        row["kind"] = {"KERNEL": CMD_KERNEL, "H2D": CMD_H2D, "D2H": CMD_D2H}[kind]
-        row["kernel"] = kernel_ids.get(c.kernel_name, -1)
-        row["arg_off"] = len(args)
-        row["nargs"] = len(c.launch_args)
+        code = _KIND_CODE[kind]
+        a0, g0 = len(args), len(gts)
         for a in c.launch_args:
-            lo, hi = _split128(a.value)
+            v = a.value
+            if -(1 << 63) <= v < (1 << 63):
+                lo, hi = v & 0xFFFFFFFFFFFFFFFF, -1 if v < 0 else 0
+            else:
+                lo, hi = _split128(v)
             if a.raw is not None:
                 args.append((lo, hi, 0, len(a.raw), len(blob)))
                 blob += a.raw
             else:
                 args.append((lo, hi, a.width, -1, 0))
-        row["gt_off"] = len(gts)
-        row["ngt"] = len(c.ground_truth_access)
         for r in c.ground_truth_access:
             gts.append((r.start_addr, r.length_bytes))
-        g, b = tuple(c.grid_dims), tuple(c.block_dims)
-        row["dims"] = g + b
-        if kind != "KERNEL":
+        if code != CMD_KERNEL:
             rng = c.device_range()   # raises ValueError for non-positive sizes (core.py:52-54)
-            row["dev_addr"], row["dev_len"] = rng.start_addr, rng.length_bytes
+            da, dl = rng.start_addr, rng.length_bytes
+        else:
+            da = dl = 0
+        rows.append((code, kid(c.kernel_name, -1), a0, len(c.launch_args), g0, len(c.ground_truth_access),
+                     tuple(c.grid_dims) + tuple(c.block_dims), da, dl))
+    carr = np.array(rows, dtype=CMD_DT) if rows else np.zeros(0, CMD_DT)
     aarr = np.array(args, dtype=ARG_DT) if args else np.zeros(1, ARG_DT)
     garr = np.array(gts, dtype=RANGE_DT) if gts else np.zeros(1, RANGE_DT)
     barr = np.frombuffer(bytes(blob) or b"\0", dtype=np.uint8)

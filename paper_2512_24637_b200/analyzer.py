@@ -337,8 +337,83 @@ def records_from_task(task) -> dict:
     return out
 
 
-def build_descriptors(task) -> dict:
+def build_descriptors(task, native: bool = True) -> dict:
+    """One descriptor per kernel name (analyzer.py:437-441).  With
+    native=True the inference runs in the C-ABI library (msg_analyze, host
+    C++, exact 256-bit ratio tests); kernels whose numbers fall outside its
+    arithmetic, and every kernel when the library is absent, take this
+    module's path.  Both give identical descriptors (tests/test_analyzer_native.py)."""
+    if native:
+        try:
+            return _build_descriptors_native(task)
+        except (ImportError, OSError, ValueError, RuntimeError):
+            pass   # no library, or inputs the encoder rejects: the host path decides
     return {name: build_descriptor(name, recs) for name, recs in records_from_task(task).items()}
+
+
+def _build_descriptors_native(task) -> dict:
+    import numpy as np
+
+    from . import _abi
+    from .tracebin import CommandColumns
+
+    cols = task.commands if isinstance(task.commands, CommandColumns) else None
+    first = {}
+    if cols is not None:   # binary trace: the columns already are the ABI tables
+        kern = cols.cmds["kernel"]
+        is_k = (cols.kinds() == _abi.CMD_KERNEL) & (kern >= 0)
+        idx = np.flatnonzero(is_k)
+        uniq, first_pos = np.unique(kern[idx], return_index=True)
+        order = np.argsort(first_pos, kind="stable")
+        names = [cols.names[int(uniq[o])] for o in order]
+        remap = np.full(len(cols.names) + 1, -1, dtype=np.int32)
+        remap[uniq[order]] = np.arange(len(order), dtype=np.int32)
+        cm = cols.cmds.copy()
+        cm["kernel"] = np.where(is_k, remap[np.where(kern >= 0, kern, len(cols.names))], -1)
+        enc = (cm, cols.args if len(cols.args) else np.zeros(1, _abi.ARG_DT),
+               cols.blob if len(cols.blob) else np.zeros(1, np.uint8), len(cols.blob),
+               cols.gts if len(cols.gts) else np.zeros(1, _abi.RANGE_DT))
+        lat_in = cols.lat
+        for o in order:
+            first[cols.names[int(uniq[o])]] = cols[int(idx[first_pos[o]])]
+    else:
+        names, seen = [], {}
+        for c in task.commands:
+            if c.kind is CommandKind.KERNEL and c.kernel_name not in seen:
+                seen[c.kernel_name] = len(names)
+                names.append(c.kernel_name)
+                first[c.kernel_name] = c
+        enc = _abi.encode_commands(task.commands, seen)
+        lat_in = [c.latency_s for c in task.commands]
+    if not names:
+        return {}
+    status, lat, unp, rules, off = _abi.analyze(enc, lat_in, len(names))
+    out = {}
+    recs = None
+    for k, name in enumerate(names):
+        if status[k]:
+            recs = recs or records_from_task(task)
+            out[name] = build_descriptor(name, recs[name])
+            continue
+        c0 = first[name]
+        vals = slot_values(c0.launch_args, c0.grid_dims, c0.block_dims)
+        rl = []
+        for r in rules[off[k]:off[k + 1]]:
+            ex = []
+            for q in range(3 if int(r["kind"]) == 2 else 1):
+                slots = tuple(_abi.slot_name(int(x)) for x in r["slot"][q][:int(r["nslots"][q])])
+                prod = 1
+                for sname in slots:
+                    prod *= vals[sname]
+                ex.append(LinearExpr(Fraction(int(r["v0"][q]), prod), slots))
+            kind = ("fixed", "linear", "strided")[int(r["kind"])]
+            if kind == "strided":
+                rl.append(TemplateRule(int(r["ptr_arg"]), kind, int(r["offset"]), stride=ex[0], chunk=ex[1],
+                                       count=ex[2]))
+            else:
+                rl.append(TemplateRule(int(r["ptr_arg"]), kind, int(r["offset"]), size=ex[0]))
+        out[name] = KernelDescriptor(name, rl, float(lat[k]), float(unp[k]))
+    return out
 
 
 def format_descriptors(descs: dict) -> str:

@@ -57,6 +57,15 @@ def main():
            "bin_bytes": os.path.getsize(binp), "text_save_s": t_text_save, "text_load_s": t_text_load,
            "bin_save_s": t_bin_save, "bin_load_s": t_bin_load,
            "text_cmds_per_s": ncmd / t_text_load, "bin_cmds_per_s": ncmd / t_bin_load}
+    # offline analysis of the whole trace: host analyzer on objects vs the
+    # native analyzer (msg_analyze) on the binary columns
+    t0 = time.perf_counter()
+    d_obj = {t.id: build_descriptors(t, native=False) for t in text_tasks}
+    out["analyze_host_objects_s"] = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    d_col = {t.id: build_descriptors(t, native=True) for t in bin_tasks}
+    out["analyze_native_columns_s"] = time.perf_counter() - t0
+    out["analyzer_outputs_equal"] = d_obj == d_col
     for label, ts in (("objects", text_tasks), ("columns", bin_tasks)):
         t0 = time.perf_counter()
         sim = engine.Simulator(ts, hw, pol, engine.Mode.proactive(), descriptors=descs)
