@@ -2310,29 +2310,47 @@ __global__ void k_release_pages(const int32_t* pages, int64_t n, uint32_t* bits,
   }
 }
 
-__global__ void k_count_resident(const int64_t* lo, const int64_t* len, int64_t n, const uint32_t* bits,
+// resident pages of a few (possibly huge) dense ranges: one thread per
+// 32-page bitmap word across all ranges, so a task span of millions of pages
+// is not walked by one warp
+__global__ void k_count_resident(const int64_t* __restrict__ lo, const int64_t* __restrict__ len,
+                                 const int64_t* __restrict__ woff, int64_t n, const uint32_t* __restrict__ bits,
                                  unsigned long long* out) {
-  int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t r = warp; r < n; r += nwarps) {
-    int64_t m = len[r] - warp_count_nonres(bits, lo[r], len[r]);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, (unsigned long long)m);
+  const int64_t nw = woff[n];
+  unsigned long long acc = 0;
+  for (int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; u < nw; u += (int64_t)gridDim.x * blockDim.x) {
+    int64_t a = 0, z = n;   // largest r with woff[r] <= u
+    while (z - a > 1) { int64_t mid = (a + z) >> 1; if (woff[mid] <= u) a = mid; else z = mid; }
+    const int64_t l = lo[a], h = l + len[a], w = (l >> 5) + (u - woff[a]);
+    const int64_t p0 = w << 5;
+    uint32_t m = ~0u;
+    if (p0 < l) m &= ~0u << (l - p0);
+    if (p0 + 32 > h) m &= (h - p0) >= 32 ? ~0u : ((1u << (h - p0)) - 1u);
+    acc += __popc(bits[w] & m);
   }
+  acc = __reduce_add_sync(0xffffffffu, (unsigned)acc);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
 }
 
 static int64_t count_resident(Ctx& c, const std::vector<int64_t>& lo, const std::vector<int64_t>& len) {
   int64_t n = (int64_t)lo.size();
   if (!n) return 0;
+  std::vector<int64_t> host(3 * n + 2, 0);
+  for (int64_t r = 0; r < n; ++r) {
+    host[r] = lo[r];
+    host[n + r] = len[r];
+    host[2 * n + r + 1] = host[2 * n + r] + (((lo[r] + len[r] + 31) >> 5) - (lo[r] >> 5));
+  }
   DVec<int64_t>& b = c.s.rb;
-  b.resize(2 * n + 1, c.st);
-  MSG_CUDA(cudaMemcpyAsync(b.p, lo.data(), n * 8, cudaMemcpyHostToDevice, c.st));
-  MSG_CUDA(cudaMemcpyAsync(b.p + n, len.data(), n * 8, cudaMemcpyHostToDevice, c.st));
-  MSG_CUDA(cudaMemsetAsync(b.p + 2 * n, 0, 8, c.st));
-  k_count_resident<<<grid_for(n * 32, 256), 256, 0, c.st>>>(b.p, b.p + n, n, c.bits.p,
-                                                           reinterpret_cast<unsigned long long*>(b.p + 2 * n));
+  b.resize(3 * n + 2, c.st);
+  MSG_CUDA(cudaMemcpyAsync(b.p, host.data(), (3 * n + 1) * 8, cudaMemcpyHostToDevice, c.st));
+  MSG_CUDA(cudaMemsetAsync(b.p + 3 * n + 1, 0, 8, c.st));
+  const int64_t words = host[3 * n];
+  k_count_resident<<<grid_for(words, 256, 148 * 8), 256, 0, c.st>>>(
+      b.p, b.p + n, b.p + 2 * n, n, c.bits.p, reinterpret_cast<unsigned long long*>(b.p + 3 * n + 1));
   MSG_CHECK_LAUNCH();
   add_launches(1);
-  MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, b.p + 2 * n, 8, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, b.p + 3 * n + 1, 8, cudaMemcpyDeviceToHost, c.st));
   MSG_CUDA(cudaStreamSynchronize(c.st));
   return c.hbuf.p[0];
 }

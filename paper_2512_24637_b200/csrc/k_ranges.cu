@@ -216,34 +216,43 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
 }
 
 // per command of [c0, c1) of a task: missing pages of its actual set against
-// the resident bitmap (engine.py:396-397), one CTA per command, no atomics
-__global__ void __launch_bounds__(1024) k_touch_counts(const Iv* __restrict__ pool, const int64_t* __restrict__ off,
+// the resident bitmap (engine.py:396-397).  blockIdx.y = command; the
+// command's bitmap words are strided over blockIdx.x so a command touching a
+// gigabyte is not walked by one CTA; out is zeroed by the caller.
+constexpr int TC_SPLIT = 8;
+
+__global__ void __launch_bounds__(256) k_touch_counts(const Iv* __restrict__ pool, const int64_t* __restrict__ off,
                                                      int32_t c0, const uint32_t* __restrict__ bits,
-                                                     int64_t* __restrict__ out) {
-  __shared__ int64_t red[32];
-  const int32_t cmd = c0 + blockIdx.x;
+                                                     unsigned long long* __restrict__ out) {
+  __shared__ unsigned long long red[8];
+  const int32_t cmd = c0 + blockIdx.y;
   const int64_t i0 = off[cmd], i1 = off[cmd + 1];
-  int64_t acc = 0;
+  const int64_t T = (int64_t)gridDim.x * blockDim.x, me = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long acc = 0;
+  int64_t skip = 0;
   for (int64_t i = i0; i < i1; ++i) {
     const Iv v = pool[i];
-    const int64_t lo = v.d, hi = v.d + (v.b - v.a);
-    for (int64_t w = (lo >> 5) + threadIdx.x; w < ((hi + 31) >> 5); w += blockDim.x)
-      acc += __popc(~bits[w] & unit_mask(lo, hi, w));
+    const int64_t lo = v.d, hi = v.d + (v.b - v.a), w0 = lo >> 5, nw = ((hi + 31) >> 5) - w0;
+    int64_t k = (me - skip) % T;
+    if (k < 0) k += T;
+    for (; k < nw; k += T) acc += __popc(~bits[w0 + k] & unit_mask(lo, hi, w0 + k));
+    skip += nw;
   }
-#pragma unroll
-  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  acc = __reduce_add_sync(0xffffffffu, (unsigned)acc);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
   __syncthreads();
   if (threadIdx.x == 0) {
-    int64_t s = 0;
+    unsigned long long s = 0;
     for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
-    out[blockIdx.x] = s;
+    if (s) atomicAdd(&out[blockIdx.y], s);
   }
 }
 
 void touch_counts_dev(Ctx& c, TaskTab& t, int32_t lo, int32_t hi, int64_t* out) {
   if (hi <= lo) return;
-  k_touch_counts<<<hi - lo, 1024, 0, c.st>>>(t.act_pool.p, t.d_act_off.p, lo, c.bits.p, out);
+  MSG_CUDA(cudaMemsetAsync(out, 0, (hi - lo) * sizeof(int64_t), c.st));
+  k_touch_counts<<<dim3(TC_SPLIT, hi - lo), 256, 0, c.st>>>(t.act_pool.p, t.d_act_off.p, lo, c.bits.p,
+                                                            reinterpret_cast<unsigned long long*>(out));
   MSG_CHECK_LAUNCH();
   add_launches(1);
 }

@@ -9,8 +9,13 @@ from paper_2512_24637_b200.analyzer import build_descriptors  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 migrate = "--migrate" in sys.argv
 reps = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 1
-tasks, hw, pol = {"cfg2": scenarios.config2_llama8b, "cfg1": scenarios.config1_gemm,
-                  "cfg4": scenarios.config4_llama70b}[cfg]()
+if cfg == "cfg3":
+    from paper_2512_24637_b200.workload_extra import config3_mixed
+
+    tasks, hw, pol = config3_mixed(hbm_bytes=16 << 30, ratio=2.0, page_size=4096, task_offset=0, timeslice_s=5e-4)
+else:
+    tasks, hw, pol = {"cfg2": scenarios.config2_llama8b, "cfg1": scenarios.config1_gemm,
+                      "cfg4": scenarios.config4_llama70b}[cfg]()
 descs = {t.id: build_descriptors(t) for t in tasks}
 sim = engine.Simulator(tasks, hw, pol, engine.Mode.proactive(), migrate=migrate, descriptors=descs)
 for r in range(reps):
