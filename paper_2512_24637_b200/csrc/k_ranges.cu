@@ -159,14 +159,23 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
   block_scan_excl_i64(pre, ws, &pre_tot);
   block_scan_excl_i64(all, ws, &all_tot);
   if (P.tag_cnt) {
-    // tag i's total over the CTAs' partials: CTA b sums tags b, b+G, ... with
-    // all its threads in parallel (one CTA row per thread)
-    for (int i = b; i < P.ntags; i += G) {
-      int64_t part = 0;
-      for (int c2 = t; c2 < G; c2 += UP_THREADS) part += __ldcg(P.hist + G + (int64_t)c2 * P.ntags + i);
-      int64_t sum;
-      block_scan_excl_i64(part, ws, &sum);
-      if (t == 0) P.tag_cnt[i] = sum;
+    if (G <= 32) {
+      // few CTAs: one thread per tag sums the G partials (coalesced over tags)
+      for (int i = b * UP_THREADS + t; i < P.ntags; i += G * UP_THREADS) {
+        int64_t sum = 0;
+        for (int c2 = 0; c2 < G; ++c2) sum += __ldcg(P.hist + G + (int64_t)c2 * P.ntags + i);
+        P.tag_cnt[i] = sum;
+      }
+    } else {
+      // many CTAs: CTA b sums tags b, b+G, ... with all its threads (one CTA
+      // row per thread)
+      for (int i = b; i < P.ntags; i += G) {
+        int64_t part = 0;
+        for (int c2 = t; c2 < G; c2 += UP_THREADS) part += __ldcg(P.hist + G + (int64_t)c2 * P.ntags + i);
+        int64_t sum;
+        block_scan_excl_i64(part, ws, &sum);
+        if (t == 0) P.tag_cnt[i] = sum;
+      }
     }
   }
   if (b == 0 && t == 0) {
