@@ -756,13 +756,12 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   }
 }
 
-static void win_kernels_init() {
-  static bool done = false;
-  if (done) return;
+static void win_kernels_init(Ctx& c) {
+  if (c.win_init) return;
   MSG_CUDA(cudaFuncSetAttribute(k_window_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
   MSG_CUDA(cudaFuncSetAttribute(k_window_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
   MSG_CUDA(cudaFuncSetAttribute(k_windows_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwSmem)));
-  done = true;
+  c.win_init = true;
 }
 
 // ---------------------------------------------------------------------------
@@ -1529,16 +1528,16 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     c.ms_ctr.exact(1 << 16);
     c.ms_tot.exact(257 * MS_MAX_PASSES);
   }
-  static int grid_cap = 0, coop_grid = 0;
-  if (!grid_cap) {
+  if (!c.ms_grid_cap) {
     int per_sm = 0, sms = 0, coop_per_sm = 0;
     MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_ms_onesweep, MS_THREADS, 0));
     MSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
     MSG_CUDA(cudaFuncSetAttribute(k_ms_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MC_SMEM));
     MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&coop_per_sm, k_ms_coop, MC_THREADS, MC_SMEM));
-    grid_cap = std::max(1, per_sm) * std::max(1, sms);
-    coop_grid = coop_per_sm * sms;
+    c.ms_grid_cap = std::max(1, per_sm) * std::max(1, sms);
+    c.ms_coop_grid = coop_per_sm * sms;
   }
+  const int grid_cap = c.ms_grid_cap, coop_grid = c.ms_coop_grid;
   // on-chip cooperative path when every CTA's chunk records fit in shared memory
   const int32_t* src0 = c.order[c.cur].p + c.head;
   const int32_t apad = (int32_t)((reinterpret_cast<uintptr_t>(src0) & 15) >> 2);
@@ -1798,7 +1797,7 @@ static bool build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
     c.s.iv.resize(need_iv, st);
     MSG_CUDA(cudaMemcpyAsync(c.s.iv.p, wd.data(), nwin * sizeof(WinDesc), cudaMemcpyHostToDevice, st));
     (void)dwd;
-    win_kernels_init();
+    win_kernels_init(c);
     k_window_runs<<<nwin, 1024, kWinSmem, st>>>(reinterpret_cast<const WinDesc*>(c.s.iv.p),
                                                 c.s.i64a.p, c.s.i64b.p, c.s.i32a.p, o, kWinSmem);
     MSG_CHECK_LAUNCH();
@@ -1827,7 +1826,7 @@ static bool build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
   P.seg_cls = c.s.i32c.p;
   P.nseg_out = P.seg_hi + 2 * M;
   P.ncls_out = P.nseg_out + 1;
-  win_kernels_init();
+  win_kernels_init(c);
   if (fused) {
     FusedWinParams F{};
     for (int w = 0; w < nwin; ++w) F.wd[w] = wd[w];
@@ -2027,7 +2026,7 @@ void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_
   P.seg_cls = c.s.i32c.p;
   P.nseg_out = P.seg_hi + 2 * Mb;
   P.ncls_out = P.nseg_out + 1;
-  win_kernels_init();
+  win_kernels_init(c);
   k_window_combine<<<1, 1024, kWinSmem, st>>>(P, kWinSmem);
   MSG_CHECK_LAUNCH();
   add_launches(1);
@@ -2549,7 +2548,7 @@ void window_runs_explicit(Ctx& c, const int64_t* first, const int64_t* end, cons
   o.run_a = rb.p; o.run_b = rb.p + scratch; o.run_d = rb.p + 2 * scratch;
   o.run_base = rb.p + 3 * scratch; o.nruns = o.run_base + 1; o.pages = o.nruns + 1;
   o.run_lab = rl.p;
-  win_kernels_init();
+  win_kernels_init(c);
   k_window_runs<<<1, 1024, kWinSmem, st>>>(d_wd.p, ka.p, va.p, lab.p, o, kWinSmem);
   MSG_CHECK_LAUNCH();
   add_launches(1);

@@ -268,13 +268,13 @@ void touch_counts_dev(Ctx& c, TaskTab& t, int32_t lo, int32_t hi, int64_t* out) 
 
 void units_plan(Ctx& c, const RangeSet& R, int64_t units_cap, int64_t* tag_cnt, int32_t ntags, int64_t cap,
                 int32_t* out, int64_t plan_capacity, int64_t* total_out) {
-  static int per_sm = -1, sms = 0;
-  if (per_sm < 0) {
+  if (c.up_per_sm < 0) {
     const int max_smem = 4 * UP_MAX_TAGS + 16 * (UP_SMEM_RANGES + 1) + 64;
     MSG_CUDA(cudaFuncSetAttribute(k_units_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
-    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_units_plan, UP_THREADS, max_smem));
-    MSG_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c.device));
+    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.up_per_sm, k_units_plan, UP_THREADS, max_smem));
+    MSG_CUDA(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, c.device));
   }
+  const int per_sm = c.up_per_sm, sms = c.nsm;
   if (ntags > UP_MAX_TAGS) throw Error(MSG_E_INVAL, "too many commands in one window for the units plan");
   int G = (int)std::min<int64_t>(std::max<int64_t>((units_cap + 2047) / 2048, 1), (int64_t)std::max(per_sm, 1) * sms);
   c.up_hist.resize((int64_t)G * (1 + std::max(ntags, 0)) + 1, c.st);

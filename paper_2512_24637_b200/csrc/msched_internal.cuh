@@ -238,6 +238,9 @@ struct Ctx {
   DVec<int32_t> ms_hist;                // per-CTA digit counts of the cooperative multisplit (+ 2 total rows)
   int ms_tot_par = 0;                   // which total row the next cooperative launch accumulates into
   DVec<int32_t> up_hist;                // k_units_plan per-CTA totals and tag partials
+  // per-device kernel setup (dynamic shared memory attributes are per device)
+  bool win_init = false;
+  int ms_grid_cap = 0, ms_coop_grid = 0, up_per_sm = -1, nsm = 0;
   uint32_t ms_epoch = 0;
   std::vector<int64_t> dbg[4];
   ~Ctx();
