@@ -1550,7 +1550,7 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     vcap = ((int64_t)MC_SMEM - MC_FIXED - 8 * (nch + 1)) / 4 - 4;   // + 16-B over-read slack
     vcap = std::min<int64_t>(vcap, E) & ~int64_t(3);
   }
-  const bool coop = vcap >= 0 && !(c.debug & 8);
+  const bool coop = vcap >= 0 && !(c.debug & 8) && !(c.fallback & 2);
   cudaEvent_t e0, e1;
   MSG_CUDA(cudaEventCreate(&e0));
   MSG_CUDA(cudaEventCreate(&e1));
@@ -1790,7 +1790,8 @@ static bool build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
   o.run_base = rbuf + 3 * off; o.nruns = o.run_base + nwin; o.pages = o.nruns + nwin;
   c.s.i32b.resize(off, st);
   o.run_lab = c.s.i32b.p;
-  const bool fused = wb.total_iv <= FW_MAX_IV && nwin <= FW_MAX_WIN && (int64_t)c.span_first.size() <= FW_MAX_SPANS;
+  const bool fused = wb.total_iv <= FW_MAX_IV && nwin <= FW_MAX_WIN && (int64_t)c.span_first.size() <= FW_MAX_SPANS &&
+                     !(c.fallback & 1);
   if (!fused) {
     DVec<WinDesc>& dwd = *reinterpret_cast<DVec<WinDesc>*>(&c.s.iv);  // reuse Iv buffer as raw bytes
     size_t need_iv = (nwin * sizeof(WinDesc) + sizeof(Iv) - 1) / sizeof(Iv);
@@ -1834,14 +1835,14 @@ static bool build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
     F.out = o;
     F.span_first = c.d_span_first.p; F.span_dense = c.d_span_dense.p; F.nspans = (int32_t)c.span_first.size();
     F.seg_lo = P.seg_lo; F.seg_hi = P.seg_hi; F.seg_cls = P.seg_cls; F.nseg_out = P.nseg_out; F.ncls_out = P.ncls_out;
-    if (dem) F.R = *dem; else F.R.nr = nullptr;
+    if (dem && !(c.fallback & 4)) F.R = *dem; else F.R.nr = nullptr;
     // one element per thread in every phase: 2N endpoints bound them all
     int threads = 64;
     while (threads < 2 * wb.total_iv) threads <<= 1;
     k_windows_fused<<<1, threads, sizeof(FwSmem), st>>>(F);
     MSG_CHECK_LAUNCH();
     add_launches(1);
-    return dem != nullptr;
+    return F.R.nr != nullptr;
   }
   k_window_combine<<<1, 1024, kWinSmem, st>>>(P, kWinSmem);
   MSG_CHECK_LAUNCH();

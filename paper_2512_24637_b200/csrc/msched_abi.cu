@@ -3,6 +3,8 @@
 // msg::Error and returns its code; no exception crosses the ABI.
 #include "msched_internal.cuh"
 
+#include <cstdlib>
+
 #include <algorithm>
 #include <cstring>
 
@@ -147,6 +149,14 @@ int msg_create(const msg_cfg* cfg, msg_ctx** out) {
     MSG_CUDA(cudaMallocHost(&c.hstate, sizeof(DevState)));
     std::memset(c.hstate, 0, sizeof(DevState));
     c.hbuf.reserve(1 << 16);
+    // test hook: MSG_FALLBACK=windows,onesweep,demand runs the general kernels
+    // in place of the fast paths, so the golden tests cover both
+    if (const char* f = std::getenv("MSG_FALLBACK")) {
+      std::string v(f);
+      if (v.find("windows") != std::string::npos) c.fallback |= 1;
+      if (v.find("onesweep") != std::string::npos) c.fallback |= 2;
+      if (v.find("demand") != std::string::npos) c.fallback |= 4;
+    }
   });
   if (rc != MSG_OK) {
     std::fprintf(stderr, "msg_create: %s\n", ctx->c.err.c_str());

@@ -231,6 +231,7 @@ struct Ctx {
   msg_stats stats{};
   // parity dumps
   int debug = 0;   // 1: plan lists, 2: full list orders
+  int fallback = 0;   // MSG_FALLBACK test hook: 1 two-kernel windows, 2 look-back multisplit, 4 demand kernel
   // single-pass multisplit state
   DVec<unsigned long long> ms_status;   // 256 per tile, epoch-tagged
   DVec<int32_t> ms_ctr;                 // tile claim counter per epoch

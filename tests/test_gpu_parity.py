@@ -92,3 +92,25 @@ def test_gpu_migration_moves_the_right_bytes(name, mode):
     got = dataclasses.asdict(m)
     got.pop("normalized_throughput")
     assert got == want["metrics"]
+
+
+FALLBACK_CASES = ["llm_2.0", "stream_ind", "frag", "struct", "feed", "opt_3", "cfg3_2.0"]
+
+
+@pytest.mark.parametrize("name", [n for n in FALLBACK_CASES if any(c["name"] == n for c in loader.sims())])
+def test_general_kernels_match_reference(name, monkeypatch):
+    """The general kernels the fast paths stand in for (two-kernel window
+    build, look-back multisplit, separate demand collection) reproduce the
+    reference too (MSG_FALLBACK test hook, read at context creation)."""
+    monkeypatch.setenv("MSG_FALLBACK", "windows,onesweep,demand")
+    case = loader.sim_case(name)
+    for mode, want in case["runs"].items():
+        if "error" in want:
+            continue
+        m, sim, rec = run_gpu(case, mode)
+        got = dataclasses.asdict(m)
+        got.pop("normalized_throughput")
+        assert got == want["metrics"], (name, mode)
+        assert [[e.t, e.kind, e.task_id, e.pages] for e in sim.events] == want["events"]
+        want_rec = loader.sample_refresh_orders(loader.canon_records(want["records"]), 1)
+        assert loader.align_sampled(loader.canon_records(rec), want_rec) == want_rec
