@@ -473,6 +473,13 @@ def main():
         with open(tpath) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
     achieved = ms_bytes / (ms_kernel_ms * 1e6) if ms_kernel_ms else 0.0
+    # the same launches timed by the kernel itself (%globaltimer, first CTA
+    # start to last CTA end): the event span above also holds launch latency
+    dev_timed = None
+    if st.get("ms_dev_launches"):
+        dms = st["ms_dev_ms"] / st["ms_dev_launches"]
+        dev_timed = {"avg_launch_ms": dms, "achieved": ms_bytes / (dms * 1e6),
+                     "frac": ms_bytes / (dms * 1e6) / hbm_peak, "launches_per_step": st["ms_dev_launches"]}
     large = None if args.skip_large else multisplit_large(local, hbm_peak)
     cpu, cpu_m = cpu_baseline(args, tasks, hw, pol)
     mig = None
@@ -505,6 +512,7 @@ def main():
                      "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic,
                      "algorithmic_bytes_per_launch": ms_bytes, "avg_launch_ms": ms_kernel_ms,
+                     "device_timed": dev_timed,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs" if peaks else "fallback 6650 GB/s"},
         "roofline_large_list": large,
         "migration": mig,

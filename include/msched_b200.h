@@ -170,6 +170,11 @@ typedef struct {
    * found non-resident, and the consumer stream's busy time (CUDA events) */
   int64_t run_cmds, run_pages, run_bad_tags, run_missing;
   double run_ms;
+  /* the cooperative multisplit's launches timed on the device itself
+   * (%globaltimer, first CTA start to last CTA end): ms_ms minus launch
+   * latency */
+  int64_t ms_dev_launches;
+  double ms_dev_ms;
 } msg_stats;
 
 /* Forget all residency (bitmap, list, frames); keep the task tables and the

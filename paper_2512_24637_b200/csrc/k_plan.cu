@@ -1177,6 +1177,8 @@ struct McArgs {
   int64_t E;             // aligned entries per CTA (multiple of MC_BLOCK)
   int32_t vcap;          // entries per CTA kept in shared memory (multiple of MC_BLOCK)
   int32_t nch_cap;       // chunk records per CTA
+  unsigned long long* t_first;   // globaltimer of the first CTA to start (atomicMin)
+  unsigned long long* t_last;    // globaltimer of the last CTA to finish (atomicMax)
 };
 
 // TMA bulk copy global -> shared, completion counted on an mbarrier.
@@ -1218,7 +1220,14 @@ __device__ __forceinline__ int ms_digit(const SegView& S, int32_t x, int32_t c_l
   return (seg_find(S, x).cls >> shift) & 255;
 }
 
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
+  if (threadIdx.x == 0) atomicMin(A.t_first, global_ns());   // device-side launch duration (stats)
   extern __shared__ __align__(16) unsigned char mc_raw[];
   int32_t* lo32 = reinterpret_cast<int32_t*>(mc_raw);
   int32_t* hi32 = lo32 + MS_SMEM_SEGS;
@@ -1449,6 +1458,8 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       }
     }
   }
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(A.t_last, global_ns());
 }
 
 // generic exclusive scan (int32 in -> int64 out), 3 phases
@@ -1510,6 +1521,20 @@ int32_t* next_barrier(Ctx& c) {
   }
   if (c.ms_epoch == 1) MSG_CUDA(cudaMemsetAsync(c.ms_ctr.p, 0, (1 << 16) * 4, c.st));
   return c.ms_ctr.p + c.ms_epoch;
+}
+
+// Sum the device-timed durations of the cooperative multisplit launches not
+// yet counted (stats); syncs the planner stream.
+void ms_harvest(Ctx& c) {
+  if (!c.ms_tring.p || c.ms_tslot <= c.ms_tbase) return;
+  const int64_t R = (int64_t)c.ms_tring.n / 2;
+  std::vector<unsigned long long> h(2 * R);
+  MSG_CUDA(cudaMemcpyAsync(h.data(), c.ms_tring.p, h.size() * 8, cudaMemcpyDeviceToHost, c.st));
+  MSG_CUDA(cudaStreamSynchronize(c.st));
+  for (int64_t k = c.ms_tbase; k < c.ms_tslot; ++k)
+    if (h[R + k] > h[k]) c.ms_dev_ms_acc += (double)(h[R + k] - h[k]) * 1e-6;
+  c.stats.ms_dev_launches += c.ms_tslot - c.ms_tbase;
+  c.ms_tbase = c.ms_tslot;
 }
 
 // Stable multisplit of order[cur][head, head+len) by class digits; result
@@ -1575,8 +1600,19 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     if (coop) {
       int32_t* totb = c.ms_hist.p + 256 * (int64_t)coop_grid;
       const int32_t a = (int32_t)((reinterpret_cast<uintptr_t>(src) & 15) >> 2);
+      if (!c.ms_tring.p || c.ms_tslot >= (int64_t)c.ms_tring.n / 2) {   // (first, last) slot per launch
+        if (!c.ms_tring.p) c.ms_tring.exact(2 * 4096);
+        else ms_harvest(c);
+        MSG_CUDA(cudaMemsetAsync(c.ms_tring.p, 0xff, 4096 * 8, c.st));
+        MSG_CUDA(cudaMemsetAsync(c.ms_tring.p + 4096, 0, 4096 * 8, c.st));
+        c.ms_tslot = 0;
+        c.ms_tbase = 0;
+      }
+      unsigned long long* tf = c.ms_tring.p + c.ms_tslot;
+      unsigned long long* tl = c.ms_tring.p + 4096 + c.ms_tslot;
+      ++c.ms_tslot;
       McArgs A{src - a, n + a, a, T, 8 * pass, dst, c.ms_hist.p, totb + 256 * c.ms_tot_par,
-               totb + 256 * (c.ms_tot_par ^ 1), bar, E, (int32_t)vcap, (int32_t)nch};
+               totb + 256 * (c.ms_tot_par ^ 1), bar, E, (int32_t)vcap, (int32_t)nch, tf, tl};
       c.ms_tot_par ^= 1;
       void* args[] = {&A};
       MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS),

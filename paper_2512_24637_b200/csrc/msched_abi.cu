@@ -3,6 +3,8 @@
 // msg::Error and returns its code; no exception crosses the ABI.
 #include "msched_internal.cuh"
 
+#include <vector>
+
 #include <cstdlib>
 
 #include <algorithm>
@@ -351,6 +353,7 @@ int msg_get_stats(msg_ctx* ctx, msg_stats* out) {
       MSG_CUDA(cudaMemcpy(acc, c.d_run_acc, sizeof(acc), cudaMemcpyDeviceToHost));
       s.run_pages = (int64_t)acc[0]; s.run_bad_tags = (int64_t)acc[1]; s.run_missing = (int64_t)acc[2];
     }
+    ms_harvest(c);
     double r = 0;
     for (auto& pr : c.busy_run) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) r += ms; }
     cudaGetLastError();
@@ -365,6 +368,8 @@ int msg_get_stats(msg_ctx* ctx, msg_stats* out) {
     for (auto& pr : c.busy_ms) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) m += ms; }
     cudaGetLastError();
     s.ms_ms = m;
+    s.ms_dev_launches = c.stats.ms_dev_launches;
+    s.ms_dev_ms = c.ms_dev_ms_acc;
     *out = s;
   });
 }
@@ -404,6 +409,9 @@ int msg_reset(msg_ctx* ctx, int32_t keep_tasks) {
     int64_t k = c.stats.kernels;
     c.stats = msg_stats{};
     c.stats.kernels = k;
+    c.ms_dev_ms_acc = 0.0;
+    c.ms_tslot = (int64_t)c.ms_tring.n / 2;   // next launch re-initialises the ring
+    c.ms_tbase = c.ms_tslot;
     for (auto& v : c.dbg) v.clear();
     MSG_CUDA(cudaStreamSynchronize(c.st));
   });

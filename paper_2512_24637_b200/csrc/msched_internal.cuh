@@ -239,6 +239,9 @@ struct Ctx {
   DVec<int32_t> ms_hist;                // per-CTA digit counts of the cooperative multisplit (+ 2 total rows)
   int ms_tot_par = 0;                   // which total row the next cooperative launch accumulates into
   DVec<int32_t> up_hist;                // k_units_plan per-CTA totals and tag partials
+  DVec<unsigned long long> ms_tring;    // k_ms_coop device timestamps: [first starts | last ends] per launch
+  int64_t ms_tslot = 0, ms_tbase = 0;   // next slot; slots before ms_tbase were already summed
+  double ms_dev_ms_acc = 0.0;
   // per-device kernel setup (dynamic shared memory attributes are per device)
   bool win_init = false;
   int ms_grid_cap = 0, ms_coop_grid = 0, up_per_sm = -1, nsm = 0;
@@ -273,6 +276,7 @@ void list_plan(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int6
 void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_t* win, int32_t n, int32_t nwin,
                   int64_t* win_pages);
 void pull_state(Ctx& c);   // sync + copy DevState to the host mirrors
+void ms_harvest(Ctx& c);   // accumulate device-timed multisplit launches into the stats
 void push_state(Ctx& c);
 
 void scan_flags(Ctx& c, const int32_t* in, int64_t n, int64_t* out);   // exclusive scan
