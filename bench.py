@@ -396,6 +396,10 @@ def main():
     launches = (sim.ctx.stats()["kernels"] - k0) // args.steps
     ms_step = max_over_ranks(torch, statistics.mean(times), ws, dev)
     pages_step = sum_over_ranks(torch, m.planned_pages, ws, dev)
+    # host-link bytes moved per step by all ranks together (weak scaling: each
+    # GPU has its own PCIe link, so the ceiling is N x the per-GPU duplex peak)
+    link_bytes_all = sum_over_ranks(torch, (stats_acc["h2d_bytes"] + stats_acc["d2h_bytes"]) / max(args.steps, 1),
+                                    ws, dev)
     value = pages_step / (ms_step / 1e3)
     # e2e: the public API from host Task objects every step (encode, H2D of
     # the command tables, K1 prediction on the device, replay, metrics back)
@@ -493,6 +497,9 @@ def main():
                "frac_h2d": h2d / peak["h2d"] if peak["h2d"] else None,
                "frac_d2h": d2h / peak["d2h"] if peak["d2h"] else None,
                "peak_duplex_gbs": peak["duplex"], "frac_duplex": both / peak["duplex"] if peak["duplex"] else None,
+               "all_ranks_gbs": link_bytes_all / (ms_step * 1e6),
+               "all_ranks_frac_duplex": (link_bytes_all / (ms_step * 1e6)) / (ws * peak["duplex"])
+               if peak["duplex"] else None,
                "peak_kind": "measured live: pinned 1 GiB cudaMemcpyAsync per direction, and both directions at "
                             "once on two streams (duplex), best of 3",
                "ce_batches": st["ce_batches"], "sm_batches": st["sm_batches"],
