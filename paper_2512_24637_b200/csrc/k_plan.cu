@@ -2503,15 +2503,21 @@ __global__ void k_table_from_iv(const Iv* iv, int64_t n, int64_t* lo, int64_t* h
 // refresh madvise(actual) as a two-class multisplit.
 void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out, int64_t* evicted_out) {
   TaskTab& t = *c.tasks[task];
+  cudaStream_t st = c.st;
   c.dbg[3].clear();
+  c.s.uscr.resize(512, st);
   for (int32_t cmd = c0; cmd < c1; ++cmd) {
-    msg_touch_out o{};
-    int64_t i0 = t.act_off[cmd], niv = t.act_off[cmd + 1] - i0;
+    const int64_t i0 = t.act_off[cmd], niv = t.act_off[cmd + 1] - i0;
     int64_t n = 0;
     if (niv) {
-      touch_counts(c, t, cmd, cmd + 1);
-      MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, c.s.tc.p, 8, cudaMemcpyDeviceToHost, c.st));
-      MSG_CUDA(cudaStreamSynchronize(c.st));
+      // missing pages of the command (count + list in page order): the one
+      // host round trip of the command
+      const int64_t nu = t.act_units[cmd + 1] - t.act_units[cmd];
+      ranges_from_actual(c, t, cmd, cmd + 1, c.s.ract);
+      c.s.miss.resize(std::max<int64_t>(32 * nu, 1), st);
+      units_plan(c, c.s.ract.set(), nu, nullptr, 0, -1, c.s.miss.p, -1, c.s.uscr.p + 400);
+      MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, c.s.uscr.p + 400, 8, cudaMemcpyDeviceToHost, st));
+      MSG_CUDA(cudaStreamSynchronize(st));
       n = c.hbuf.p[0];
     }
     missing_out[cmd - c0] = n;
@@ -2521,9 +2527,20 @@ void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out
                                       std::to_string(c.C) + " pages)");
     }
     if (n) {
-      int64_t over = c.len + n - c.C;
-      touch_slow(c, task, cmd, over > 0 ? over : 0, nullptr, 0, cmd + 1, t.kind[cmd] == MSG_CMD_H2D, &o, nullptr);
-      evicted_out[cmd - c0] = o.evicted;
+      // capacity evictions from the LRU head, then install (engine.py:408-419)
+      const int64_t over = std::max<int64_t>(c.len + n - c.C, 0);
+      int64_t* mig = mig_buf(c, over + n);
+      const int64_t free_before = c.C - c.len;
+      const int64_t ev = std::min(over, c.len);
+      if (c.debug & 3) {
+        dump_dense(c, c.order[c.cur].p + c.head, ev, c.dbg[1]);
+        dump_dense(c, c.s.miss.p, n, c.dbg[2]);
+      }
+      evict_head_n(c, ev, mig);
+      compact_if_needed(c);
+      install_pages(c, c.s.miss.p, n, mig ? mig + ev : nullptr);
+      if (mig) migrate_batch(c, ev, n, free_before, t.kind[cmd] != MSG_CMD_H2D);
+      evicted_out[cmd - c0] = ev;
       if (c.debug & 3) {  // [cmd, nmiss, miss..., nev, ev...] per faulting command
         auto& u = c.dbg[3];
         u.push_back(cmd);
@@ -2534,19 +2551,20 @@ void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out
       }
     }
     if (niv && c.len) {
+      // LRU refresh madvise(actual) (engine.py:398-401, 425-426): a two-class multisplit
       DVec<int64_t>& tb = c.s.tb;
       DVec<int32_t>& tcls = c.s.tcls;
-      tb.resize(2 * niv + 2, c.st);
-      tcls.resize(niv, c.st);
-      k_table_from_iv<<<grid_for(niv, 256), 256, 0, c.st>>>(t.act_pool.p + i0, niv, tb.p, tb.p + niv, tcls.p,
-                                                           tb.p + 2 * niv);
+      tb.resize(2 * niv + 2, st);
+      tcls.resize(niv, st);
+      k_table_from_iv<<<grid_for(niv, 256), 256, 0, st>>>(t.act_pool.p + i0, niv, tb.p, tb.p + niv, tcls.p,
+                                                         tb.p + 2 * niv);
       MSG_CHECK_LAUNCH();
       add_launches(1);
       SegTab T{tb.p, tb.p + niv, tcls.p, tb.p + 2 * niv};
       multisplit(c, T, 1);
     }
   }
-  MSG_CUDA(cudaStreamSynchronize(c.st));
+  MSG_CUDA(cudaStreamSynchronize(st));
 }
 
 }  // namespace msg
