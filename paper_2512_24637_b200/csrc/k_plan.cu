@@ -2550,8 +2550,10 @@ void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out
         u.insert(u.end(), c.dbg[1].begin(), c.dbg[1].end());
       }
     }
-    if (niv && c.len) {
-      // LRU refresh madvise(actual) (engine.py:398-401, 425-426): a two-class multisplit
+    // LRU refresh madvise(actual) (engine.py:398-401, 425-426): a two-class
+    // multisplit -- unless every page of the set was just installed, in page
+    // order, at the tail, where the refresh leaves it
+    if (niv && c.len && n != t.act_pages[cmd]) {
       DVec<int64_t>& tb = c.s.tb;
       DVec<int32_t>& tcls = c.s.tcls;
       tb.resize(2 * niv + 2, st);

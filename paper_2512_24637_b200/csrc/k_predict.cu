@@ -256,6 +256,7 @@ struct NormParams {
   Iv* out;                   // normalised intervals written at raw offsets
   int64_t* nout;             // normalised counts
   int64_t* nunits;           // 32-page bitmap words the command's intervals cover
+  int64_t* npages;           // pages of the command's intervals inside the dense map
   const int64_t* span_first;
   const int64_t* span_n;
   const int64_t* span_dense;
@@ -305,7 +306,7 @@ __global__ void k_normalize(NormParams P) {
   int64_t base = P.off[c];
   const int64_t* raw = P.raw + 2 * base;
   if (n == 0) {
-    if (threadIdx.x == 0) { P.nout[c] = 0; P.nunits[c] = 0; }
+    if (threadIdx.x == 0) { P.nout[c] = 0; P.nunits[c] = 0; P.npages[c] = 0; }
     return;
   }
   int64_t npow2 = 1;
@@ -327,7 +328,7 @@ __global__ void k_normalize(NormParams P) {
   // (touching runs merge: core.py:184 uses a <= prev_end).  Done by thread 0 for
   // small n; large n uses a chunked scan of running maxima.
   if (threadIdx.x == 0) {
-    int64_t m = 0, units = 0;
+    int64_t m = 0, units = 0, pages = 0;
     int64_t ca = key[0], cb = val[0];
     bool bad = false;
     Iv* out = P.out + base;
@@ -339,11 +340,12 @@ __global__ void k_normalize(NormParams P) {
       int64_t d = dense_of(P, ca, cb);
       if (d < 0 && P.strict) bad = true;
       out[m++] = Iv{ca, cb, d};
-      if (d >= 0) units += ((d + (cb - ca) + 31) >> 5) - (d >> 5);
+      if (d >= 0) { units += ((d + (cb - ca) + 31) >> 5) - (d >> 5); pages += cb - ca; }
       if (i < n) { ca = key[i]; cb = val[i]; }
     }
     P.nout[c] = m;
     P.nunits[c] = units;
+    P.npages[c] = pages;
     if (bad) atomicExch(P.err, 2);
   }
   (void)run_end_scan;
@@ -427,20 +429,22 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
 
   // normalise both sets
   DVec<Iv> np_, na_; np_.exact(std::max<int64_t>(tp, 1)); na_.exact(std::max<int64_t>(ta, 1));
-  DVec<int64_t> nn; nn.exact(4 * (int64_t)ncmd);
+  DVec<int64_t> nn; nn.exact(6 * (int64_t)ncmd);   // counts | units | pages, pred then act
   DVec<int64_t> gk; gk.exact(4 * std::max(tp, ta) + 4);
   NormParams N{};
   N.span_first = c.d_span_first.p; N.span_n = c.d_span_n.p; N.span_dense = c.d_span_dense.p;
   N.nspans = (int32_t)c.span_first.size(); N.err = err.p; N.gkeys = gk.p;
   N.strict = !(c.cfg.flags & MSG_F_LOOSE_DOMAIN);
   N.raw = rawp.p; N.off = P.off_pred; N.cnt = P.cnt_pred; N.out = np_.p; N.nout = nn.p; N.nunits = nn.p + 2 * ncmd;
+  N.npages = nn.p + 4 * ncmd;
   k_normalize<<<ncmd, kNormThreads, 0, st>>>(N);
   MSG_CHECK_LAUNCH();
   N.raw = rawa.p; N.off = P.off_act; N.cnt = P.cnt_act; N.out = na_.p; N.nout = nn.p + ncmd; N.nunits = nn.p + 3 * ncmd;
+  N.npages = nn.p + 5 * ncmd;
   k_normalize<<<ncmd, kNormThreads, 0, st>>>(N);
   MSG_CHECK_LAUNCH(); add_launches(2);
-  std::vector<int64_t> hn(4 * (size_t)ncmd);
-  MSG_CUDA(cudaMemcpyAsync(hn.data(), nn.p, 4 * ncmd * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  std::vector<int64_t> hn(6 * (size_t)ncmd);
+  MSG_CUDA(cudaMemcpyAsync(hn.data(), nn.p, 6 * ncmd * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(herr, err.p, sizeof(herr), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaStreamSynchronize(st));
   if (herr[0] == 2) throw Error(MSG_E_DOMAIN, "predicted or accessed page outside the dense page map");
@@ -455,6 +459,7 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
     t.act_off.push_back(pa);
     t.pred_units.push_back(t.pred_units.back() + hn[2 * ncmd + i]);
     t.act_units.push_back(t.act_units.back() + hn[3 * ncmd + i]);
+    t.act_pages.push_back(hn[5 * ncmd + i]);
     t.selfpop.push_back(cmds[i].kind == MSG_CMD_H2D);
     t.kind.push_back((uint8_t)cmds[i].kind);
   }

@@ -102,6 +102,7 @@ struct TaskTab {
   // host mirrors of the interval CSR offsets (pred / actual) into the pools
   std::vector<int64_t> pred_off{0}, act_off{0};
   std::vector<int64_t> pred_units{0}, act_units{0};   // cumulative bitmap-word units per command
+  std::vector<int64_t> act_pages;                    // pages of each command's actual set (dense map)
   std::vector<uint8_t> selfpop, kind;
   std::vector<Rule> rules;
   std::vector<int32_t> kern_off{0};
