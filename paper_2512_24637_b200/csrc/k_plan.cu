@@ -557,7 +557,7 @@ __device__ __forceinline__ int32_t fw_lb(const uint64_t* a, int32_t n, uint64_t 
 __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   extern __shared__ __align__(16) unsigned char fw_raw[];
   FwSmem& s = *reinterpret_cast<FwSmem*>(fw_raw);
-  const int t = threadIdx.x, lane = t & 31;
+  const int t = threadIdx.x;
   const int W = P.nwin;
   if (t == 0) {
     s.ioff[0] = 0; s.coff[0] = 0;

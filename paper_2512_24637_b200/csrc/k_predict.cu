@@ -300,7 +300,6 @@ __device__ int64_t dense_of(const NormParams& P, int64_t a, int64_t b) {
 
 __global__ void k_normalize(NormParams P) {
   __shared__ int64_t sk[kNormSmem], sv[kNormSmem];
-  __shared__ int64_t run_end_scan[kNormThreads];
   int c = blockIdx.x;
   int64_t n = P.cnt[c];
   int64_t base = P.off[c];
@@ -348,7 +347,6 @@ __global__ void k_normalize(NormParams P) {
     P.npages[c] = pages;
     if (bad) atomicExch(P.err, 2);
   }
-  (void)run_end_scan;
 }
 
 __global__ void k_compact_iv(const Iv* src, const int64_t* src_off, const int64_t* cnt, const int64_t* dst_off,
