@@ -1829,11 +1829,10 @@ static bool build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
   const bool fused = wb.total_iv <= FW_MAX_IV && nwin <= FW_MAX_WIN && (int64_t)c.span_first.size() <= FW_MAX_SPANS &&
                      !(c.fallback & 1);
   if (!fused) {
-    DVec<WinDesc>& dwd = *reinterpret_cast<DVec<WinDesc>*>(&c.s.iv);  // reuse Iv buffer as raw bytes
+    // the window descriptors go through the Iv scratch buffer, sized in Iv units
     size_t need_iv = (nwin * sizeof(WinDesc) + sizeof(Iv) - 1) / sizeof(Iv);
     c.s.iv.resize(need_iv, st);
     MSG_CUDA(cudaMemcpyAsync(c.s.iv.p, wd.data(), nwin * sizeof(WinDesc), cudaMemcpyHostToDevice, st));
-    (void)dwd;
     win_kernels_init(c);
     k_window_runs<<<nwin, 1024, kWinSmem, st>>>(reinterpret_cast<const WinDesc*>(c.s.iv.p),
                                                 c.s.i64a.p, c.s.i64b.p, c.s.i32a.p, o, kWinSmem);
