@@ -1359,32 +1359,32 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     for (int w = 0; w < MC_WARPS; ++w) { int32_t t = cnt[w][tid]; cnt[w][tid] = acc; acc += t; }
     __stcg(A.hist + (int64_t)blockIdx.x * 256 + tid, acc);
     if (acc) atomicAdd(A.tot + tid, acc);
+    red[1024 + tid] = acc;   // this slice's digit counts
+    red[tid] = 0;            // prefix accumulators
   }
+  if (tid == 0) red[2304] = 0;
   grid_barrier(A.bar);
   // ---- phase 2: digit bases = totals scan + this CTA's prefix over the
-  // histogram rows of the CTAs before it (16-byte loads, 16 row groups)
+  // CTAs before it.  Only the digits present in this slice need a base (long
+  // runs make that a handful), so the CTA reads those columns of the earlier
+  // rows -- one round of independent loads -- instead of whole rows.
   {
-    const int qd = tid & 63, g = tid >> 6;      // digits 4qd..4qd+3, rows g, g+16, ...
-    int4 pre = make_int4(0, 0, 0, 0);
-    const int me = (int)blockIdx.x;
-    for (int r0 = g; r0 < me; r0 += 64) {
-      int4 v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        int c = r0 + 16 * u;
-        v[u] = c < me ? __ldcg(reinterpret_cast<const int4*>(A.hist + (int64_t)c * 256) + qd) : make_int4(0, 0, 0, 0);
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) { pre.x += v[u].x; pre.y += v[u].y; pre.z += v[u].z; pre.w += v[u].w; }
+    int32_t* dl = red + 2048;   // present digits
+    if (tid < 256 && red[1024 + tid] > 0) dl[atomicAdd(&red[2304], 1)] = tid;
+    __syncthreads();
+    const int nd = red[2304], me = (int)blockIdx.x;
+    for (int k = tid; k < nd * me; k += MC_THREADS) {
+      const int j = k / me, c2 = k - j * me;
+      const int d = dl[j];
+      const int32_t v = __ldcg(A.hist + (int64_t)c2 * 256 + d);
+      if (v) atomicAdd(&red[d], v);
     }
-    reinterpret_cast<int4*>(red + g * 256)[qd] = pre;
   }
   __syncthreads();
   {
     int64_t pre = 0, tot = 0, x = 0;
     if (tid < 256) {
-#pragma unroll
-      for (int g = 0; g < 16; ++g) pre += red[g * 256 + tid];
+      pre = red[tid];
       tot = __ldcg(A.tot + tid);
       x = tot;
 #pragma unroll
