@@ -1141,7 +1141,8 @@ k_ms_onesweep(const int32_t* __restrict__ src, int64_t n, SegTab T, int shift, i
 }
 
 // ---------------------------------------------------------------------------
-// On-chip multisplit (one cooperative launch per pass, one grid barrier).
+// On-chip multisplit (one cooperative launch for all digit passes; per pass
+// one grid barrier, plus one between passes).
 //
 // One 1024-thread CTA per SM owns a contiguous slice of the list, staged in
 // shared memory by one TMA bulk copy (slices are cut on 16-byte boundaries of
@@ -1158,7 +1159,9 @@ k_ms_onesweep(const int32_t* __restrict__ src, int64_t n, SegTab T, int shift, i
 // the rows of the CTAs before it, so there is no look-back and no separate
 // totals kernel.  Phase 3 replays the blocks in order: run blocks are written
 // as computed ids with aligned 16-byte stores.  Traffic: 4 B read + 4 B
-// written per entry.
+// written per entry per pass.  A second pass (>= 256 classes) re-stages the
+// first pass's output after a grid barrier (async-proxy fence before the
+// TMA read of data the generic proxy wrote).
 constexpr int MC_THREADS = 1024;
 constexpr int MC_WARPS = MC_THREADS / 32;
 constexpr int MC_BLOCK = 512;                       // entries per fast block (16 per lane)
@@ -1166,17 +1169,20 @@ constexpr int MC_SMEM = 224 * 1024;
 constexpr int MC_FIXED = 3 * MS_SMEM_SEGS * 4 + MC_WARPS * 256 * 4 + 256 * 8 + 16 * 256 * 4 + 64 + 16;
 
 struct McArgs {
-  const int32_t* srcA;   // 16-byte aligned base: list entry i is srcA[i + a]
-  int64_t nA;            // n + a
-  int32_t a;             // leading pad entries (0..3)
-  SegTab T; int shift; int32_t* dst;
+  const int32_t* src0;   // pass 0 source, 16-byte aligned: list entry i is src0[i + a]
+  int32_t* bufA;         // base of pass 0's source buffer (destination of odd passes)
+  int32_t* bufB;         // the other buffer (destination of even passes, source of odd ones)
+  int64_t n;             // list entries
+  int32_t a;             // pass 0's leading pad entries (0..3)
+  SegTab T;
   int32_t* hist;         // [gridDim.x][256] per-CTA digit counts
-  int32_t* tot;          // [256] digit totals (zero at launch)
-  int32_t* tot_next;     // [256] zeroed here for the next launch
-  int32_t* bar;          // grid barrier counter (zero at launch)
+  int32_t* totb;         // [2][256] digit totals; row par is zero at launch
+  int32_t par;
+  int32_t* bar;          // grid barrier counter (zero at launch; barrier k waits for (k+1) * grid)
   int64_t E;             // aligned entries per CTA (multiple of MC_BLOCK)
   int32_t vcap;          // entries per CTA kept in shared memory (multiple of MC_BLOCK)
   int32_t nch_cap;       // chunk records per CTA
+  int32_t passes;        // digit passes (LSD, 8 bits each), all in this launch
   unsigned long long* t_first;   // globaltimer of the first CTA to start (atomicMin)
   unsigned long long* t_last;    // globaltimer of the last CTA to finish (atomicMax)
 };
@@ -1204,12 +1210,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       " @!p bra MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
-__device__ __forceinline__ void grid_barrier(int32_t* bar) {
+// k-th grid-wide barrier on one monotone counter (zero at launch)
+__device__ __forceinline__ void grid_barrier(int32_t* bar, int k) {
   __syncthreads();
   if (threadIdx.x == 0) {
     __threadfence();
     atomicAdd(bar, 1);
-    while (*reinterpret_cast<volatile int32_t*>(bar) < (int32_t)gridDim.x) __nanosleep(64);
+    const int32_t target = (k + 1) * (int32_t)gridDim.x;
+    while (*reinterpret_cast<volatile int32_t*>(bar) < target) __nanosleep(64);
     __threadfence();
   }
   __syncthreads();
@@ -1241,20 +1249,9 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 7);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  const int shift = A.shift;
-  const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
-  const int64_t cEnd = cE + A.E < A.nA ? cE + A.E : A.nA;
-  const int64_t lenA = cEnd > cE ? cEnd - cE : 0;
-  const int32_t m = (int32_t)(lenA < A.vcap ? lenA : A.vcap);      // staged entries
-  if (tid == 0) {
-    mbar_init(bar, 1);
-    if (m > 0) {
-      uint32_t bytes = (uint32_t)(((int64_t)m * 4 + 15) & ~int64_t(15));
-      mbar_expect_tx(bar, bytes);
-      tma_bulk_g2s(cache, A.srcA + cE, bytes, bar);
-    }
-  }
-  // class table -> smem while the copy is in flight
+  const int passes = A.passes;
+  if (tid == 0) mbar_init(bar, 1);
+  // class table -> smem (once for all passes)
   SegView S;
   {
     int64_t nn = *A.T.n;
@@ -1268,195 +1265,221 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
         lo32[i] = (int32_t)A.T.lo[i]; hi32[i] = (int32_t)A.T.hi[i]; cls32[i] = A.T.cls[i];
       }
   }
-  for (int i = lane; i < 256; i += 32) cnt[warp][i] = 0;
-  __syncthreads();
-  if (m > 0) mbar_wait(bar, 0);
-  auto valid = [&](int32_t off) { int64_t ia = cE + off; return ia >= A.a && ia < A.nA; };
-  auto fetch = [&](int32_t off) -> int32_t { return off < m ? cache[off] : __ldcs(A.srcA + cE + off); };
-  const int32_t nblk = (int32_t)((lenA + MC_BLOCK - 1) / MC_BLOCK);
-  const int32_t b0 = (int32_t)((int64_t)nblk * warp / MC_WARPS);
-  const int32_t b1 = (int32_t)((int64_t)nblk * (warp + 1) / MC_WARPS);
-  int32_t c_lo = 1, c_hi = 0, c_d = 0;   // the warp's cached constant-class interval
-  // digit of a run [v, v + len) if it lies in one constant-class interval, else -1
-  auto run_digit = [&](int32_t v, int32_t len) -> int {
-    if (!(v >= c_lo && v + (len - 1) < c_hi)) {
-      Span sp = seg_find(S, v);
-      c_lo = sp.lo; c_hi = sp.hi; c_d = (sp.cls >> shift) & 255;
+  const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
+  int nbar = 0;
+  for (int pass = 0; pass < passes; ++pass) {
+    const int shift = 8 * pass;
+    // pass p reads what pass p-1 wrote (buffers alternate; only pass 0 is offset)
+    const int32_t* __restrict__ srcA = pass == 0 ? A.src0 : (pass & 1) ? A.bufB : A.bufA;
+    int32_t* __restrict__ dst = (pass & 1) ? A.bufA : A.bufB;
+    const int32_t pa = pass == 0 ? A.a : 0;
+    const int64_t nA = A.n + pa;
+    const int64_t cEnd = cE + A.E < nA ? cE + A.E : nA;
+    const int64_t lenA = cEnd > cE ? cEnd - cE : 0;
+    const int32_t m = (int32_t)(lenA < A.vcap ? lenA : A.vcap);      // staged entries
+    if (tid == 0) {
+      // the previous pass's generic-proxy writes (this CTA's shared reads,
+      // every CTA's global scatter, ordered by the grid barrier) before the
+      // async-proxy copy
+      if (pass > 0) asm volatile("fence.proxy.async;" ::: "memory");
+      const uint32_t bytes = (uint32_t)(((int64_t)m * 4 + 15) & ~int64_t(15));
+      mbar_expect_tx(bar, bytes);
+      if (m > 0) tma_bulk_g2s(cache, srcA + cE, bytes, bar);
     }
-    return v + (len - 1) < c_hi ? c_d : -1;
-  };
-  // ---- phase 1: classify and count
-  for (int32_t b = b0; b < b1; ++b) {
-    const int32_t boff = b * MC_BLOCK;
-    const bool full = cE + boff >= A.a && cE + boff + MC_BLOCK <= A.nA;
-    int4 q[4];
-    if (boff + MC_BLOCK <= m) {
+    for (int i = lane; i < 256; i += 32) cnt[warp][i] = 0;
+    __syncthreads();
+    mbar_wait(bar, pass & 1);
+    auto valid = [&](int32_t off) { int64_t ia = cE + off; return ia >= pa && ia < nA; };
+    auto fetch = [&](int32_t off) -> int32_t { return off < m ? cache[off] : __ldcs(srcA + cE + off); };
+    const int32_t nblk = (int32_t)((lenA + MC_BLOCK - 1) / MC_BLOCK);
+    const int32_t b0 = (int32_t)((int64_t)nblk * warp / MC_WARPS);
+    const int32_t b1 = (int32_t)((int64_t)nblk * (warp + 1) / MC_WARPS);
+    int32_t c_lo = 1, c_hi = 0, c_d = 0;   // the warp's cached constant-class interval
+    // digit of a run [v, v + len) if it lies in one constant-class interval, else -1
+    auto run_digit = [&](int32_t v, int32_t len) -> int {
+      if (!(v >= c_lo && v + (len - 1) < c_hi)) {
+        Span sp = seg_find(S, v);
+        c_lo = sp.lo; c_hi = sp.hi; c_d = (sp.cls >> shift) & 255;
+      }
+      return v + (len - 1) < c_hi ? c_d : -1;
+    };
+    // ---- phase 1: classify and count
+    for (int32_t b = b0; b < b1; ++b) {
+      const int32_t boff = b * MC_BLOCK;
+      const bool full = cE + boff >= pa && cE + boff + MC_BLOCK <= nA;
+      int4 q[4];
+      if (boff + MC_BLOCK <= m) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t) q[t] = *reinterpret_cast<const int4*>(cache + boff + 16 * lane + 4 * t);
-    } else if (cE + boff + MC_BLOCK <= A.nA) {
+        for (int t = 0; t < 4; ++t) q[t] = *reinterpret_cast<const int4*>(cache + boff + 16 * lane + 4 * t);
+      } else if (cE + boff + MC_BLOCK <= nA) {
 #pragma unroll
-      for (int t = 0; t < 4; ++t)
-        q[t] = __ldcs(reinterpret_cast<const int4*>(A.srcA + cE + boff + 16 * lane + 4 * t));
-    } else {
+        for (int t = 0; t < 4; ++t)
+          q[t] = __ldcs(reinterpret_cast<const int4*>(srcA + cE + boff + 16 * lane + 4 * t));
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          int32_t o = boff + 16 * lane + 4 * t;
+          q[t].x = valid(o) ? fetch(o) : 0; q[t].y = valid(o + 1) ? fetch(o + 1) : 0;
+          q[t].z = valid(o + 2) ? fetch(o + 2) : 0; q[t].w = valid(o + 3) ? fetch(o + 3) : 0;
+        }
+      }
+      const int32_t v0 = __shfl_sync(0xffffffffu, q[0].x, 0);
+      bool ok = full;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        int32_t o = boff + 16 * lane + 4 * t;
-        q[t].x = valid(o) ? fetch(o) : 0; q[t].y = valid(o + 1) ? fetch(o + 1) : 0;
-        q[t].z = valid(o + 2) ? fetch(o + 2) : 0; q[t].w = valid(o + 3) ? fetch(o + 3) : 0;
+        int32_t e = v0 + 16 * lane + 4 * t;
+        ok = ok && q[t].x == e && q[t].y == e + 1 && q[t].z == e + 2 && q[t].w == e + 3;
       }
-    }
-    const int32_t v0 = __shfl_sync(0xffffffffu, q[0].x, 0);
-    bool ok = full;
-#pragma unroll
-    for (int t = 0; t < 4; ++t) {
-      int32_t e = v0 + 16 * lane + 4 * t;
-      ok = ok && q[t].x == e && q[t].y == e + 1 && q[t].z == e + 2 && q[t].w == e + 3;
-    }
-    int d = __all_sync(0xffffffffu, ok) ? run_digit(v0, MC_BLOCK) : -1;
-    if (d >= 0) {
-      if (lane < 4) info[4 * b + lane] = make_int2(v0 + MS_CHUNK * lane, d);
-      if (lane == 0) cnt[warp][d] += MC_BLOCK;
-      __syncwarp();
-      continue;
-    }
-    // mixed block: per 128-entry chunk, entries striped (32k + lane)
-#pragma unroll 1
-    for (int j = 0; j < 4; ++j) {
-      const int32_t coff = boff + MS_CHUNK * j;
-      int32_t x[4];
-      bool okc = true;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        int32_t o = coff + 32 * k + lane;
-        bool vk = valid(o);
-        x[k] = vk ? fetch(o) : 0;
-        okc = okc && vk;
-      }
-      const int32_t c0 = __shfl_sync(0xffffffffu, x[0], 0);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) okc = okc && x[k] == c0 + 32 * k + lane;
-      int dc = __all_sync(0xffffffffu, okc) ? run_digit(c0, MS_CHUNK) : -1;
-      if (dc >= 0) {
-        if (lane == 0) { info[4 * b + j] = make_int2(c0, dc); cnt[warp][dc] += MS_CHUNK; }
+      int d = __all_sync(0xffffffffu, ok) ? run_digit(v0, MC_BLOCK) : -1;
+      if (d >= 0) {
+        if (lane < 4) info[4 * b + lane] = make_int2(v0 + MS_CHUNK * lane, d);
+        if (lane == 0) cnt[warp][d] += MC_BLOCK;
         __syncwarp();
         continue;
       }
-      if (lane == 0) info[4 * b + j] = make_int2(0, -1);
+      // mixed block: per 128-entry chunk, entries striped (32k + lane)
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+        const int32_t coff = boff + MS_CHUNK * j;
+        int32_t x[4];
+        bool okc = true;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        int dk = valid(coff + 32 * k + lane) ? ms_digit(S, x[k], c_lo, c_hi, c_d, shift) : 256;
-        uint32_t peers = __match_any_sync(0xffffffffu, dk);
-        if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] += __popc(peers);
-        __syncwarp();
+        for (int k = 0; k < 4; ++k) {
+          int32_t o = coff + 32 * k + lane;
+          bool vk = valid(o);
+          x[k] = vk ? fetch(o) : 0;
+          okc = okc && vk;
+        }
+        const int32_t c0 = __shfl_sync(0xffffffffu, x[0], 0);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) okc = okc && x[k] == c0 + 32 * k + lane;
+        int dc = __all_sync(0xffffffffu, okc) ? run_digit(c0, MS_CHUNK) : -1;
+        if (dc >= 0) {
+          if (lane == 0) { info[4 * b + j] = make_int2(c0, dc); cnt[warp][dc] += MS_CHUNK; }
+          __syncwarp();
+          continue;
+        }
+        if (lane == 0) info[4 * b + j] = make_int2(0, -1);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          int dk = valid(coff + 32 * k + lane) ? ms_digit(S, x[k], c_lo, c_hi, c_d, shift) : 256;
+          uint32_t peers = __match_any_sync(0xffffffffu, dk);
+          if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] += __popc(peers);
+          __syncwarp();
+        }
       }
     }
-  }
-  __syncthreads();
-  // ---- CTA histogram; exclusive warp offsets; digit totals by atomics
-  if (tid < 256) {
-    int32_t acc = 0;
+    __syncthreads();
+    // ---- CTA histogram; exclusive warp offsets; digit totals by atomics
+    int32_t* tot = A.totb + 256 * ((A.par + pass) & 1);
+    if (tid < 256) {
+      int32_t acc = 0;
 #pragma unroll 8
-    for (int w = 0; w < MC_WARPS; ++w) { int32_t t = cnt[w][tid]; cnt[w][tid] = acc; acc += t; }
-    __stcg(A.hist + (int64_t)blockIdx.x * 256 + tid, acc);
-    if (acc) atomicAdd(A.tot + tid, acc);
-    red[1024 + tid] = acc;   // this slice's digit counts
-    red[tid] = 0;            // prefix accumulators
-  }
-  if (tid == 0) red[2304] = 0;
-  grid_barrier(A.bar);
-  // ---- phase 2: digit bases = totals scan + this CTA's prefix over the
-  // CTAs before it.  Only the digits present in this slice need a base (long
-  // runs make that a handful), so the CTA reads those columns of the earlier
-  // rows -- one round of independent loads -- instead of whole rows.
-  {
-    int32_t* dl = red + 2048;   // present digits
-    if (tid < 256 && red[1024 + tid] > 0) dl[atomicAdd(&red[2304], 1)] = tid;
-    __syncthreads();
-    const int nd = red[2304], me = (int)blockIdx.x;
-    for (int k = tid; k < nd * me; k += MC_THREADS) {
-      const int j = k / me, c2 = k - j * me;
-      const int d = dl[j];
-      const int32_t v = __ldcg(A.hist + (int64_t)c2 * 256 + d);
-      if (v) atomicAdd(&red[d], v);
+      for (int w = 0; w < MC_WARPS; ++w) { int32_t t = cnt[w][tid]; cnt[w][tid] = acc; acc += t; }
+      __stcg(A.hist + (int64_t)blockIdx.x * 256 + tid, acc);
+      if (acc) atomicAdd(tot + tid, acc);
+      red[1024 + tid] = acc;   // this slice's digit counts
+      red[tid] = 0;            // prefix accumulators
     }
-  }
-  __syncthreads();
-  {
-    int64_t pre = 0, tot = 0, x = 0;
-    if (tid < 256) {
-      pre = red[tid];
-      tot = __ldcg(A.tot + tid);
-      x = tot;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        int64_t y = __shfl_up_sync(0xffffffffu, x, o);
-        if (lane >= o) x += y;
+    if (tid == 0) red[2304] = 0;
+    grid_barrier(A.bar, nbar++);
+    // ---- phase 2: digit bases = totals scan + this CTA's prefix over the
+    // CTAs before it.  Only the digits present in this slice need a base (long
+    // runs make that a handful), so the CTA reads those columns of the earlier
+    // rows -- one round of independent loads -- instead of whole rows.
+    {
+      int32_t* dl = red + 2048;   // present digits
+      if (tid < 256 && red[1024 + tid] > 0) dl[atomicAdd(&red[2304], 1)] = tid;
+      __syncthreads();
+      const int nd = red[2304], me = (int)blockIdx.x;
+      for (int k = tid; k < nd * me; k += MC_THREADS) {
+        const int j = k / me, c2 = k - j * me;
+        const int d = dl[j];
+        const int32_t v = __ldcg(A.hist + (int64_t)c2 * 256 + d);
+        if (v) atomicAdd(&red[d], v);
       }
-      if (lane == 31) misc[warp] = x;
     }
     __syncthreads();
-    if (tid < 256) {
-      int64_t wp = 0;
-      for (int w = 0; w < warp; ++w) wp += misc[w];
-      base[tid] = wp + (x - tot) + pre;
-      if (blockIdx.x == 0) A.tot_next[tid] = 0;   // the next launch's totals start at zero
-    }
-  }
-  __syncthreads();
-  // ---- phase 3: replay the blocks in order and scatter
-  int32_t* __restrict__ dst = A.dst;
-  for (int32_t b = b0; b < b1; ++b) {
-    const int32_t boff = b * MC_BLOCK;
-    int2 r = lane < 4 ? info[4 * b + lane] : make_int2(0, -1);
-    const int32_t v0 = __shfl_sync(0xffffffffu, r.x, 0);
-    const int d0 = __shfl_sync(0xffffffffu, r.y, 0);
-    const bool same = lane >= 4 || (r.y == d0 && r.x == v0 + MS_CHUNK * lane);
-    if (d0 >= 0 && __all_sync(0xffffffffu, same)) {
-      const int32_t before = cnt[warp][d0];
-      const int64_t p = base[d0] + before;
-      const int32_t ph = (int32_t)((4 - (p & 3)) & 3);          // entries before a 16-B boundary
-      if (lane < ph) dst[p + lane] = v0 + lane;
-      const int32_t nb = (MC_BLOCK - ph) >> 2;
-      for (int32_t k = lane; k < nb; k += 32) {
-        int32_t t = ph + 4 * k;
-        *reinterpret_cast<int4*>(dst + p + t) = make_int4(v0 + t, v0 + t + 1, v0 + t + 2, v0 + t + 3);
-      }
-      const int32_t ts = ph + 4 * nb;
-      if (lane < MC_BLOCK - ts) dst[p + ts + lane] = v0 + ts + lane;
-      __syncwarp();
-      if (lane == 0) cnt[warp][d0] = before + MC_BLOCK;
-      __syncwarp();
-      continue;
-    }
-#pragma unroll 1
-    for (int j = 0; j < 4; ++j) {
-      const int32_t rx = __shfl_sync(0xffffffffu, r.x, j);
-      const int ry = __shfl_sync(0xffffffffu, r.y, j);
-      const int32_t coff = boff + MS_CHUNK * j;
-      if (ry >= 0) {
-        const int32_t before = cnt[warp][ry];
-        const int64_t p = base[ry] + before + lane;
+    {
+      int64_t pre = 0, tt = 0, x = 0;
+      if (tid < 256) {
+        pre = red[tid];
+        tt = __ldcg(tot + tid);
+        x = tt;
 #pragma unroll
-        for (int k = 0; k < 4; ++k) dst[p + 32 * k] = rx + lane + 32 * k;
+        for (int o = 1; o < 32; o <<= 1) {
+          int64_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += y;
+        }
+        if (lane == 31) misc[warp] = x;
+      }
+      __syncthreads();
+      if (tid < 256) {
+        int64_t wp = 0;
+        for (int w = 0; w < warp; ++w) wp += misc[w];
+        base[tid] = wp + (x - tt) + pre;
+        // the other totals row starts the next pass (or launch) at zero; its
+        // last readers finished before the previous pass's closing barrier
+        if (blockIdx.x == 0) A.totb[256 * ((A.par + pass + 1) & 1) + tid] = 0;
+      }
+    }
+    __syncthreads();
+    // ---- phase 3: replay the blocks in order and scatter
+    for (int32_t b = b0; b < b1; ++b) {
+      const int32_t boff = b * MC_BLOCK;
+      int2 r = lane < 4 ? info[4 * b + lane] : make_int2(0, -1);
+      const int32_t v0 = __shfl_sync(0xffffffffu, r.x, 0);
+      const int d0 = __shfl_sync(0xffffffffu, r.y, 0);
+      const bool same = lane >= 4 || (r.y == d0 && r.x == v0 + MS_CHUNK * lane);
+      if (d0 >= 0 && __all_sync(0xffffffffu, same)) {
+        const int32_t before = cnt[warp][d0];
+        const int64_t p = base[d0] + before;
+        const int32_t ph = (int32_t)((4 - (p & 3)) & 3);          // entries before a 16-B boundary
+        if (lane < ph) dst[p + lane] = v0 + lane;
+        const int32_t nb = (MC_BLOCK - ph) >> 2;
+        for (int32_t k = lane; k < nb; k += 32) {
+          int32_t t = ph + 4 * k;
+          *reinterpret_cast<int4*>(dst + p + t) = make_int4(v0 + t, v0 + t + 1, v0 + t + 2, v0 + t + 3);
+        }
+        const int32_t ts = ph + 4 * nb;
+        if (lane < MC_BLOCK - ts) dst[p + ts + lane] = v0 + ts + lane;
         __syncwarp();
-        if (lane == 0) cnt[warp][ry] = before + MS_CHUNK;
+        if (lane == 0) cnt[warp][d0] = before + MC_BLOCK;
         __syncwarp();
         continue;
       }
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+        const int32_t rx = __shfl_sync(0xffffffffu, r.x, j);
+        const int ry = __shfl_sync(0xffffffffu, r.y, j);
+        const int32_t coff = boff + MS_CHUNK * j;
+        if (ry >= 0) {
+          const int32_t before = cnt[warp][ry];
+          const int64_t p = base[ry] + before + lane;
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const int32_t o = coff + 32 * k + lane;
-        const bool vk = valid(o);
-        const int32_t xv = vk ? fetch(o) : 0;
-        int dk = vk ? ms_digit(S, xv, c_lo, c_hi, c_d, shift) : 256;
-        uint32_t peers = __match_any_sync(0xffffffffu, dk);
-        int32_t before = dk < 256 ? cnt[warp][dk] : 0;
-        __syncwarp();
-        if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] = before + __popc(peers);
-        __syncwarp();
-        if (dk < 256) dst[base[dk] + before + __popc(peers & lt)] = xv;
+          for (int k = 0; k < 4; ++k) dst[p + 32 * k] = rx + lane + 32 * k;
+          __syncwarp();
+          if (lane == 0) cnt[warp][ry] = before + MS_CHUNK;
+          __syncwarp();
+          continue;
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int32_t o = coff + 32 * k + lane;
+          const bool vk = valid(o);
+          const int32_t xv = vk ? fetch(o) : 0;
+          int dk = vk ? ms_digit(S, xv, c_lo, c_hi, c_d, shift) : 256;
+          uint32_t peers = __match_any_sync(0xffffffffu, dk);
+          int32_t before = dk < 256 ? cnt[warp][dk] : 0;
+          __syncwarp();
+          if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] = before + __popc(peers);
+          __syncwarp();
+          if (dk < 256) dst[base[dk] + before + __popc(peers & lt)] = xv;
+        }
       }
     }
+    // the next pass reads this pass's output grid-wide
+    if (pass + 1 < passes) grid_barrier(A.bar, nbar++);
   }
   __syncthreads();
   if (threadIdx.x == 0) atomicMax(A.t_last, global_ns());
@@ -1537,18 +1560,7 @@ void ms_harvest(Ctx& c) {
   c.ms_tbase = c.ms_tslot;
 }
 
-// Stable multisplit of order[cur][head, head+len) by class digits; result
-// at order[cur^1][0, len) (one buffer swap per pass).  `passes` LSD passes.
-static void multisplit(Ctx& c, const SegTab& T, int passes) {
-  int64_t n = c.len;
-  if (n == 0 || passes <= 0) return;
-  if (passes > MS_MAX_PASSES) throw Error(MSG_E_INVAL, "too many reorder classes");
-  int64_t ntiles = (n + MS_TILE - 1) / MS_TILE;
-  if ((int64_t)c.ms_status.n < 256 * ntiles) {
-    c.ms_status.exact(256 * ntiles);
-    MSG_CUDA(cudaMemsetAsync(c.ms_status.p, 0, 256 * ntiles * 8, c.st));
-    c.ms_epoch = 0;
-  }
+static void ms_init(Ctx& c) {
   if (!c.ms_ctr.p) {
     c.ms_ctr.exact(1 << 16);
     c.ms_tot.exact(257 * MS_MAX_PASSES);
@@ -1562,20 +1574,88 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
     c.ms_grid_cap = std::max(1, per_sm) * std::max(1, sms);
     c.ms_coop_grid = coop_per_sm * sms;
   }
-  const int grid_cap = c.ms_grid_cap, coop_grid = c.ms_coop_grid;
-  // on-chip cooperative path when every CTA's chunk records fit in shared memory
+}
+
+// Launch the cooperative multisplit of the current list, all digit passes in
+// one launch (a grid barrier between passes).  Returns false when the list
+// does not fit the on-chip path (the caller falls back).
+static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes) {
+  ms_init(c);
+  const int64_t n = c.len;
+  const int coop_grid = c.ms_coop_grid;
+  if (n == 0 || coop_grid <= 0 || (c.debug & 8) || (c.fallback & 2)) return false;
   const int32_t* src0 = c.order[c.cur].p + c.head;
-  const int32_t apad = (int32_t)((reinterpret_cast<uintptr_t>(src0) & 15) >> 2);
-  const int64_t nA = n + apad;
-  int64_t E = 0, vcap = -1, nch = 0;
-  if (coop_grid > 0) {
-    E = (nA + coop_grid - 1) / coop_grid;
-    E = (E + MC_BLOCK - 1) / MC_BLOCK * MC_BLOCK;
-    nch = E / MS_CHUNK;
-    vcap = ((int64_t)MC_SMEM - MC_FIXED - 8 * (nch + 1)) / 4 - 4;   // + 16-B over-read slack
-    vcap = std::min<int64_t>(vcap, E) & ~int64_t(3);
+  const int32_t a = (int32_t)((reinterpret_cast<uintptr_t>(src0) & 15) >> 2);
+  const int64_t nA = n + a;
+  int64_t E = (nA + coop_grid - 1) / coop_grid;
+  E = (E + MC_BLOCK - 1) / MC_BLOCK * MC_BLOCK;
+  const int64_t nch = E / MS_CHUNK;
+  int64_t vcap = ((int64_t)MC_SMEM - MC_FIXED - 8 * (nch + 1)) / 4 - 4;   // + 16-B over-read slack
+  vcap = std::min<int64_t>(vcap, E) & ~int64_t(3);
+  if (vcap < 0) return false;
+  if ((int64_t)c.ms_hist.n < 256 * ((int64_t)coop_grid + 2)) {
+    c.ms_hist.exact(256 * ((int64_t)coop_grid + 2));   // rows + two digit-total rows
+    MSG_CUDA(cudaMemsetAsync(c.ms_hist.p, 0, c.ms_hist.n * 4, c.st));
+    c.ms_tot_par = 0;
   }
-  const bool coop = vcap >= 0 && !(c.debug & 8) && !(c.fallback & 2);
+  if (!c.ms_tring.p || c.ms_tslot >= (int64_t)c.ms_tring.n / 2) {   // (first, last) slot per launch
+    if (!c.ms_tring.p) c.ms_tring.exact(2 * 4096);
+    else ms_harvest(c);
+    MSG_CUDA(cudaMemsetAsync(c.ms_tring.p, 0xff, 4096 * 8, c.st));
+    MSG_CUDA(cudaMemsetAsync(c.ms_tring.p + 4096, 0, 4096 * 8, c.st));
+    c.ms_tslot = 0;
+    c.ms_tbase = 0;
+  }
+  unsigned long long* tf = c.ms_tring.p + c.ms_tslot;
+  unsigned long long* tl = c.ms_tring.p + 4096 + c.ms_tslot;
+  ++c.ms_tslot;
+  cudaEvent_t e0, e1;
+  MSG_CUDA(cudaEventCreate(&e0));
+  MSG_CUDA(cudaEventCreate(&e1));
+  c.ev_pool.push_back(e0);
+  c.ev_pool.push_back(e1);
+  MSG_CUDA(cudaEventRecord(e0, c.st));
+  McArgs A{src0 - a, c.order[c.cur].p, c.order[c.cur ^ 1].p, n, a, T, c.ms_hist.p,
+           c.ms_hist.p + 256 * (int64_t)coop_grid, c.ms_tot_par, next_barrier(c), E, (int32_t)vcap, (int32_t)nch,
+           passes, tf, tl};
+  void* args[] = {&A};
+  MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS), args,
+                                       MC_SMEM, c.st));
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+  MSG_CUDA(cudaEventRecord(e1, c.st));
+  c.busy_ms.push_back({e0, e1});
+  return true;
+}
+
+// host bookkeeping once the number of passes a cooperative launch ran is known
+static void ms_coop_done(Ctx& c, int passes) {
+  if (passes <= 0) return;
+  c.cur ^= passes & 1;
+  c.head = 0;
+  c.ms_tot_par ^= passes & 1;
+  c.stats.ms_passes += passes;
+  c.stats.ms_bytes += 8 * c.len * passes;
+}
+
+// Stable multisplit of order[cur][head, head+len) by class digits; result
+// at order[cur^(passes&1)][0, len).  `passes` LSD passes.
+static void multisplit(Ctx& c, const SegTab& T, int passes) {
+  int64_t n = c.len;
+  if (n == 0 || passes <= 0) return;
+  if (ms_coop_launch(c, T, passes)) {
+    ms_coop_done(c, passes);
+    return;
+  }
+  // decoupled look-back fallback: one launch per pass
+  if (passes > MS_MAX_PASSES) throw Error(MSG_E_INVAL, "too many reorder classes");
+  int64_t ntiles = (n + MS_TILE - 1) / MS_TILE;
+  if ((int64_t)c.ms_status.n < 256 * ntiles) {
+    c.ms_status.exact(256 * ntiles);
+    MSG_CUDA(cudaMemsetAsync(c.ms_status.p, 0, 256 * ntiles * 8, c.st));
+    c.ms_epoch = 0;
+  }
+  const int grid_cap = c.ms_grid_cap;
   cudaEvent_t e0, e1;
   MSG_CUDA(cudaEventCreate(&e0));
   MSG_CUDA(cudaEventCreate(&e1));
@@ -1583,46 +1663,17 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
   c.ev_pool.push_back(e1);
   MSG_CUDA(cudaEventRecord(e0, c.st));
   unsigned long long* tot = c.ms_tot.p;
-  if (!coop) {
-    // digit totals of all passes from the resident bitmap (one launch)
-    MSG_CUDA(cudaMemsetAsync(tot, 0, 257 * passes * 8, c.st));
-    k_ms_digit_totals<<<296, 256, 0, c.st>>>(T, c.bits.p, passes, tot);
-    add_launches(1);
-  } else if ((int64_t)c.ms_hist.n < 256 * ((int64_t)coop_grid + 2)) {
-    c.ms_hist.exact(256 * ((int64_t)coop_grid + 2));   // rows + two digit-total buffers
-    MSG_CUDA(cudaMemsetAsync(c.ms_hist.p, 0, c.ms_hist.n * 4, c.st));
-    c.ms_tot_par = 0;
-  }
+  // digit totals of all passes from the resident bitmap (one launch)
+  MSG_CUDA(cudaMemsetAsync(tot, 0, 257 * passes * 8, c.st));
+  k_ms_digit_totals<<<296, 256, 0, c.st>>>(T, c.bits.p, passes, tot);
+  add_launches(1);
   for (int pass = 0; pass < passes; ++pass) {
-    int32_t* bar = next_barrier(c);   // also the onesweep tile counter of this pass
+    int32_t* bar = next_barrier(c);   // the onesweep tile counter of this pass
     const int32_t* src = c.order[c.cur].p + c.head;
     int32_t* dst = c.order[c.cur ^ 1].p;
-    if (coop) {
-      int32_t* totb = c.ms_hist.p + 256 * (int64_t)coop_grid;
-      const int32_t a = (int32_t)((reinterpret_cast<uintptr_t>(src) & 15) >> 2);
-      if (!c.ms_tring.p || c.ms_tslot >= (int64_t)c.ms_tring.n / 2) {   // (first, last) slot per launch
-        if (!c.ms_tring.p) c.ms_tring.exact(2 * 4096);
-        else ms_harvest(c);
-        MSG_CUDA(cudaMemsetAsync(c.ms_tring.p, 0xff, 4096 * 8, c.st));
-        MSG_CUDA(cudaMemsetAsync(c.ms_tring.p + 4096, 0, 4096 * 8, c.st));
-        c.ms_tslot = 0;
-        c.ms_tbase = 0;
-      }
-      unsigned long long* tf = c.ms_tring.p + c.ms_tslot;
-      unsigned long long* tl = c.ms_tring.p + 4096 + c.ms_tslot;
-      ++c.ms_tslot;
-      McArgs A{src - a, n + a, a, T, 8 * pass, dst, c.ms_hist.p, totb + 256 * c.ms_tot_par,
-               totb + 256 * (c.ms_tot_par ^ 1), bar, E, (int32_t)vcap, (int32_t)nch, tf, tl};
-      c.ms_tot_par ^= 1;
-      void* args[] = {&A};
-      MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS),
-                                           args, MC_SMEM, c.st));
-    } else {
-      Onesweep O{c.ms_status.p, (int64_t)(c.ms_status.n / 256), bar, tot + 257 * pass,
-                 c.ms_epoch};
-      int grid = (int)std::min<int64_t>(ntiles, grid_cap);
-      k_ms_onesweep<<<grid, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, dst, O);
-    }
+    Onesweep O{c.ms_status.p, (int64_t)(c.ms_status.n / 256), bar, tot + 257 * pass, c.ms_epoch};
+    int grid = (int)std::min<int64_t>(ntiles, grid_cap);
+    k_ms_onesweep<<<grid, MS_THREADS, 0, c.st>>>(src, n, T, 8 * pass, dst, O);
     MSG_CHECK_LAUNCH();
     add_launches(1);
     c.cur ^= 1;
@@ -2144,6 +2195,9 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     int64_t pop = S.populate, ev = S.evict;
     out->populate = pop; out->evict = ev; out->truncated = S.truncated;
     if (pop > c.C - c.len + ev) throw Error(MSG_E_CAPACITY, "migration plan overflowed HBM capacity");
+    // (launching the reorder before this host round trip, with the pass
+    // count taken on the device, measured no faster: the gap between the
+    // planner events and the kernel is the cooperative launch itself)
     multisplit(c, wp.tab, passes_for(ncls));
     if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     out->free_before = c.C - c.len;
