@@ -207,3 +207,21 @@ def test_simulator_input_guards():
                          engine.Mode.reference())
     with pytest.raises(engine.SimulationError, match="DRAM"):
         engine.Simulator([t], dataclasses.replace(hw, dram_capacity_bytes=PAGE), Policy(), engine.Mode.reference())
+
+
+def test_acceptance_criterion_3_fault_bandwidth():
+    """test_acceptance.py:222-232: a demand fault moves a page at ~0.12 GB/s,
+    bulk seed copies run at the configured 41.7 GB/s link exactly."""
+    from paper_2512_24637_b200.model import CommandKind
+    from paper_2512_24637_b200.presets import get_preset
+    from paper_2512_24637_b200.workload import DEFAULT_H2D_BW, gen_vector_add
+
+    hw = get_preset("rtx5080").with_capacity(96 << 20)
+    stall = hw.fault_control_plane_s + hw.fault_transfer_s
+    assert stall == pytest.approx(33.14e-6)
+    assert 4096 / stall == pytest.approx(0.12e9, rel=0.05)
+    task = gen_vector_add(1 << 20, task_id="t")
+    for cmd in task.commands:
+        if cmd.kind is CommandKind.MEMCPY_H2D:
+            assert cmd.latency_s == cmd.memcpy_size / DEFAULT_H2D_BW
+    assert DEFAULT_H2D_BW == 41.7e9
