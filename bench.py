@@ -8,7 +8,7 @@ HBM frame arena on the copy engines.  Metric (BASELINE.json): pages
 planned+migrated per second = (populate + evict + fault pages) / replay time.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                  [--config cfg2|cfg1|cfg3|cfg4] [--page-size B] [--no-migrate]
+                  [--config cfg2|cfg1|cfg3|cfg4|cfg4x8] [--page-size B] [--no-migrate]
 
 Multi-GPU: one process per GPU (torchrun), each replaying its own
 independent tenant mix under its own HBM budget (weak scaling, no
@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg3", "cfg4"], default="cfg2")
+    ap.add_argument("--config", choices=["cfg2", "cfg1", "cfg3", "cfg4", "cfg4x8"], default="cfg2")
     ap.add_argument("--page-size", type=int, default=0, help="config 5: override the page size (bytes)")
     ap.add_argument("--no-migrate", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=3, help="oracle replays in the cpu_baseline sample")
@@ -70,6 +70,9 @@ def workload(name, rank, page=0):
     elif name == "cfg4":
         tasks, hw, pol = scenarios.config4_llama70b(page=page or 4096, task_offset=4 * rank)
         desc = "4x 70B-class decode (70 GB weights + 5 GB KV, 3 steps), 180 GB HBM budget, RR 5 ms"
+    elif name == "cfg4x8":
+        tasks, hw, pol = scenarios.config4_llama70b(n_tenants=8, page=page or 4096, task_offset=8 * rank)
+        desc = "8x 70B-class decode (70 GB weights + 5 GB KV, 3 steps), 180 GB HBM budget (3.3x), RR 5 ms"
     else:
         tasks, hw, pol = scenarios.config2_llama8b(page=page or 4096, task_offset=3 * rank)
         desc = ("3x Llama3-8B int8 decode (7.6 GB weights + 0.9 GB KV each, 32 layers, 8 steps), "

@@ -114,3 +114,19 @@ def test_general_kernels_match_reference(name, monkeypatch):
         assert [[e.t, e.kind, e.task_id, e.pages] for e in sim.events] == want["events"]
         want_rec = loader.sample_refresh_orders(loader.canon_records(want["records"]), 1)
         assert loader.align_sampled(loader.canon_records(rec), want_rec) == want_rec
+
+
+@pytest.mark.slow
+def test_cfg4_eight_tenants_matches_oracle():
+    """Config 4 at N = 8 tenants (N in {4, 8}; 600 GB of
+    70B-class tenants against 180 GB, 87.8 M pages of domain): no golden
+    exists at this size, so the GPU replay is checked against the pinned
+    oracle port, every metric with ==."""
+    from oracle import msched_port as port
+    from paper_2512_24637_b200 import scenarios
+
+    tasks, hw, pol = scenarios.config4_llama70b(n_tenants=8)
+    want = vars(port.PortSim(tasks, hw, pol, engine.Mode.proactive()).run())
+    got = dataclasses.asdict(engine.simulate(tasks, hw, pol, engine.Mode.proactive()))
+    got.pop("normalized_throughput")
+    assert got == want
