@@ -425,8 +425,9 @@ def main():
         e2e = {"value": pages_step / (e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": int(io[-1][0]),
                "d2h_bytes_per_step": int(io[-1][1]), "ms_per_step": e_ms,
                "includes": "inside the timed region: host Task objects -> encode -> H2D of the command tables "
-                           "(pageable numpy buffers) -> device K1 prediction -> residency reset -> replay with real "
-                           "migration -> per-switch results D2H -> metrics"}
+                           "(pageable numpy buffers) -> device K1 prediction -> residency reset -> replay ("
+                           + ("migration off" if args.no_migrate else "with real migration")
+                           + ") -> per-switch results D2H -> metrics"}
     # planning only: the same replay with the copies switched off — the work
     # the reference itself does (it models migration time, it moves no bytes)
     plan_only = None
