@@ -68,13 +68,16 @@ static void set_domain(Ctx& c, const int64_t* first, const int64_t* npages, int3
     else m.push_back(x);
   }
   int64_t d = 0;
+  for (auto& x : m) d += x.second - x.first;
+  // validate before touching the context: a rejected domain leaves it unset
+  if (d >= (1ll << 31)) throw Error(MSG_E_DOMAIN, "dense page map exceeds 2^31 pages");
+  d = 0;
   for (auto& x : m) {
     c.span_first.push_back(x.first);
     c.span_n.push_back(x.second - x.first);
     c.span_dense.push_back(d);
     d += x.second - x.first;
   }
-  if (d >= (1ll << 31)) throw Error(MSG_E_DOMAIN, "dense page map exceeds 2^31 pages");
   c.D = d;
   cudaStream_t st = c.st;
   size_t ns = std::max<size_t>(m.size(), 1);
@@ -100,6 +103,10 @@ static void set_domain(Ctx& c, const int64_t* first, const int64_t* npages, int3
   c.fifo_len = c.C;
   migration_init(c);
   MSG_CUDA(cudaStreamSynchronize(st));
+}
+
+static void nonneg(int64_t n) {
+  if (n < 0) throw Error(MSG_E_INVAL, "negative count");
 }
 
 static TaskTab& task_of(Ctx& c, int32_t task) {
@@ -224,6 +231,7 @@ int msg_add_commands(msg_ctx* ctx, int32_t task, int32_t ncmd, const msg_cmd* cm
                      const uint8_t* blob, int64_t blob_len, const msg_range* gt, uint8_t* complete_out) {
   return guard(ctx, [&] {
     TaskTab& t = task_of(ctx->c, task);
+    if (ncmd < 0 || blob_len < 0) throw Error(MSG_E_INVAL, "negative count");
     predict_commands(ctx->c, t, ncmd, cmds, args, blob, blob_len, gt, complete_out);
   });
 }
@@ -248,9 +256,19 @@ int msg_read_pages(msg_ctx* ctx, int32_t task, int32_t cmd, int32_t which, int64
   });
 }
 
+// every window names a registered task and a command range inside it
+static void check_windows(Ctx& c, const msg_window* win, int32_t nwin) {
+  if (nwin < 0 || (nwin > 0 && !win)) throw Error(MSG_E_INVAL, "bad window list");
+  for (int32_t w = 0; w < nwin; ++w) {
+    TaskTab& t = task_of(c, win[w].task);
+    if (win[w].c0 < 0 || win[w].c1 < win[w].c0 || win[w].c1 > t.ncmd) throw Error(MSG_E_INVAL, "bad window range");
+  }
+}
+
 int msg_plan_switch(msg_ctx* ctx, const msg_window* win, int32_t nwin, int32_t reorder_always, msg_switch_out* out,
                     int64_t* win_pages_out, int64_t* prefix_out, int64_t* touch_cnt_out) {
   return guard(ctx, [&] {
+    check_windows(ctx->c, win, nwin);
     plan_switch(ctx->c, win, nwin, reorder_always != 0, out, win_pages_out, prefix_out, touch_cnt_out);
   });
 }
@@ -258,28 +276,39 @@ int msg_plan_switch(msg_ctx* ctx, const msg_window* win, int32_t nwin, int32_t r
 int msg_touch(msg_ctx* ctx, int32_t task, int32_t cmd, int64_t evict, const msg_window* win, int32_t nwin,
               int32_t scan_end, int32_t write_tags, msg_touch_out* out, int64_t* win_pages_out) {
   return guard(ctx, [&] {
+    check_windows(ctx->c, win, nwin);
     touch_slow(ctx->c, task, cmd, evict, win, nwin, scan_end, write_tags != 0, out, win_pages_out);
   });
 }
 
 int msg_um_slice(msg_ctx* ctx, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out, int64_t* evicted_out) {
   return guard(ctx, [&] {
-    task_of(ctx->c, task);
+    TaskTab& t = task_of(ctx->c, task);
+    if (c0 < 0 || c1 < c0 || c1 > t.ncmd) throw Error(MSG_E_INVAL, "bad command range");
     um_slice(ctx->c, task, c0, c1, missing_out, evicted_out);
   });
 }
 
 int msg_release_task(msg_ctx* ctx, const int64_t* span_first, const int64_t* span_end, int32_t nspans,
                      int64_t* removed) {
-  return guard(ctx, [&] { release_pages(ctx->c, span_first, span_end, nspans, removed); });
+  return guard(ctx, [&] {
+    nonneg(nspans);
+    release_pages(ctx->c, span_first, span_end, nspans, removed);
+  });
 }
 
 int msg_list_append(msg_ctx* ctx, const int64_t* first, const int64_t* end, int32_t n) {
-  return guard(ctx, [&] { list_append_abs(ctx->c, first, end, n); });
+  return guard(ctx, [&] {
+    nonneg(n);
+    list_append_abs(ctx->c, first, end, n);
+  });
 }
 
 int msg_list_madvise(msg_ctx* ctx, const int64_t* first, const int64_t* end, int32_t n) {
-  return guard(ctx, [&] { list_madvise_abs(ctx->c, first, end, n); });
+  return guard(ctx, [&] {
+    nonneg(n);
+    list_madvise_abs(ctx->c, first, end, n);
+  });
 }
 
 int msg_list_evict_head(msg_ctx* ctx, int64_t n, int64_t* pages_out, int64_t* nout) {
@@ -291,23 +320,35 @@ int msg_list_len(msg_ctx* ctx, int64_t* n) {
 }
 
 int msg_list_read(msg_ctx* ctx, int64_t* pages_out, int64_t cap, int64_t* n) {
-  return guard(ctx, [&] { list_read(ctx->c, pages_out, cap, n); });
+  return guard(ctx, [&] {
+    nonneg(cap);
+    list_read(ctx->c, pages_out, cap, n);
+  });
 }
 
 int msg_list_reorder(msg_ctx* ctx, const int64_t* first, const int64_t* end, const int32_t* win, int32_t n,
                      int32_t nwin, int64_t* win_pages) {
-  return guard(ctx, [&] { list_reorder(ctx->c, first, end, win, n, nwin, win_pages); });
+  return guard(ctx, [&] {
+    nonneg(n);
+    nonneg(nwin);
+    list_reorder(ctx->c, first, end, win, n, nwin, win_pages);
+  });
 }
 
 int msg_window_runs(msg_ctx* ctx, const int64_t* iv_first, const int64_t* iv_end, const int32_t* iv_cmd, int32_t niv,
                     int32_t ncmd, int64_t* runs_out, int64_t* nruns, int64_t* pages) {
-  return guard(ctx, [&] { window_runs_explicit(ctx->c, iv_first, iv_end, iv_cmd, niv, ncmd, runs_out, nruns, pages); });
+  return guard(ctx, [&] {
+    nonneg(niv);
+    nonneg(ncmd);
+    window_runs_explicit(ctx->c, iv_first, iv_end, iv_cmd, niv, ncmd, runs_out, nruns, pages);
+  });
 }
 
 int msg_list_plan(msg_ctx* ctx, const int64_t* run_first, const int64_t* run_end, int32_t nruns, int64_t capacity,
                   int64_t* populate_out, int64_t* npopulate, int64_t* evict_out, int64_t* nevict,
                   int64_t* truncated) {
   return guard(ctx, [&] {
+    nonneg(nruns);
     list_plan(ctx->c, run_first, run_end, nruns, capacity, populate_out, npopulate, evict_out, nevict, truncated);
   });
 }
