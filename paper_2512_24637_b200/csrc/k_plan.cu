@@ -1166,7 +1166,7 @@ constexpr int MC_THREADS = 1024;
 constexpr int MC_WARPS = MC_THREADS / 32;
 constexpr int MC_BLOCK = 512;                       // entries per fast block (16 per lane)
 constexpr int MC_SMEM = 224 * 1024;
-constexpr int MC_FIXED = 3 * MS_SMEM_SEGS * 4 + MC_WARPS * 256 * 4 + 256 * 8 + 16 * 256 * 4 + 64 + 16;
+constexpr int MC_FIXED = 3 * MS_SMEM_SEGS * 4 + MC_WARPS * 256 * 4 + 256 * 8 + 16 * 256 * 4 + 80 + 16;
 
 struct McArgs {
   const int32_t* src0;   // pass 0 source, 16-byte aligned: list entry i is src0[i + a]
@@ -1243,10 +1243,12 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(cls32 + MS_SMEM_SEGS);
   int64_t* base = reinterpret_cast<int64_t*>(cnt + MC_WARPS);
   int32_t* red = reinterpret_cast<int32_t*>(base + 256);          // [16][256]
-  int64_t* misc = reinterpret_cast<int64_t*>(red + 16 * 256);     // 8 x int64: warp totals; [7] = mbarrier
-  int2* info = reinterpret_cast<int2*>(misc + 8);                 // chunk records
+  int64_t* misc = reinterpret_cast<int64_t*>(red + 16 * 256);     // [0, 8): warp totals; [8]: mbarrier
+  int2* info = reinterpret_cast<int2*>(misc + 10);                // chunk records (16-B aligned)
   int32_t* cache = reinterpret_cast<int32_t*>(info + ((A.nch_cap + 1) & ~1));   // 16-B aligned
-  uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 7);
+  // the mbarrier lives for every pass: it must not share a slot with the
+  // phase-2 warp totals
+  uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 8);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = (1u << lane) - 1u;
   const int passes = A.passes;
@@ -1265,6 +1267,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
         lo32[i] = (int32_t)A.T.lo[i]; hi32[i] = (int32_t)A.T.hi[i]; cls32[i] = A.T.cls[i];
       }
   }
+  __syncthreads();   // the initialised mbarrier and the class table, before any use
   const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
   int nbar = 0;
   for (int pass = 0; pass < passes; ++pass) {

@@ -1,0 +1,23 @@
+#!/bin/bash
+# compute-sanitizer passes over the CUDA path (run on the GPU box under gpurun):
+#   gpurun --timeout 2400 -- 'bash tools/sanitize.sh'
+# memcheck on golden replays (fast paths and, via MSG_FALLBACK, the general
+# kernels) and a full cfg2 replay; racecheck and synccheck on the facade's
+# reorder tests (the cooperative multisplit, the fused window kernel).
+set -u
+O=gpurun_out/sanitize.txt
+: > $O
+run() {
+  echo "### $*" >> $O
+  timeout 1200 "$@" > /tmp/san.log 2>&1
+  grep -E "passed|failed|rep 0|SUMMARY" /tmp/san.log | tail -3 >> $O
+}
+CS="compute-sanitizer --print-limit 20"
+run $CS --tool memcheck python -m pytest tests/test_gpu_parity.py tests/test_gpu_facade.py -x -q \
+    -k "stream_2.0 or frag or opt_3 or llm_1.5 or struct or madvise or reorder or evict or plan_migration"
+MSG_FALLBACK=windows,onesweep,demand run $CS --tool memcheck python -m pytest tests/test_gpu_parity.py -x -q \
+    -k "cfg3_2.0 or frag"
+run $CS --tool memcheck python tools/prof_replay.py cfg2 1
+run $CS --tool racecheck python -m pytest tests/test_gpu_facade.py -x -q -k "multi_window or large_reorder or randomized"
+run $CS --tool synccheck python -m pytest tests/test_gpu_facade.py -x -q -k "multi_window or large_reorder"
+cat $O
