@@ -18,6 +18,10 @@ run $CS --tool memcheck python -m pytest tests/test_gpu_parity.py tests/test_gpu
 MSG_FALLBACK=windows,onesweep,demand run $CS --tool memcheck python -m pytest tests/test_gpu_parity.py -x -q \
     -k "cfg3_2.0 or frag"
 run $CS --tool memcheck python tools/prof_replay.py cfg2 1
+run $CS --tool memcheck python -m pytest tests/test_gpu_parity.py tests/test_gpu_execute.py -x -q \
+    -k "(moves_the_right_bytes and (stream_3.0 or llm_2.0 or frag)) or executed or execute_needs"
+run $CS --tool memcheck python -m pytest tests/test_gpu_abi_errors.py tests/test_gpu_tracebin.py -x -q
+run $CS --tool racecheck python -m pytest tests/test_gpu_parity.py -x -q -k "moves_the_right_bytes and (stream_3.0 or frag)"
 run $CS --tool racecheck python -m pytest tests/test_gpu_facade.py -x -q -k "multi_window or large_reorder or randomized"
 run $CS --tool synccheck python -m pytest tests/test_gpu_facade.py -x -q -k "multi_window or large_reorder"
 cat $O
