@@ -476,8 +476,10 @@ struct FwSmem {
   int32_t iw[FW_MAX_IV], icmd[FW_MAX_IV];
   uint64_t E[1024];             // unique window-tagged endpoints
   int32_t L[1024];              // first-access command per segment
-  uint64_t xk[1024], xk2[1024]; // bitonic exchange
+  uint64_t xk[1024], xk2[1024]; // bitonic exchange (two buffers: one barrier per wide stage)
   int32_t xv[1024];
+  uint64_t yk[1024], yk2[1024];
+  int32_t yv[1024];
   int64_t ra[1024], rb[1024];   // runs by id (start order), abs
   int32_t rl[1024], rsk[1024], rek[1024];
   int64_t sa[1024], sb[1024];   // runs in first-access order (window, label, start)
@@ -506,14 +508,19 @@ template <bool HI, bool PAY>
 __device__ __forceinline__ void fw_sortT(uint64_t& hi, uint64_t& lo, int32_t& v, FwSmem& s, int n) {
   const int t = threadIdx.x;
   const bool act = t < (n < 32 ? 32 : n);
+  int buf = 0;   // wide stages alternate exchange buffers, so one barrier each suffices
+  if (n > 32) __syncthreads();   // callers' earlier uses of the exchange buffers are done
   for (int kk = 2; kk <= n; kk <<= 1) {
     for (int j = kk >> 1; j > 0; j >>= 1) {
       uint64_t ph = 0, pl = 0; int32_t pv = 0;
       if (j >= 32) {
-        if (act) { if (HI) s.xk[t] = hi; s.xk2[t] = lo; if (PAY) s.xv[t] = v; }
+        uint64_t* bk = buf ? s.yk : s.xk;
+        uint64_t* bk2 = buf ? s.yk2 : s.xk2;
+        int32_t* bv = buf ? s.yv : s.xv;
+        buf ^= 1;
+        if (act) { if (HI) bk[t] = hi; bk2[t] = lo; if (PAY) bv[t] = v; }
         __syncthreads();
-        if (act) { if (HI) ph = s.xk[t ^ j]; pl = s.xk2[t ^ j]; if (PAY) pv = s.xv[t ^ j]; }
-        __syncthreads();
+        if (act) { if (HI) ph = bk[t ^ j]; pl = bk2[t ^ j]; if (PAY) pv = bv[t ^ j]; }
       } else if (act) {
         if (HI) ph = __shfl_xor_sync(0xffffffffu, hi, j);
         pl = __shfl_xor_sync(0xffffffffu, lo, j);
@@ -528,6 +535,7 @@ __device__ __forceinline__ void fw_sortT(uint64_t& hi, uint64_t& lo, int32_t& v,
       }
     }
   }
+  if (n > 32) __syncthreads();   // last wide stage's reads, before callers reuse the buffers
 }
 
 // (hi, lo, payload) triples, lexicographic; payloads unique
