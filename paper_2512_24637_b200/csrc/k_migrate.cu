@@ -161,6 +161,33 @@ void migration_init(Ctx& c) {
   }
 }
 
+static double sum_pairs(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+  double t = 0;
+  for (auto& pr : v) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) t += ms; }
+  cudaGetLastError();
+  v.clear();
+  return t;
+}
+
+// A long-lived context (no reset between replays) would otherwise keep every
+// per-batch and per-chunk event: past a bound, wait for the streams, fold the
+// busy-time pairs into running sums and release the events.  Batch events
+// become null (the batches are complete; nothing needs to wait on them).
+void fold_events(Ctx& c, size_t bound) {
+  if (c.ev_pool.size() <= bound) return;
+  for (cudaStream_t s : {c.st, c.st_d2h, c.st_h2d, c.st_run})
+    if (s) MSG_CUDA(cudaStreamSynchronize(s));
+  ms_harvest(c);
+  c.fold_h2d_ms += sum_pairs(c.busy_h2d);
+  c.fold_d2h_ms += sum_pairs(c.busy_d2h);
+  c.fold_ms_ms += sum_pairs(c.busy_ms);
+  c.fold_run_ms += sum_pairs(c.busy_run);
+  for (auto e : c.ev_pool) cudaEventDestroy(e);
+  c.ev_pool.clear();
+  std::fill(c.ev_d2h_of.begin(), c.ev_d2h_of.end(), nullptr);
+  std::fill(c.ev_h2d_of.begin(), c.ev_h2d_of.end(), nullptr);
+}
+
 static cudaEvent_t new_event(Ctx& c, bool timing) {
   cudaEvent_t e;
   MSG_CUDA(cudaEventCreateWithFlags(&e, timing ? cudaEventDefault : cudaEventDisableTiming));
@@ -270,7 +297,7 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     std::vector<std::pair<int64_t, cudaEvent_t>> done;   // (evictions complete up to, event)
     std::vector<void*> dd, ss;
     std::vector<size_t> zz;
-    if (dep_d2h >= 0 && dep_d2h < (int32_t)c.ev_h2d_of.size())
+    if (dep_d2h >= 0 && dep_d2h < (int32_t)c.ev_h2d_of.size() && c.ev_h2d_of[dep_d2h])   // null: folded, done
       MSG_CUDA(cudaStreamWaitEvent(c.st_d2h, c.ev_h2d_of[dep_d2h], 0));
     MSG_CUDA(cudaEventRecord(d2h_start, c.st_d2h));
     int64_t k = 0, next_cut = chunk;
@@ -300,7 +327,7 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     done.push_back({n_d2h, d2h_end});
     // installs: frames that were free before this batch may still be draining
     // from earlier evictions; frames freed by this batch wait for their chunk
-    if (dep_h2d >= 0 && dep_h2d < (int32_t)c.ev_d2h_of.size())
+    if (dep_h2d >= 0 && dep_h2d < (int32_t)c.ev_d2h_of.size() && c.ev_d2h_of[dep_h2d])   // null: folded, done
       MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_d2h_of[dep_h2d], 0));
     MSG_CUDA(cudaEventRecord(h2d_start, c.st_h2d));
     size_t waited = 0;

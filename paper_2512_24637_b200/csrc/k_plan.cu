@@ -2146,6 +2146,7 @@ static void touch_counts(Ctx& c, TaskTab& t, int32_t lo, int32_t hi) {
 void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_always, msg_switch_out* out,
                  int64_t* win_pages, int64_t* prefix, int64_t* touch_cnt) {
   if (nwin < 1) throw Error(MSG_E_INVAL, "need at least one window");
+  fold_events(c, c.event_bound);
   cudaStream_t st = c.st;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   MSG_CUDA(cudaEventCreate(&e0)); MSG_CUDA(cudaEventCreate(&e1));
@@ -2270,6 +2271,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
 
 void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_window* win, int32_t nwin,
                 int32_t scan_end, bool write_tags, msg_touch_out* out, int64_t* win_pages) {
+  fold_events(c, c.event_bound);
   if (task < 0 || task >= (int32_t)c.tasks.size() || !c.tasks[task]) throw Error(MSG_E_INVAL, "unknown task");
   TaskTab& t = *c.tasks[task];
   if (cmd < 0 || cmd >= t.ncmd || scan_end > t.ncmd) throw Error(MSG_E_INVAL, "bad command index");
@@ -2566,6 +2568,7 @@ __global__ void k_table_from_iv(const Iv* iv, int64_t n, int64_t* lo, int64_t* h
 // missing count, capacity evictions from the LRU head, install, and the LRU
 // refresh madvise(actual) as a two-class multisplit.
 void um_slice(Ctx& c, int32_t task, int32_t c0, int32_t c1, int64_t* missing_out, int64_t* evicted_out) {
+  fold_events(c, c.event_bound);
   TaskTab& t = *c.tasks[task];
   cudaStream_t st = c.st;
   c.dbg[3].clear();

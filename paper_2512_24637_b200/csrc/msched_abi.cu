@@ -166,6 +166,8 @@ int msg_create(const msg_cfg* cfg, msg_ctx** out) {
       if (v.find("onesweep") != std::string::npos) c.fallback |= 2;
       if (v.find("demand") != std::string::npos) c.fallback |= 4;
     }
+    // test hook: MSG_EVENT_BOUND=n folds the context's events past n (fold_events)
+    if (const char* f = std::getenv("MSG_EVENT_BOUND")) c.event_bound = (size_t)std::max(1ll, std::atoll(f));
   });
   if (rc != MSG_OK) {
     std::fprintf(stderr, "msg_create: %s\n", ctx->c.err.c_str());
@@ -395,17 +397,17 @@ int msg_get_stats(msg_ctx* ctx, msg_stats* out) {
       s.run_pages = (int64_t)acc[0]; s.run_bad_tags = (int64_t)acc[1]; s.run_missing = (int64_t)acc[2];
     }
     ms_harvest(c);
-    double r = 0;
+    double r = c.fold_run_ms;
     for (auto& pr : c.busy_run) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) r += ms; }
     cudaGetLastError();
     s.run_ms = r;
-    double h = 0, d = 0;
+    double h = c.fold_h2d_ms, d = c.fold_d2h_ms;
     for (auto& pr : c.busy_h2d) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) h += ms; }
     for (auto& pr : c.busy_d2h) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) d += ms; }
     cudaGetLastError();
     s.h2d_busy_ms = h;
     s.d2h_busy_ms = d;
-    double m = 0;
+    double m = c.fold_ms_ms;
     for (auto& pr : c.busy_ms) { float ms = 0; if (cudaEventElapsedTime(&ms, pr.first, pr.second) == cudaSuccess) m += ms; }
     cudaGetLastError();
     s.ms_ms = m;
@@ -441,6 +443,7 @@ int msg_reset(msg_ctx* ctx, int32_t keep_tasks) {
     for (auto e : c.ev_pool) cudaEventDestroy(e);
     c.ev_pool.clear();
     c.busy_h2d.clear(); c.busy_d2h.clear(); c.busy_plan.clear(); c.busy_ms.clear();
+    c.fold_h2d_ms = c.fold_d2h_ms = c.fold_ms_ms = c.fold_run_ms = 0;
     c.ev_d2h_of.clear(); c.ev_h2d_of.clear();
     c.mig_batch = 0;
     if (c.inst_ep.p) {

@@ -227,6 +227,9 @@ struct Ctx {
   std::vector<cudaEvent_t> ev_d2h_of, ev_h2d_of;   // per batch completion events
   cudaEvent_t ev_mig[2] = {nullptr, nullptr};
   std::vector<cudaEvent_t> ev_pool;
+  // busy times of event pairs already folded away (fold_events)
+  double fold_h2d_ms = 0, fold_d2h_ms = 0, fold_ms_ms = 0, fold_run_ms = 0;
+  size_t event_bound = 1 << 15;   // events kept before folding
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_h2d, busy_d2h;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_plan, busy_ms, busy_run;
   msg_stats stats{};
@@ -278,6 +281,7 @@ void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_
                   int64_t* win_pages);
 void pull_state(Ctx& c);   // sync + copy DevState to the host mirrors
 void ms_harvest(Ctx& c);   // accumulate device-timed multisplit launches into the stats
+void fold_events(Ctx& c, size_t bound);   // release events past `bound` (busy times kept as sums)
 void push_state(Ctx& c);
 
 void scan_flags(Ctx& c, const int32_t* in, int64_t n, int64_t* out);   // exclusive scan

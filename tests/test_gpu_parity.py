@@ -94,6 +94,34 @@ def test_gpu_migration_moves_the_right_bytes(name, mode):
     assert got == want["metrics"]
 
 
+@pytest.mark.parametrize("name", ["llm_2.0", "stream_3.0"])
+def test_event_folding_keeps_copies_and_timings(name, monkeypatch):
+    """A long-lived context folds its per-batch/per-chunk events into running
+    busy-time sums past a bound (fold_events): with the bound at 16 events
+    the migrating replay still matches the reference, every frame holds its
+    page, and the copy-engine busy times are still reported."""
+    monkeypatch.setenv("MSG_EVENT_BOUND", "16")
+    case = loader.sim_case(name)
+    want = case["runs"]["proactive"]
+    tasks = [loader.dec_task(t) for t in case["tasks"]]
+    tasks, feeder = loader.feeder_for(case["feeder"], tasks)
+    from paper_2512_24637_b200.model import HwConfig
+    from paper_2512_24637_b200.scheduler import Policy
+
+    sim = engine.Simulator(tasks, HwConfig(**case["hw"]), Policy(**case["policy"]), engine.Mode(**want["mode"]),
+                           feeder=feeder, migrate=True, verify=True)
+    try:
+        m = sim.run()
+        assert sim.ctx.verify() == 0
+        st = sim.ctx.stats()
+        assert st["h2d_busy_ms"] > 0 and st["d2h_busy_ms"] > 0 and st["ms_ms"] > 0
+    finally:
+        sim.close()
+    got = dataclasses.asdict(m)
+    got.pop("normalized_throughput")
+    assert got == want["metrics"]
+
+
 FALLBACK_CASES = ["llm_2.0", "stream_ind", "frag", "struct", "feed", "opt_3", "cfg3_2.0"]
 
 
