@@ -25,10 +25,12 @@ def _load(name):
 
 @functools.lru_cache(maxsize=None)
 def sims():
-    """Reference-generated simulations: make_golden.py + make_golden_extra.py."""
+    """Reference-generated simulations: make_golden.py, make_golden_extra.py,
+    make_golden_edge.py."""
     out = _load("sims.json.gz")
-    if os.path.exists(os.path.join(HERE, "sims_extra.json.gz")):
-        out = out + _load("sims_extra.json.gz")
+    for extra in ("sims_extra.json.gz", "sims_edge.json.gz"):
+        if os.path.exists(os.path.join(HERE, extra)):
+            out = out + _load(extra)
     return out
 
 
