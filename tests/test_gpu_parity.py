@@ -62,7 +62,8 @@ def test_gpu_matches_reference(name, mode):
     assert loader.align_sampled(got_rec, want_rec) == want_rec
 
 
-MIGRATION_CASES = ["llm_2.0", "stream_3.0", "stream_ind", "frag", "struct", "feed"]
+MIGRATION_CASES = ["llm_2.0", "stream_3.0", "stream_ind", "frag", "struct", "feed", "edge_tiny_ranges",
+                   "edge_capacity_plus_one", "edge_many_tasks", "edge_unknown_kernel"]
 
 
 @pytest.mark.parametrize("name", MIGRATION_CASES)
