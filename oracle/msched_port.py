@@ -182,10 +182,13 @@ class RunList:
         starts = [a for a, _ in pages]
         stay: list = []
         move: list = []
+        npg = len(pages)
         for a, b in self.runs:
             pos = a
-            i = max(bisect_right(starts, pos) - 1, 0)
-            while pos < b and i < len(pages):
+            i = bisect_right(starts, pos) - 1
+            if i < 0:
+                i = 0
+            while pos < b and i < npg:
                 c, d = pages[i]
                 if d <= pos:
                     i += 1
@@ -201,8 +204,9 @@ class RunList:
                     i += 1
             if pos < b:
                 _append_run(stay, pos, b)
+        stay.extend(move)
         merged: list = []
-        for a, b in stay + move:
+        for a, b in stay:
             _append_run(merged, a, b)
         self.runs = merged
 
