@@ -18,5 +18,8 @@ ncu --set full --import-source on --clock-control none -f -k regex:k_ms_coop -s 
     python tools/prof_replay.py cfg2 1 > /dev/null 2>&1
 ncu --set full --clock-control none -f -k regex:k_ms_coop -s 100 -c 1 -o $O/ncu_coop_cfg4 \
     python tools/prof_replay.py cfg4 1 > /dev/null 2>&1
+timeout 300 python tools/um_time.py > $O/um_time.txt 2>&1; tail -1 $O/um_time.txt
+timeout 300 python tools/ms_probe.py cfg2 3 > $O/ms_probe.txt 2>&1; timeout 300 python tools/ms_probe.py cfg4 2 >> $O/ms_probe.txt 2>&1
+tail -2 $O/ms_probe.txt
 timeout 1200 python bench.py > $O/bench.jsonl 2> $O/bench.err; tail -c 400 $O/bench.jsonl
 timeout 900 python bench.py --impl reference > $O/bench_ref.jsonl 2> $O/bench_ref.err; tail -c 300 $O/bench_ref.jsonl
