@@ -5,10 +5,14 @@ import sys
 import time
 
 sys.path.insert(0, ".")
+from paper_2512_24637_b200 import _abi  # noqa: E402
+
+if "--lib" in sys.argv:
+    _abi.LIB_PATH = sys.argv[sys.argv.index("--lib") + 1]
 from paper_2512_24637_b200 import engine, scenarios  # noqa: E402
 from paper_2512_24637_b200.analyzer import build_descriptors  # noqa: E402
 
-reps = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+reps = int(sys.argv[1]) if len(sys.argv) > 1 and sys.argv[1].isdigit() else 4
 tasks, hw, pol = scenarios.config2_llama8b()
 descs = {t.id: build_descriptors(t) for t in tasks}
 sim = engine.Simulator(tasks, hw, pol, engine.Mode.proactive(), migrate=True, execute=True, descriptors=descs)
