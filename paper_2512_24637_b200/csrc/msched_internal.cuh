@@ -52,6 +52,8 @@ struct DVec {
       cudaGetLastError();
       throw Error(MSG_E_OOM, "device allocation of " + std::to_string(nc * sizeof(T)) + " bytes failed");
     }
+    // zero-filled, so growth never carries uninitialised bytes (only on growth: geometric, rare)
+    MSG_CUDA(cudaMemsetAsync(q, 0, nc * sizeof(T), s));
     if (n) MSG_CUDA(cudaMemcpyAsync(q, p, n * sizeof(T), cudaMemcpyDeviceToDevice, s));
     if (p) { MSG_CUDA(cudaStreamSynchronize(s)); cudaFree(p); }
     p = q;

@@ -3,7 +3,8 @@
 #   gpurun --timeout 2400 -- 'bash tools/sanitize.sh'
 # memcheck on golden replays (fast paths and, via MSG_FALLBACK, the general
 # kernels) and a full cfg2 replay; racecheck and synccheck on the facade's
-# reorder tests (the cooperative multisplit, the fused window kernel).
+# reorder tests (the cooperative multisplit, the fused window kernel);
+# initcheck on golden replays.
 set -u
 O=gpurun_out/sanitize.txt
 : > $O
@@ -22,6 +23,8 @@ run $CS --tool memcheck python -m pytest tests/test_gpu_parity.py tests/test_gpu
     -k "(moves_the_right_bytes and (stream_3.0 or llm_2.0 or frag)) or executed or execute_needs"
 run $CS --tool memcheck python -m pytest tests/test_gpu_abi_errors.py tests/test_gpu_tracebin.py -x -q
 run $CS --tool racecheck python -m pytest tests/test_gpu_parity.py -x -q -k "moves_the_right_bytes and (stream_3.0 or frag)"
+run $CS --tool initcheck python -m pytest tests/test_gpu_parity.py tests/test_gpu_facade.py -x -q \
+    -k "(test_gpu_matches and (stream_2.0 or llm_1.5 or edge_tiny or frag)) or madvise or plan_migration or (moves_the_right_bytes and stream_3.0)"
 run $CS --tool racecheck python -m pytest tests/test_gpu_facade.py -x -q -k "multi_window or large_reorder or randomized"
 run $CS --tool synccheck python -m pytest tests/test_gpu_facade.py -x -q -k "multi_window or large_reorder"
 cat $O
