@@ -276,7 +276,7 @@ void units_plan(Ctx& c, const RangeSet& R, int64_t units_cap, int64_t* tag_cnt, 
   }
   const int per_sm = c.up_per_sm, sms = c.nsm;
   if (ntags > UP_MAX_TAGS) throw Error(MSG_E_INVAL, "too many commands in one window for the units plan");
-  int G = (int)std::min<int64_t>(std::max<int64_t>((units_cap + 2047) / 2048, 1), (int64_t)std::max(per_sm, 1) * sms);
+  int G = (int)std::min<int64_t>(std::max<int64_t>((units_cap + 511) / 512, 1), (int64_t)std::max(per_sm, 1) * sms);
   c.up_hist.resize((int64_t)G * (1 + std::max(ntags, 0)) + 1, c.st);
   const int nt = tag_cnt ? ntags : 0;
   const size_t smem = ((4 * (size_t)nt + 15) & ~size_t(15)) + 16 * ((size_t)UP_SMEM_RANGES + 1);
