@@ -135,6 +135,14 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
   }
   int64_t tot;
   block_scan_excl_i64(acc, ws, &tot);
+  int64_t pre_tot = 0, all_tot = tot;
+  if (G == 1) {
+    // one CTA: its totals are the grid's; no histogram round trip, no barrier
+    if (P.tag_cnt) {
+      __syncthreads();
+      for (int i = t; i < P.ntags; i += UP_THREADS) P.tag_cnt[i] = tagc[i];
+    }
+  } else {
   if (t == 0) __stcg(P.hist + b, (int32_t)tot);
   __syncthreads();
   if (P.tag_cnt)
@@ -155,7 +163,6 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
     all += v;
     if (i < b) pre += v;
   }
-  int64_t pre_tot, all_tot;
   block_scan_excl_i64(pre, ws, &pre_tot);
   block_scan_excl_i64(all, ws, &all_tot);
   if (P.tag_cnt) {
@@ -178,6 +185,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
       }
     }
   }
+  }   // G > 1
   if (b == 0 && t == 0) {
     if (P.total_out) *P.total_out = all_tot;
     if (P.S) {
