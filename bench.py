@@ -404,7 +404,8 @@ def main():
                 stats_acc = {k: 0 for k in st}
             for k, v in st.items():
                 stats_acc[k] += v if k != "kernels" else 0
-    launches = (sim.ctx.stats()["kernels"] - k0) // args.steps
+    launches_total = sim.ctx.stats()["kernels"] - k0   # our kernels inside the timed region (K steps)
+    launches = launches_total // args.steps
     ms_step = max_over_ranks(torch, statistics.mean(times), ws, dev)
     pages_step = sum_over_ranks(torch, m.planned_pages, ws, dev)
     # host-link bytes moved per step by all ranks together (weak scaling: each
@@ -556,7 +557,7 @@ def main():
         "execute": execute,
         "cpu_baseline": cpu,
         "e2e": e2e,
-        "gpu_launches": int(launches),
+        "gpu_launches": int(launches_total), "gpu_launches_per_step": int(launches),
         "clocks": clk.summary(),
         "parity": parity,
     }
