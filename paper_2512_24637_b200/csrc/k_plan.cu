@@ -1306,6 +1306,15 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     const int32_t b0 = (int32_t)((int64_t)nblk * warp / MC_WARPS);
     const int32_t b1 = (int32_t)((int64_t)nblk * (warp + 1) / MC_WARPS);
     int32_t c_lo = 1, c_hi = 0, c_d = 0;   // the warp's cached constant-class interval
+    int32_t l_lo = 1, l_hi = 0, l_d = 0;   // this lane's (per-entry paths: lane k sees every 32nd entry)
+    auto lane_digit = [&](int32_t x) -> int {
+      if (x >= c_lo && x < c_hi) return c_d;
+      if (x < l_lo || x >= l_hi) {
+        const Span sp = seg_find(S, x);
+        l_lo = sp.lo; l_hi = sp.hi; l_d = (sp.cls >> shift) & 255;
+      }
+      return l_d;
+    };
     // digit of a run [v, v + len) if it lies in one constant-class interval, else -1
     auto run_digit = [&](int32_t v, int32_t len) -> int {
       if (!(v >= c_lo && v + (len - 1) < c_hi)) {
@@ -1373,7 +1382,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
         if (lane == 0) info[4 * b + j] = make_int2(0, -1);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-          int dk = valid(coff + 32 * k + lane) ? ms_digit(S, x[k], c_lo, c_hi, c_d, shift) : 256;
+          int dk = valid(coff + 32 * k + lane) ? lane_digit(x[k]) : 256;
           uint32_t peers = __match_any_sync(0xffffffffu, dk);
           if (dk < 256 && lane == __ffs(peers) - 1) cnt[warp][dk] += __popc(peers);
           __syncwarp();
@@ -1479,7 +1488,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
           const int32_t o = coff + 32 * k + lane;
           const bool vk = valid(o);
           const int32_t xv = vk ? fetch(o) : 0;
-          int dk = vk ? ms_digit(S, xv, c_lo, c_hi, c_d, shift) : 256;
+          int dk = vk ? lane_digit(xv) : 256;
           uint32_t peers = __match_any_sync(0xffffffffu, dk);
           int32_t before = dk < 256 ? cnt[warp][dk] : 0;
           __syncwarp();
