@@ -15,7 +15,13 @@ build/%.o: paper_2512_24637_b200/csrc/%.cu $(wildcard paper_2512_24637_b200/csrc
 $(LIB): $(OBJ)
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJ) -lcudart
 
+# k_ms_coop with phase timestamps (tools/mc_phase_replay.py, tools/mc_phase_probe.py)
+phase-ts: $(filter-out build/k_plan.o,$(OBJ))
+	@mkdir -p build tools/bin
+	$(NVCC) $(NVFLAGS) -DMSG_MC_PHASE_TS -c paper_2512_24637_b200/csrc/k_plan.cu -o build/k_plan_ts.o 2> build/k_plan_ts.ptxas.log
+	$(NVCC) $(ARCH) -shared -o tools/bin/libmsched_mcts.so build/k_plan_ts.o $(filter-out build/k_plan.o,$(OBJ)) -lcudart
+
 clean:
 	rm -rf build $(LIB)
 
-.PHONY: all clean
+.PHONY: all clean phase-ts

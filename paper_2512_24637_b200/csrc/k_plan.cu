@@ -1242,7 +1242,31 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
+// Phase timestamps of k_ms_coop (instrumented build only: `make phase-ts`,
+// read by tools/mc_phase_replay.py): per stamp the earliest / latest CTA and
+// the sum over CTAs of the time since that CTA's start.
+#ifdef MSG_MC_PHASE_TS
+__device__ unsigned long long g_mc_min[16], g_mc_max[16], g_mc_sum[16], g_mc_n;
+__device__ __forceinline__ unsigned long long mc_now() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define MCTS(i)                                                                            \
+  do {                                                                                     \
+    if (threadIdx.x == 0) {                                                                \
+      const unsigned long long t_ = mc_now();                                              \
+      atomicMin(&g_mc_min[i], t_); atomicMax(&g_mc_max[i], t_); atomicAdd(&g_mc_sum[i], t_ - mc_t0); \
+    }                                                                                      \
+  } while (0)
+#define MCTS_START const unsigned long long mc_t0 = mc_now(); MCTS(0)
+#else
+#define MCTS(i) do {} while (0)
+#define MCTS_START do {} while (0)
+#endif
+
 __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
+  MCTS_START;
   if (threadIdx.x == 0) atomicMin(A.t_first, global_ns());   // device-side launch duration (stats)
   extern __shared__ __align__(16) unsigned char mc_raw[];
   int32_t* lo32 = reinterpret_cast<int32_t*>(mc_raw);
@@ -1300,6 +1324,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     for (int i = lane; i < 256; i += 32) cnt[warp][i] = 0;
     __syncthreads();
     mbar_wait(bar, pass & 1);
+    if (pass == 0) MCTS(1);
     auto valid = [&](int32_t off) { int64_t ia = cE + off; return ia >= pa && ia < nA; };
     auto fetch = [&](int32_t off) -> int32_t { return off < m ? cache[off] : __ldcs(srcA + cE + off); };
     const int32_t nblk = (int32_t)((lenA + MC_BLOCK - 1) / MC_BLOCK);
@@ -1390,6 +1415,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       }
     }
     __syncthreads();
+    if (pass == 0) MCTS(2);
     // ---- CTA histogram; exclusive warp offsets; digit totals by atomics
     int32_t* tot = A.totb + 256 * ((A.par + pass) & 1);
     if (tid < 256) {
@@ -1402,7 +1428,9 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       red[tid] = 0;            // prefix accumulators
     }
     if (tid == 0) red[2304] = 0;
+    if (pass == 0) MCTS(3);
     grid_barrier(A.bar, nbar++);
+    if (pass == 0) MCTS(4);
     // ---- phase 2: digit bases = totals scan + this CTA's prefix over the
     // CTAs before it.  Only the digits present in this slice need a base (long
     // runs make that a handful), so the CTA reads those columns of the earlier
@@ -1444,6 +1472,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       }
     }
     __syncthreads();
+    if (pass == 0) MCTS(5);
     // ---- phase 3: replay the blocks in order and scatter
     for (int32_t b = b0; b < b1; ++b) {
       const int32_t boff = b * MC_BLOCK;
@@ -1502,6 +1531,10 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     if (pass + 1 < passes) grid_barrier(A.bar, nbar++);
   }
   __syncthreads();
+  MCTS(6);
+#ifdef MSG_MC_PHASE_TS
+  if (threadIdx.x == 0) atomicAdd(&g_mc_n, 1ull);
+#endif
   if (threadIdx.x == 0) atomicMax(A.t_last, global_ns());
 }
 
@@ -2761,3 +2794,21 @@ void list_plan(Ctx& c, const int64_t* first, const int64_t* end, int32_t n, int6
 }
 
 }  // namespace msg
+
+#ifdef MSG_MC_PHASE_TS
+extern "C" void msg_dbg_mc_ts(unsigned long long* out) {
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, msg::g_mc_min, 16 * 8);
+  cudaMemcpyFromSymbol(out + 16, msg::g_mc_max, 16 * 8);
+  cudaMemcpyFromSymbol(out + 32, msg::g_mc_sum, 16 * 8);
+  cudaMemcpyFromSymbol(out + 48, msg::g_mc_n, 8);
+}
+extern "C" void msg_dbg_mc_reset() {
+  unsigned long long lo[16], hi[16] = {0}, z[16] = {0}, zn = 0;
+  for (int i = 0; i < 16; ++i) lo[i] = ~0ull;
+  cudaMemcpyToSymbol(msg::g_mc_min, lo, 128);
+  cudaMemcpyToSymbol(msg::g_mc_max, hi, 128);
+  cudaMemcpyToSymbol(msg::g_mc_sum, z, 128);
+  cudaMemcpyToSymbol(msg::g_mc_n, &zn, 8);
+}
+#endif

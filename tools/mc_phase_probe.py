@@ -1,7 +1,10 @@
+"""k_ms_coop phase timings on a synthetic list (needs `make phase-ts`; GPU box).
+
+usage: python tools/mc_phase_probe.py PAGES RUN_LEN"""
 import ctypes as C, random, sys
 sys.path.insert(0, ".")
 from paper_2512_24637_b200 import _abi
-_abi.LIB_PATH = "tools/bin/libmsched_mcts.so"
+_abi.LIB_PATH = "tools/bin/libmsched_mcts.so"   # built by `make phase-ts`
 from paper_2512_24637_b200._abi import Context
 pages, run_len = int(sys.argv[1]), int(sys.argv[2])
 rng = random.Random(1)
