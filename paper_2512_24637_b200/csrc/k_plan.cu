@@ -1284,7 +1284,19 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = (1u << lane) - 1u;
   const int passes = A.passes;
-  if (tid == 0) mbar_init(bar, 1);
+  const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
+  if (tid == 0) {
+    // pass 0's slice goes to shared memory first, so the copy overlaps the
+    // class-table load below
+    mbar_init(bar, 1);
+    const int64_t nA0 = A.n + A.a;
+    const int64_t cEnd0 = cE + A.E < nA0 ? cE + A.E : nA0;
+    const int64_t len0 = cEnd0 > cE ? cEnd0 - cE : 0;
+    const int32_t m0 = (int32_t)(len0 < A.vcap ? len0 : A.vcap);
+    const uint32_t bytes = (uint32_t)(((int64_t)m0 * 4 + 15) & ~int64_t(15));
+    mbar_expect_tx(bar, bytes);
+    if (m0 > 0) tma_bulk_g2s(cache, A.src0 + cE, bytes, bar);
+  }
   // class table -> smem (once for all passes)
   SegView S;
   {
@@ -1300,7 +1312,6 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       }
   }
   __syncthreads();   // the initialised mbarrier and the class table, before any use
-  const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
   int nbar = 0;
   for (int pass = 0; pass < passes; ++pass) {
     const int shift = 8 * pass;
@@ -1312,11 +1323,11 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     const int64_t cEnd = cE + A.E < nA ? cE + A.E : nA;
     const int64_t lenA = cEnd > cE ? cEnd - cE : 0;
     const int32_t m = (int32_t)(lenA < A.vcap ? lenA : A.vcap);      // staged entries
-    if (tid == 0) {
+    if (tid == 0 && pass > 0) {   // (pass 0's copy was issued at kernel start)
       // the previous pass's generic-proxy writes (this CTA's shared reads,
       // every CTA's global scatter, ordered by the grid barrier) before the
       // async-proxy copy
-      if (pass > 0) asm volatile("fence.proxy.async;" ::: "memory");
+      asm volatile("fence.proxy.async;" ::: "memory");
       const uint32_t bytes = (uint32_t)(((int64_t)m * 4 + 15) & ~int64_t(15));
       mbar_expect_tx(bar, bytes);
       if (m > 0) tma_bulk_g2s(cache, srcA + cE, bytes, bar);
