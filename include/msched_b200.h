@@ -239,11 +239,15 @@ int msg_um_slice(msg_ctx *ctx, int32_t task, int32_t c0, int32_t c1, int64_t *mi
  * in flight, and the hardware would stall on it) — then launch a
  * kernel that reads every page of the command's actual set from its HBM
  * frame (16-byte loads) and checks the payload tags when the context
- * verifies them.  Pass need_pages = populate count to wait for the whole
- * batch (Mode.early_start = False).  Later migrations wait for the executed
- * commands before they evict or overwrite frames.  Needs MSG_F_MIGRATE and
- * MSG_F_EXECUTE (the H2D stream publishes populate progress only then). */
-int msg_run_command(msg_ctx *ctx, int32_t task, int32_t cmd, int64_t need_pages);
+ * verifies them; the kernel then occupies the GPU until `latency_s` (the
+ * command's profiled duration, Command.latency_s, core.py:231) has passed
+ * since it started, so an executed replay runs in the time the model
+ * charges for exec_s (engine.py:373-384).  Pass need_pages = populate count
+ * to wait for the whole batch (Mode.early_start = False).  Later migrations
+ * wait for the executed commands before they evict or overwrite frames.
+ * Needs MSG_F_MIGRATE and MSG_F_EXECUTE (the H2D stream publishes populate
+ * progress only then).  latency_s < 0 or > 60 s is MSG_E_INVAL. */
+int msg_run_command(msg_ctx *ctx, int32_t task, int32_t cmd, int64_t need_pages, double latency_s);
 
 /* Release a task: drop its pages (absolute page spans) from the list. */
 int msg_release_task(msg_ctx *ctx, const int64_t *span_first, const int64_t *span_end, int32_t nspans,

@@ -126,7 +126,7 @@ def load():
         "msg_get_stats": ([vp, C.POINTER(Stats)], C.c_int),
         "msg_verify_residency": ([vp, C.POINTER(i64)], C.c_int),
         "msg_flush_l2": ([vp], C.c_int),
-        "msg_run_command": ([vp, i32, i32, i64], C.c_int),
+        "msg_run_command": ([vp, i32, i32, i64, C.c_double], C.c_int),
         "msg_analyze": ([vp, i32, vp, vp, i64, vp, vp, i32, vp, vp, vp, vp, i32, vp], C.c_int),
     }
     for name, (args, res) in sig.items():
@@ -396,10 +396,11 @@ class Context:
                                       int(write_tags), C.byref(out), _p(win_pages)))
         return out, win_pages[:nw]
 
-    def run_command(self, idx, cmd, need_pages):
+    def run_command(self, idx, cmd, need_pages, latency_s=0.0):
         """Execute a command on the device once `need_pages` of the current
-        switch's populate have landed (early-start gating)."""
-        self.check(self.lib.msg_run_command(self.h, idx, cmd, int(need_pages)))
+        switch's populate have landed (early-start gating); it reads its
+        pages and occupies the GPU for its profiled latency."""
+        self.check(self.lib.msg_run_command(self.h, idx, cmd, int(need_pages), float(latency_s)))
 
     def um_slice(self, idx, c0, c1):
         n = c1 - c0

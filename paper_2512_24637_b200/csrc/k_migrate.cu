@@ -5,8 +5,9 @@
 // order), then installs (populate order).  This file
 //   1. cuts the list into maximal segments that are contiguous in both the
 //      host backing (slot = dense page mod pool pages) and the frame arena;
-//   2. moves large segments with the copy engines (cudaMemcpyBatchAsync, one
-//      stream per direction so D2H and H2D overlap, full duplex), gating each
+//   2. moves large segments with the copy engines (one cudaMemcpyAsync per
+//      segment piece, one stream per direction so D2H and H2D overlap, full
+//      duplex), gating each
 //      install chunk on the eviction chunk that frees its frames — the real
 //      counterpart of the pipelined-swap model (engine.py:139-166);
 //   3. moves fragmented batches with SM gather/scatter kernels reading and
@@ -195,14 +196,12 @@ static cudaEvent_t new_event(Ctx& c, bool timing) {
   return e;
 }
 
-static void ce_batch(std::vector<void*>& d, std::vector<void*>& s, std::vector<size_t>& z, cudaStream_t st) {
-  if (d.empty()) return;
-  cudaMemcpyAttributes attr = {};
-  attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-  static const int overlap_flag = getenv("MSG_CE_NO_OVERLAP_HINT") ? 0 : 1;
-  attr.flags = overlap_flag ? cudaMemcpyFlagPreferOverlapWithCompute : 0;
-  size_t idx0 = 0, fail = 0;
-  MSG_CUDA(cudaMemcpyBatchAsync(d.data(), s.data(), z.data(), d.size(), &attr, &idx0, 1, &fail, st));
+// Issues the pending copy-engine pieces of one direction on `st`, one
+// cudaMemcpyAsync each (the segments are maximal runs contiguous on both
+// sides, so a piece is a large copy: cfg4 averages ~100 pieces per switch).
+static void ce_batch(std::vector<void*>& d, std::vector<void*>& s, std::vector<size_t>& z, cudaStream_t st,
+                     cudaMemcpyKind kind) {
+  for (size_t i = 0; i < d.size(); ++i) MSG_CUDA(cudaMemcpyAsync(d[i], s[i], z[i], kind, st));
   d.clear(); s.clear(); z.clear();
 }
 
@@ -314,7 +313,7 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
         c.stats.d2h_segments++;
         pos += take;
         if (pos == next_cut && pos < n_d2h) {
-          ce_batch(dd, ss, zz, c.st_d2h);
+          ce_batch(dd, ss, zz, c.st_d2h, cudaMemcpyDeviceToHost);
           cudaEvent_t e = new_event(c, false);
           MSG_CUDA(cudaEventRecord(e, c.st_d2h));
           done.push_back({pos, e});
@@ -322,13 +321,17 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
         }
       }
     }
-    ce_batch(dd, ss, zz, c.st_d2h);
+    ce_batch(dd, ss, zz, c.st_d2h, cudaMemcpyDeviceToHost);
     MSG_CUDA(cudaEventRecord(d2h_end, c.st_d2h));
     done.push_back({n_d2h, d2h_end});
     // installs: frames that were free before this batch may still be draining
     // from earlier evictions; frames freed by this batch wait for their chunk
     if (dep_h2d >= 0 && dep_h2d < (int32_t)c.ev_d2h_of.size() && c.ev_d2h_of[dep_h2d])   // null: folded, done
       MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_d2h_of[dep_h2d], 0));
+    // a page evicted by an earlier batch (its D2H writes the page's host
+    // slot) may be re-installed now into a frame that was already free: the
+    // H2D reading that slot must follow the earlier batch's write-back
+    MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_d2h_prev, 0));
     MSG_CUDA(cudaEventRecord(h2d_start, c.st_h2d));
     size_t waited = 0;
     bool any_wait = false;
@@ -339,7 +342,7 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
     const int64_t h2d_chunk = publish ? std::max<int64_t>((n_h2d + 15) / 16, 256) : INT64_MAX;
     int64_t issued = 0, published = 0;
     auto flush_h2d = [&]() {
-      ce_batch(dd, ss, zz, c.st_h2d);
+      ce_batch(dd, ss, zz, c.st_h2d, cudaMemcpyHostToDevice);
       if (publish && copy_h2d && issued > published) {
         write_progress(c, c.st_h2d, base + issued);
         published = issued;
@@ -407,8 +410,21 @@ void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bo
 // PAPER.md:1000-1009; the early-start model of engine.py:139-158, 373-378).
 // Each reads every page of its actual set from its HBM frame.
 
-__global__ void k_consume(const Iv* __restrict__ iv, int64_t n_iv, const int32_t* __restrict__ frame,
-                          const char* __restrict__ arena, int64_t P, int verify, unsigned long long* acc) {
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// lat_ns: the command's profiled duration; every CTA stays resident until
+// that long after it started (the grid is sized to be co-resident: at most
+// kConsumeCtasPerSm CTAs of 256 threads per SM), so the command occupies its
+// modeled latency even when its reads finish sooner
+constexpr int kConsumeCtasPerSm = 4;
+__global__ void __launch_bounds__(256, kConsumeCtasPerSm) k_consume(const Iv* __restrict__ iv, int64_t n_iv, const int32_t* __restrict__ frame,
+                          const char* __restrict__ arena, int64_t P, int verify, unsigned long long* acc,
+                          uint64_t lat_ns) {
+  const uint64_t t_start = lat_ns ? globaltimer_ns() : 0;
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -448,6 +464,9 @@ __global__ void k_consume(const Iv* __restrict__ iv, int64_t n_iv, const int32_t
     if (miss) atomicAdd(&acc[2], miss);
     atomicXor(&acc[3], (unsigned long long)sig);
   }
+  if (lat_ns && threadIdx.x == 0) {
+    while (globaltimer_ns() - t_start < lat_ns) __nanosleep(2000);
+  }
 }
 
 // copies of a new batch must not evict or overwrite frames that executed
@@ -457,7 +476,9 @@ void run_wait_before_copies(Ctx& c) {
   MSG_CUDA(cudaStreamWaitEvent(c.st_h2d, c.ev_run_last, 0));
 }
 
-void run_command(Ctx& c, int32_t task, int32_t cmd, int64_t need_pages) {
+void run_command(Ctx& c, int32_t task, int32_t cmd, int64_t need_pages, double latency_s) {
+  if (!(latency_s >= 0.0 && latency_s <= 60.0)) throw Error(MSG_E_INVAL, "command latency outside [0, 60] s");
+  if (!c.nsm) MSG_CUDA(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, c.device));
   if (!(c.cfg.flags & MSG_F_MIGRATE) || !(c.cfg.flags & MSG_F_EXECUTE) || !c.st_run)
     throw Error(MSG_E_INVAL, "executing commands needs MSG_F_MIGRATE | MSG_F_EXECUTE");
   if (task < 0 || task >= (int32_t)c.tasks.size() || !c.tasks[task]) throw Error(MSG_E_INVAL, "unknown task");
@@ -483,12 +504,13 @@ void run_command(Ctx& c, int32_t task, int32_t cmd, int64_t need_pages) {
   MSG_CUDA(cudaEventRecord(e0, c.st_run));
   int64_t i0 = t.act_off[cmd], niv = t.act_off[cmd + 1] - i0;
   int64_t pages = 0;
-  if (niv) {
+  const uint64_t lat_ns = (uint64_t)(latency_s * 1e9 + 0.5);
+  if (niv || lat_ns) {
     // bitmap-word units bound the page count (enough to size the grid)
     pages = (t.act_units[cmd + 1] - t.act_units[cmd]) * 32;
-    int blocks = (int)std::min<int64_t>(std::max<int64_t>((pages + 7) / 8, 1), 148 * 8);
+    int blocks = (int)std::min<int64_t>(std::max<int64_t>((pages + 7) / 8, 1), (int64_t)std::max(c.nsm, 1) * kConsumeCtasPerSm);
     k_consume<<<blocks, 256, 0, c.st_run>>>(t.act_pool.p + i0, niv, c.frame.p, c.arena, c.P,
-                                             (c.cfg.flags & MSG_F_VERIFY_TAGS) ? 1 : 0, c.d_run_acc);
+                                             (c.cfg.flags & MSG_F_VERIFY_TAGS) ? 1 : 0, c.d_run_acc, lat_ns);
     MSG_CHECK_LAUNCH();
     add_launches(1);
   }

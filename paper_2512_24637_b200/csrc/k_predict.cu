@@ -369,10 +369,27 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
   cudaStream_t st = c.st;
   int64_t nargs = 0, ngt = 0;
   for (int i = 0; i < ncmd; ++i) {
-    nargs = std::max<int64_t>(nargs, (int64_t)cmds[i].arg_off + cmds[i].nargs);
-    ngt = std::max<int64_t>(ngt, (int64_t)cmds[i].gt_off + cmds[i].ngt);
-    if (cmds[i].kind < 0 || cmds[i].kind > 2) throw Error(MSG_E_INVAL, "bad command kind");
+    const msg_cmd& m = cmds[i];
+    if (m.arg_off < 0 || m.nargs < 0 || m.gt_off < 0 || m.ngt < 0)
+      throw Error(MSG_E_INVAL, "negative argument or ground-truth table offset/count");
+    nargs = std::max<int64_t>(nargs, (int64_t)m.arg_off + m.nargs);
+    ngt = std::max<int64_t>(ngt, (int64_t)m.gt_off + m.ngt);
+    if (m.kind < 0 || m.kind > 2) throw Error(MSG_E_INVAL, "bad command kind");
+    if (m.kind != MSG_CMD_KERNEL && m.dev_len <= 0) throw Error(MSG_E_INVAL, "zero or negative length range");
   }
+  if (nargs && !args) throw Error(MSG_E_INVAL, "null argument table");
+  if (ngt && !gt) throw Error(MSG_E_INVAL, "null ground-truth table");
+  if (blob_len && !blob) throw Error(MSG_E_INVAL, "null struct blob");
+  // raw struct arguments are read from the blob on the device: their byte
+  // windows must lie inside it
+  for (int64_t j = 0; j < nargs; ++j) {
+    const msg_arg& a = args[j];
+    if (a.raw_len >= 0 && (a.raw_off < 0 || a.raw_off > blob_len - a.raw_len))
+      throw Error(MSG_E_INVAL, "raw struct argument outside the blob");
+  }
+  // ByteRange rejects empty and negative lengths (core.py:52-54)
+  for (int64_t j = 0; j < ngt; ++j)
+    if (gt[j].len <= 0) throw Error(MSG_E_INVAL, "zero or negative length range");
   // device copies of the inputs
   DVec<msg_cmd> d_cmds; d_cmds.exact(ncmd);
   DVec<msg_arg> d_args; d_args.exact(std::max<int64_t>(nargs, 1));

@@ -193,6 +193,8 @@ int msg_add_task(msg_ctx* ctx, int32_t task, const msg_range* allocs, int32_t na
     Ctx& c = ctx->c;
     if (!c.D && !c.span_first.size()) throw Error(MSG_E_INVAL, "set the domain first");
     if (task < 0) throw Error(MSG_E_INVAL, "negative task id");
+    if (nallocs < 0) throw Error(MSG_E_INVAL, "negative count");
+    if (nallocs > 0 && !allocs) throw Error(MSG_E_INVAL, "null allocation table");
     if ((int32_t)c.tasks.size() <= task) c.tasks.resize(task + 1, nullptr);
     if (c.tasks[task]) throw Error(MSG_E_INVAL, "task registered twice");
     auto* t = new TaskTab();
@@ -378,8 +380,8 @@ int msg_sync(msg_ctx* ctx) {
   });
 }
 
-int msg_run_command(msg_ctx* ctx, int32_t task, int32_t cmd, int64_t need_pages) {
-  return guard(ctx, [&] { run_command(ctx->c, task, cmd, need_pages); });
+int msg_run_command(msg_ctx* ctx, int32_t task, int32_t cmd, int64_t need_pages, double latency_s) {
+  return guard(ctx, [&] { run_command(ctx->c, task, cmd, need_pages, latency_s); });
 }
 
 int msg_get_stats(msg_ctx* ctx, msg_stats* out) {
@@ -468,9 +470,8 @@ int msg_verify_residency(msg_ctx* ctx, int64_t* bad_pages) {
 int msg_flush_l2(msg_ctx* ctx) {
   return guard(ctx, [&] {
     Ctx& c = ctx->c;
-    static DVec<int4> junk;
-    if (!junk.p) junk.exact((256ll << 20) / 16);
-    k_flush<<<1184, 256, 0, c.st>>>(junk.p, (int64_t)junk.n);
+    if (!c.flush_buf.p) c.flush_buf.exact((256ll << 20) / 16);
+    k_flush<<<1184, 256, 0, c.st>>>(c.flush_buf.p, (int64_t)c.flush_buf.n);
     MSG_CHECK_LAUNCH();
     add_launches(1);
     MSG_CUDA(cudaStreamSynchronize(c.st));

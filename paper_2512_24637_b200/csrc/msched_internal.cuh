@@ -182,6 +182,7 @@ struct Ctx {
   cudaStream_t st = nullptr;          // planner stream
   cudaStream_t st_d2h = nullptr, st_h2d = nullptr;
   cudaStream_t st_run = nullptr;      // executed commands (msg_run_command)
+  DVec<int4> flush_buf;               // msg_flush_l2's 256 MiB write target (this ctx's device)
   unsigned long long* d_progress = nullptr;   // populate pages landed so far (written by the H2D stream)
   unsigned long long* d_run_acc = nullptr;    // [0] pages read [1] bad tags [2] non-resident
   int64_t installed_total = 0;        // populate pages whose copies have been issued
@@ -292,7 +293,7 @@ void scan_flags(Ctx& c, const int32_t* in, int64_t n, int64_t* out);   // exclus
 void migration_init(Ctx& c);
 void migrate_batch(Ctx& c, int64_t n_d2h, int64_t n_h2d, int64_t free_before, bool copy_h2d);
 void verify_tags(Ctx& c, int64_t* bad);
-void run_command(Ctx& c, int32_t task, int32_t cmd, int64_t need_pages);
+void run_command(Ctx& c, int32_t task, int32_t cmd, int64_t need_pages, double latency_s);
 void run_wait_before_copies(Ctx& c);
 
 int64_t kernel_launches();

@@ -313,6 +313,10 @@ class Simulator:
         reupload=False it also keeps the predicted page sets (the trace stays
         resident in HBM), with reupload=True the task tables are rebuilt from
         the host Task objects (encode, H2D, K1 prediction)."""
+        # a feeder appends commands while the replay runs: the device tables
+        # then hold the previous replay's appended commands, so they are
+        # rebuilt from the source tasks
+        reupload = reupload or self.feeder is not None
         self._host_state()
         if self.ctx is not None:
             self.ctx.reset(keep_tasks=not reupload)
@@ -521,7 +525,7 @@ class Simulator:
             offset += self._touch(task, selfpop[cur], cur, timeline, state, budget - elapsed, um)
             if self.execute:
                 gate = state["gate"] if state else None
-                self.ctx.run_command(self._idx[task.id], cur, gate.get(cur, 0) if gate else 0)
+                self.ctx.run_command(self._idx[task.id], cur, gate.get(cur, 0) if gate else 0, lat[cur])
             offset += lat[cur]
             elapsed += lat[cur]
             task.cursor = cur + 1

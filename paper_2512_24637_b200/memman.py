@@ -175,12 +175,25 @@ class MigrationPlan:
 
 def plan_migration(evlist: EvictionList, next_ws_runs: Sequence[Run], capacity_pages: int) -> MigrationPlan:
     """memman.py:269-302 on the device (k_demand_* kernels + list head)."""
-    pop, ev, trunc = evlist.ctx.list_plan([(a, b) for a, b in next_ws_runs], capacity_pages)
-    return MigrationPlan(_runs_of(ev), _split_runs(pop), trunc)
+    runs = [(a, b) for a, b in next_ws_runs]
+    pop, ev, trunc = evlist.ctx.list_plan(runs, capacity_pages)
+    return MigrationPlan(_runs_of(ev), _split_runs(pop, runs), trunc)
 
 
-def _split_runs(pages) -> list:
-    return _runs_of(pages)
+def _split_runs(pages, runs) -> list:
+    """Populate pages (first-access order) -> the reference's populate_runs:
+    the missing pieces of each requested run separately (memman.py:283-290),
+    so pieces of two adjacent requested runs stay two runs."""
+    out: list = []
+    i, n = 0, len(pages)
+    for a, b in runs:
+        j = i
+        while j < n and a <= int(pages[j]) < b:
+            j += 1
+        out.extend(_runs_of(pages[i:j]))
+        i = j
+    out.extend(_runs_of(pages[i:]))   # nothing is left unless runs overlap
+    return out
 
 
 def apply_plan(evlist: EvictionList, plan: MigrationPlan):

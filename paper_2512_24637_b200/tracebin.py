@@ -139,6 +139,41 @@ def save_trace_bin(tasks: Sequence[Task], path: str):
             pos = o + len(b)
 
 
+def _validate_columns(cols: "CommandColumns", where: str):
+    """The tables go to msg_add_commands as they are: every offset, count,
+    raw-struct window, range length and kernel index must lie inside its
+    array, and the per-command runs must tile the argument and ground-truth
+    arrays in order (encode_columns slices them by the first and last)."""
+    cm, n = cols.cmds, len(cols.cmds)
+    if len(cols.lat) != n:
+        raise TraceBinError(f"{where}: {len(cols.lat)} latencies for {n} commands")
+    if n:
+        kind = cm["kind"]
+        if np.any((kind < _abi.CMD_KERNEL) | (kind > _abi.CMD_D2H)):
+            raise TraceBinError(f"{where}: bad command kind")
+        for off, cnt, arr, what in (("arg_off", "nargs", cols.args, "argument"),
+                                    ("gt_off", "ngt", cols.gts, "ground-truth")):
+            o, c = cm[off].astype(np.int64), cm[cnt].astype(np.int64)
+            if np.any(o < 0) or np.any(c < 0):
+                raise TraceBinError(f"{where}: negative {what} offset or count")
+            if o[0] != 0 or np.any(o[1:] != o[:-1] + c[:-1]) or o[-1] + c[-1] != len(arr):
+                raise TraceBinError(f"{where}: {what} runs do not tile the {what} array")
+        k = cm["kernel"]
+        if np.any((k < -1) | (k >= len(cols.names))):
+            raise TraceBinError(f"{where}: kernel index outside the name table")
+        mem = kind != _abi.CMD_KERNEL
+        if np.any(cm["dev_len"][mem] <= 0) or np.any(cm["nargs"][mem] != 3):
+            raise TraceBinError(f"{where}: memcpy without a positive extent and 3 arguments")
+    a = cols.args
+    raw = a["raw_len"] >= 0
+    if np.any((a["raw_off"][raw] < 0) | (a["raw_off"][raw] + a["raw_len"][raw] > len(cols.blob))):
+        raise TraceBinError(f"{where}: raw struct argument outside the blob")
+    if np.any(~raw & (a["width"] != 32) & (a["width"] != 64)):
+        raise TraceBinError(f"{where}: argument width must be 32 or 64")
+    if len(cols.gts) and np.any(cols.gts["len"] <= 0):
+        raise TraceBinError(f"{where}: zero or negative length range")
+
+
 def load_trace_bin(path: str) -> list:
     """Read an MSIM-TRACE-BIN v1 file into ColumnarTasks (zero-copy views)."""
     with open(path, "rb") as f:
@@ -169,6 +204,7 @@ def load_trace_bin(path: str) -> list:
                               view(h["lat"], np.float64), list(h["names"]))
         if np.any(cols.lat <= 0):
             raise TraceBinError(f"{path}: task {h['id']!r} has non-positive latencies")
+        _validate_columns(cols, f"{path}: task {h['id']!r}")
         allocs = [Allocation(a, int(b), int(s), h["id"]) for a, b, s in h["allocations"]]
         out.append(ColumnarTask(id=h["id"], allocations=allocs, commands=cols, priority=int(h["priority"]),
                                 arrival_s=float(h["arrival_s"])))

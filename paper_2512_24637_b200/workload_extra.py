@@ -162,3 +162,39 @@ def config3_mixed(hbm_bytes: int = 96 << 20, ratio: float = 2.0, page_size: int 
 
     hw = dataclasses.replace(hw, page_size_bytes=pg, dram_capacity_bytes=max(256 * GIB, 4 * hbm_bytes))
     return tasks, hw, Policy("rr", timeslice_s)
+
+
+def gen_scatter(npages: int, k: int, ncmds: int, *, task_id: str, base_addr: int, page_size: int = 4096,
+                seed: int = 0, latency_s: float = 50e-6) -> Task:
+    """One allocation of `npages` pages; every command touches `k` distinct
+    pages drawn with `random.Random(seed)` (SURVEY.md Appendix B's fragmented
+    probe: scattered single pages, one run per page in the eviction list)."""
+    rng = random.Random(seed)
+    pg = page_size
+    cmds = []
+    for _ in range(ncmds):
+        pages = rng.sample(range(npages), k)
+        cmds.append(Command(kind=CommandKind.KERNEL, latency_s=latency_s, kernel_name="scatter",
+                            launch_args=(Arg(base_addr, 64), Arg(k, 32)),
+                            ground_truth_access=tuple(ByteRange(base_addr + p * pg, pg) for p in pages)))
+    return Task(id=task_id, allocations=[Allocation(f"{task_id}.a", base_addr, npages * pg, task_id)],
+                commands=cmds)
+
+
+def fragmented_mix(n_tasks: int = 4, npages: int = 1 << 20, k: int = 16, ncmds: int = 8192,
+                   capacity_pages: int = 1 << 18, page_size: int = 4096, task_offset: int = 0,
+                   timeslice_s: float = 1e-3):
+    """The fragmented regime the reference collapses on (SURVEY.md §0 fact 4,
+    Appendix B), scaled up: `n_tasks` tasks of `npages`-page allocations,
+    `k` scattered single pages per command, against `capacity_pages` frames.
+    Defaults: 4 x 2^20 pages, 16 pages/command, 8192 commands per task
+    (524 K page touches, twice the 2^18-frame capacity), RR 1 ms, 4 KiB pages.
+    Replayed with Mode.ideal() as in the probe."""
+    import dataclasses
+
+    tasks = [gen_scatter(npages, k, ncmds, task_id=f"f{i + task_offset}", base_addr=task_base_addr(i + task_offset),
+                         page_size=page_size, seed=i + task_offset) for i in range(n_tasks)]
+    hw = dataclasses.replace(get_preset("rtx5080"), hbm_capacity_bytes=capacity_pages * page_size,
+                             page_size_bytes=page_size,
+                             dram_capacity_bytes=max(256 * GIB, 2 * n_tasks * npages * page_size))
+    return tasks, hw, Policy("rr", timeslice_s)

@@ -92,3 +92,45 @@ def test_bad_ranges_and_negative_counts_are_inval():
         assert m.completed_tasks == len(tasks)
     finally:
         sim.close()
+
+
+def test_add_commands_rejects_tables_outside_their_arrays():
+    """msg_add_commands copies and reads exactly the windows the command
+    table names: negative offsets/counts, raw-struct windows past the blob,
+    non-positive range lengths and memcpy extents are MSG_E_INVAL before any
+    byte is read, and the task stays usable."""
+    import numpy as np
+
+    from paper_2512_24637_b200.model import Arg, ByteRange, Command, CommandKind
+
+    base = 1 << 40
+    ctx = Context(4096, 64)
+    try:
+        ctx.set_domain([(base >> 12, 64)])
+        ctx.add_task(0, [(base, 64 * 4096)])
+        cmds = [Command(CommandKind.KERNEL, 1e-5, "k", (Arg(base, 64), Arg(0, 64, raw=base.to_bytes(8, "little"))),
+                        ground_truth_access=(ByteRange(base, 8192),)),
+                Command(CommandKind.MEMCPY_H2D, 1e-5, "", (Arg(0), Arg(base), Arg(4096)))]
+        good = _abi.encode_commands(cmds, {"k": 0})
+
+        def mutated(fn):
+            c, a, b, bl, g = (x.copy() if isinstance(x, np.ndarray) else x for x in good)
+            fn(c, a, b, g)
+            return c, a, b, bl, g
+
+        bad = [
+            lambda c, a, b, g: c["arg_off"].__setitem__(0, -1),
+            lambda c, a, b, g: c["ngt"].__setitem__(0, -1),
+            lambda c, a, b, g: a["raw_off"].__setitem__(1, 4),           # 8-byte window at 4 of an 8-byte blob
+            lambda c, a, b, g: a["raw_off"].__setitem__(1, -8),
+            lambda c, a, b, g: g["len"].__setitem__(0, 0),
+            lambda c, a, b, g: g["len"].__setitem__(0, -4096),
+            lambda c, a, b, g: c["dev_len"].__setitem__(1, 0),
+            lambda c, a, b, g: c["kind"].__setitem__(0, 5),
+        ]
+        for fn in bad:
+            assert code_of(ctx.add_commands, 0, mutated(fn)) == _abi.MSG_E_INVAL
+        ctx.add_commands(0, good)                # the untouched tables still go in
+        assert ctx.read_pages(0, 0, 1) == [(base >> 12, (base >> 12) + 2)]
+    finally:
+        ctx.close()

@@ -59,6 +59,37 @@ def test_evict_head_and_remove():                             # :62-75
     assert ev.pages_in_order() == [1, 3, 5] and len(ev) == 3
 
 
+def test_plan_migration_keeps_requested_run_boundaries():   # memman.py:283-290
+    # pieces of two adjacent requested runs stay two runs, as in the reference
+    plan = memman.plan_migration(memman.EvictionList(domain_pages=64), [(0, 5), (5, 10)], capacity_pages=16)
+    assert plan.populate_runs == [(0, 5), (5, 10)]
+    ev = make_list([2, 7])
+    plan = memman.plan_migration(ev, [(0, 5), (5, 10), (20, 22)], capacity_pages=9)
+    assert plan.populate_runs == [(0, 2), (3, 5), (5, 7), (8, 10), (20, 21)] and plan.truncated_pages == 1
+
+
+@settings(max_examples=60, deadline=None)
+@given(st.lists(st.integers(0, 60), unique=True, max_size=30),
+       st.lists(st.tuples(st.integers(0, 63), st.integers(1, 8)), max_size=8), st.integers(1, 40))
+def test_plan_migration_matches_oracle_runs(pages, reqs, cap):
+    runs, used = [], set()
+    for a, n in reqs:                     # disjoint first-access runs, as compute_window makes them
+        r = [p for p in range(a, min(a + n, 64)) if p not in used]
+        if r and r == list(range(r[0], r[-1] + 1)):
+            runs.append((r[0], r[-1] + 1))
+            used.update(r)
+    pages = pages[:cap]
+    ev = make_list(pages, domain=64)
+    plan = memman.plan_migration(ev, runs, capacity_pages=cap)
+    rl = port.RunList()
+    for p in pages:
+        rl.append([(p, p + 1)])
+    ref = port.make_plan(rl, runs, cap)
+    assert plan.populate_runs == ref.populate
+    assert plan.evict_runs == ref.evict
+    assert plan.truncated_pages == ref.truncated
+
+
 def test_plan_migration_known_answers():                      # :118-141
     ev = make_list([0, 1, 2])
     plan = memman.plan_migration(ev, [(0, 5)], capacity_pages=8)

@@ -109,3 +109,50 @@ def test_lazy_commands_support_the_reference_api(tmp_path):
     assert b.commands[-1] == tasks[0].commands[-1]
     assert b.commands[1:3] == tasks[0].commands[1:3]
     assert dataclasses.replace(b, cursor=2).remaining() == len(tasks[0].commands) - 2
+
+
+def _corrupt(tmp_path, mutate):
+    """Write a valid trace, load its columns, mutate them, re-save through
+    the columnar path and load again: the loader must reject it."""
+    from paper_2512_24637_b200.model import Allocation, Arg, ByteRange, Command, CommandKind
+
+    base = 1 << 40
+    raw = Task(id="raw", allocations=[Allocation("raw.a", base, 1 << 20, "raw")],
+               commands=[Command(CommandKind.KERNEL, 1e-5, f"k{i % 2}",
+                                 (Arg(base, 64), Arg(0, 64, raw=(base + 4096 * i).to_bytes(8, "little") * 2)),
+                                 ground_truth_access=(ByteRange(base + 4096 * i, 4096),)) for i in range(6)])
+    p = tmp_path / "ok.msimb"
+    tracebin.save_trace_bin(_tasks() + [raw], str(p))
+    back = tracebin.load_trace_bin(str(p))
+    # a task with raw struct args when there is one (the struct-arg tasks)
+    t = max(back, key=lambda x: (int((x.commands.args["raw_len"] >= 0).sum()), len(x.commands)))
+    c = t.commands
+    cols = tracebin.CommandColumns(c.cmds.copy(), c.args.copy(), c.blob.copy(), c.gts.copy(), c.lat.copy(),
+                                   list(c.names))
+    mutate(cols)
+    q = tmp_path / "bad.msimb"
+    bad = tracebin.ColumnarTask(id=t.id, allocations=t.allocations, commands=cols, priority=t.priority,
+                                arrival_s=t.arrival_s)
+    tracebin.save_trace_bin([bad], str(q))
+    with pytest.raises(tracebin.TraceBinError):
+        tracebin.load_trace_bin(str(q))
+
+
+def _first_raw(cols):
+    return int(np.flatnonzero(cols.args["raw_len"] >= 0)[0])
+
+
+@pytest.mark.parametrize("name,mutate", [
+    ("arg_off past the table", lambda c: c.cmds["arg_off"].__setitem__(-1, len(c.args) + 5)),
+    ("negative nargs", lambda c: c.cmds["nargs"].__setitem__(0, -1)),
+    ("gt runs overlap", lambda c: c.cmds["gt_off"].__setitem__(1, 0)),
+    ("raw window past the blob",
+     lambda c: c.args["raw_off"].__setitem__(_first_raw(c), len(c.blob))),
+    ("negative raw offset", lambda c: c.args["raw_off"].__setitem__(_first_raw(c), -8)),
+    ("empty ground-truth range", lambda c: c.gts["len"].__setitem__(0, 0)),
+    ("negative ground-truth range", lambda c: c.gts["len"].__setitem__(0, -4096)),
+    ("kernel index past the names", lambda c: c.cmds["kernel"].__setitem__(0, len(c.names))),
+    ("bad kind", lambda c: c.cmds["kind"].__setitem__(0, 7)),
+])
+def test_loader_rejects_out_of_range_tables(tmp_path, name, mutate):
+    _corrupt(tmp_path, mutate)

@@ -44,28 +44,23 @@ int main() {
     float m1, m2; cudaEventElapsedTime(&m1, a, b); cudaEventElapsedTime(&m2, a, c);
     printf("CE duplex: H2D %.1f GB/s D2H %.1f GB/s aggregate %.1f GB/s\n", gbs(B, m1), gbs(B, m2), gbs(2.0 * B, m1 > m2 ? m1 : m2));
   }
-  // batched 4 KiB and 64 KiB copies
+  // 4 KiB, 64 KiB and 2 MiB pieces, one cudaMemcpyAsync each (the migration
+  // engine's copy-engine path issues one call per contiguous segment piece)
   for (size_t piece : {4096ul, 65536ul, 2ul << 20}) {
     size_t n = B / piece;
-    std::vector<void*> dst(n), src(n); std::vector<size_t> sz(n, piece);
-    for (size_t i = 0; i < n; ++i) { dst[i] = (char*)d1 + ((i * 7919) % n) * piece; src[i] = (char*)h1 + i * piece; }
-    cudaMemcpyAttributes attr = {}; attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-    size_t idx0 = 0, fail = 0;
-    for (int rep = 0; rep < 2; ++rep) {
-      cudaEventRecord(a, s1);
-      cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), n, &attr, &idx0, 1, &fail, s1);
-      cudaEventRecord(b, s1); cudaEventSynchronize(b);
-      cudaEventElapsedTime(&ms, a, b);
-      printf("CE batch H2D piece=%zu n=%zu: %s %.1f GB/s (%.2f ms)\n", piece, n, cudaGetErrorString(e), gbs(B, ms), ms);
-    }
-    for (size_t i = 0; i < n; ++i) { std::swap(dst[i], src[i]); dst[i] = (char*)h2 + i * piece; src[i] = (char*)d1 + ((i * 7919) % n) * piece; }
-    for (int rep = 0; rep < 2; ++rep) {
-      cudaEventRecord(a, s1);
-      cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), sz.data(), n, &attr, &idx0, 1, &fail, s1);
-      cudaEventRecord(b, s1); cudaEventSynchronize(b);
-      cudaEventElapsedTime(&ms, a, b);
-      printf("CE batch D2H piece=%zu n=%zu: %s %.1f GB/s (%.2f ms)\n", piece, n, cudaGetErrorString(e), gbs(B, ms), ms);
+    for (int dir = 0; dir < 2; ++dir) {
+      for (int rep = 0; rep < 2; ++rep) {
+        cudaEventRecord(a, s1);
+        for (size_t i = 0; i < n; ++i) {
+          char* dv = (char*)d1 + ((i * 7919) % n) * piece;
+          char* hv = (char*)(dir ? h2 : h1) + i * piece;
+          if (dir == 0) CK(cudaMemcpyAsync(dv, hv, piece, cudaMemcpyHostToDevice, s1));
+          else CK(cudaMemcpyAsync(hv, dv, piece, cudaMemcpyDeviceToHost, s1));
+        }
+        cudaEventRecord(b, s1); cudaEventSynchronize(b);
+        cudaEventElapsedTime(&ms, a, b);
+        printf("CE per-piece %s piece=%zu n=%zu: %.1f GB/s (%.2f ms)\n", dir ? "D2H" : "H2D", piece, n, gbs(B, ms), ms);
+      }
     }
   }
   void *hm1, *hm2; CK(cudaHostGetDevicePointer(&hm1, h1, 0)); CK(cudaHostGetDevicePointer(&hm2, h2, 0));
