@@ -134,18 +134,9 @@ def reference_sim_factory(name, rank, page=0):
     import msim.engine as E
     from msim import core as mc
 
-    def conv_task(t):
-        allocs = [mc.Allocation(id=a.id, base_addr=a.base_addr, size_bytes=a.size_bytes, owner_task=a.owner_task)
-                  for a in t.allocations]
-        cmds = [mc.Command(kind=mc.CommandKind[c.kind.name], latency_s=c.latency_s, kernel_name=c.kernel_name,
-                           launch_args=tuple(mc.Arg(a.value, a.width, a.raw) for a in c.launch_args),
-                           grid_dims=tuple(c.grid_dims), block_dims=tuple(c.block_dims),
-                           ground_truth_access=tuple(mc.ByteRange(r.start_addr, r.length_bytes)
-                                                     for r in c.ground_truth_access))
-                for c in t.commands]
-        return mc.Task(id=t.id, allocations=allocs, commands=cmds, priority=t.priority, arrival_s=t.arrival_s)
+    from paper_2512_24637_b200.msim_plugin import to_msim_tasks
 
-    rtasks = [conv_task(t) for t in tasks]
+    rtasks = to_msim_tasks(mc, tasks)
     rhw = mc.HwConfig(**dataclasses.asdict(hw))
     from msim.scheduler import Policy as RPolicy
 

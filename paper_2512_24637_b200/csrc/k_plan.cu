@@ -1193,6 +1193,7 @@ struct McArgs {
   int32_t passes;        // digit passes (LSD, 8 bits each), all in this launch
   unsigned long long* t_first;   // globaltimer of the first CTA to start (atomicMin)
   unsigned long long* t_last;    // globaltimer of the last CTA to finish (atomicMax)
+  int32_t dbg_id;                // launch ordinal (phase-timing build)
 };
 
 // TMA bulk copy global -> shared, completion counted on an mbarrier.
@@ -1247,6 +1248,8 @@ __device__ __forceinline__ unsigned long long global_ns() {
 // the sum over CTAs of the time since that CTA's start.
 #ifdef MSG_MC_PHASE_TS
 __device__ unsigned long long g_mc_min[16], g_mc_max[16], g_mc_sum[16], g_mc_n;
+// per-CTA absolute stamps of the last 256 launches: [launch & 255][cta][stamp]
+__device__ unsigned long long g_mc_cta[256][160][8];
 __device__ __forceinline__ unsigned long long mc_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1257,6 +1260,7 @@ __device__ __forceinline__ unsigned long long mc_now() {
     if (threadIdx.x == 0) {                                                                \
       const unsigned long long t_ = mc_now();                                              \
       atomicMin(&g_mc_min[i], t_); atomicMax(&g_mc_max[i], t_); atomicAdd(&g_mc_sum[i], t_ - mc_t0); \
+      if (blockIdx.x < 160 && (i) < 8) g_mc_cta[A.dbg_id & 255][blockIdx.x][i] = t_;      \
     }                                                                                      \
   } while (0)
 #define MCTS_START const unsigned long long mc_t0 = mc_now(); MCTS(0)
@@ -1681,7 +1685,7 @@ static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes) {
   MSG_CUDA(cudaEventRecord(e0, c.st));
   McArgs A{src0 - a, c.order[c.cur].p, c.order[c.cur ^ 1].p, n, a, T, c.ms_hist.p,
            c.ms_hist.p + 256 * (int64_t)coop_grid, c.ms_tot_par, next_barrier(c), E, (int32_t)vcap, (int32_t)nch,
-           passes, tf, tl};
+           passes, tf, tl, (int32_t)(c.ms_launch_id++)};
   void* args[] = {&A};
   MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS), args,
                                        MC_SMEM, c.st));
@@ -2813,6 +2817,10 @@ extern "C" void msg_dbg_mc_ts(unsigned long long* out) {
   cudaMemcpyFromSymbol(out + 16, msg::g_mc_max, 16 * 8);
   cudaMemcpyFromSymbol(out + 32, msg::g_mc_sum, 16 * 8);
   cudaMemcpyFromSymbol(out + 48, msg::g_mc_n, 8);
+}
+extern "C" void msg_dbg_mc_cta(unsigned long long* out) {   // 256 x 160 x 8 stamps
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, msg::g_mc_cta, sizeof(msg::g_mc_cta));
 }
 extern "C" void msg_dbg_mc_reset() {
   unsigned long long lo[16], hi[16] = {0}, z[16] = {0}, zn = 0;

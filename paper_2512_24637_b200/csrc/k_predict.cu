@@ -390,14 +390,15 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
   // ByteRange rejects empty and negative lengths (core.py:52-54)
   for (int64_t j = 0; j < ngt; ++j)
     if (gt[j].len <= 0) throw Error(MSG_E_INVAL, "zero or negative length range");
-  // device copies of the inputs
-  DVec<msg_cmd> d_cmds; d_cmds.exact(ncmd);
-  DVec<msg_arg> d_args; d_args.exact(std::max<int64_t>(nargs, 1));
-  DVec<uint8_t> d_blob; d_blob.exact(std::max<int64_t>(blob_len, 1));
-  DVec<msg_range> d_gt; d_gt.exact(std::max<int64_t>(ngt, 1));
-  DVec<Rule> d_rules; d_rules.exact(std::max<size_t>(t.rules.size(), 1));
-  DVec<int32_t> d_koff; d_koff.exact(t.kern_off.size());
-  DVec<msg_range> d_allocs; d_allocs.exact(std::max<size_t>(t.allocs.size(), 1));
+  // device copies of the inputs (the context's grow-only K1 scratch)
+  PredScratch& S = c.ps;
+  auto& d_cmds = S.cmds; d_cmds.fit(ncmd);
+  auto& d_args = S.args; d_args.fit(std::max<int64_t>(nargs, 1));
+  auto& d_blob = S.blob; d_blob.fit(std::max<int64_t>(blob_len, 1));
+  auto& d_gt = S.gt; d_gt.fit(std::max<int64_t>(ngt, 1));
+  auto& d_rules = S.rules; d_rules.fit(std::max<size_t>(t.rules.size(), 1));
+  auto& d_koff = S.koff; d_koff.fit(t.kern_off.size());
+  auto& d_allocs = S.allocs; d_allocs.fit(std::max<size_t>(t.allocs.size(), 1));
   MSG_CUDA(cudaMemcpyAsync(d_cmds.p, cmds, ncmd * sizeof(msg_cmd), cudaMemcpyHostToDevice, st));
   if (nargs) MSG_CUDA(cudaMemcpyAsync(d_args.p, args, nargs * sizeof(msg_arg), cudaMemcpyHostToDevice, st));
   if (blob_len) MSG_CUDA(cudaMemcpyAsync(d_blob.p, blob, blob_len, cudaMemcpyHostToDevice, st));
@@ -410,9 +411,9 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
     MSG_CUDA(cudaMemcpyAsync(d_allocs.p, t.allocs.data(), t.allocs.size() * sizeof(msg_range),
                              cudaMemcpyHostToDevice, st));
 
-  DVec<int64_t> cnt; cnt.exact(4 * (int64_t)ncmd + 2);   // cnt_pred | cnt_act | off_pred | off_act
-  DVec<uint8_t> comp; comp.exact(ncmd);
-  DVec<int32_t> err; err.exact(2);
+  auto& cnt = S.cnt; cnt.fit(4 * (int64_t)ncmd + 2);   // cnt_pred | cnt_act | off_pred | off_act
+  auto& comp = S.comp; comp.fit(ncmd);
+  auto& err = S.err; err.fit(2);
   MSG_CUDA(cudaMemsetAsync(err.p, 0, 2 * sizeof(int32_t), st));
 
   PredParams P{};
@@ -437,15 +438,17 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
   int64_t tp = 0, ta = 0;
   for (int i = 0; i < ncmd; ++i) { off[i] = tp; tp += hc[i]; off[ncmd + i] = ta; ta += hc[ncmd + i]; }
   MSG_CUDA(cudaMemcpyAsync(cnt.p + 2 * ncmd, off.data(), 2 * ncmd * sizeof(int64_t), cudaMemcpyHostToDevice, st));
-  DVec<int64_t> rawp, rawa; rawp.exact(2 * std::max<int64_t>(tp, 1)); rawa.exact(2 * std::max<int64_t>(ta, 1));
+  auto& rawp = S.rawp; auto& rawa = S.rawa;
+  rawp.fit(2 * std::max<int64_t>(tp, 1)); rawa.fit(2 * std::max<int64_t>(ta, 1));
   P.off_pred = cnt.p + 2 * ncmd; P.off_act = cnt.p + 3 * ncmd; P.raw_pred = rawp.p; P.raw_act = rawa.p;
   k_pred_pass<<<grid, 128, 0, st>>>(P, 1);
   MSG_CHECK_LAUNCH(); add_launches(1);
 
   // normalise both sets
-  DVec<Iv> np_, na_; np_.exact(std::max<int64_t>(tp, 1)); na_.exact(std::max<int64_t>(ta, 1));
-  DVec<int64_t> nn; nn.exact(6 * (int64_t)ncmd);   // counts | units | pages, pred then act
-  DVec<int64_t> gk; gk.exact(4 * std::max(tp, ta) + 4);
+  auto& np_ = S.np; auto& na_ = S.na;
+  np_.fit(std::max<int64_t>(tp, 1)); na_.fit(std::max<int64_t>(ta, 1));
+  auto& nn = S.nn; nn.fit(6 * (int64_t)ncmd);   // counts | units | pages, pred then act
+  auto& gk = S.gk; gk.fit(4 * std::max(tp, ta) + 4);
   NormParams N{};
   N.span_first = c.d_span_first.p; N.span_n = c.d_span_n.p; N.span_dense = c.d_span_dense.p;
   N.nspans = (int32_t)c.span_first.size(); N.err = err.p; N.gkeys = gk.p;
@@ -480,7 +483,7 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
   }
   t.pred_pool.resize(std::max<int64_t>(pp, 1), st);
   t.act_pool.resize(std::max<int64_t>(pa, 1), st);
-  DVec<int64_t> ddst; ddst.exact(2 * (int64_t)ncmd);
+  auto& ddst = S.dst; ddst.fit(2 * (int64_t)ncmd);
   MSG_CUDA(cudaMemcpyAsync(ddst.p, dst.data(), 2 * ncmd * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   k_compact_iv<<<std::min(ncmd, 4096), 128, 0, st>>>(np_.p, P.off_pred, nn.p, ddst.p, t.pred_pool.p, ncmd);
   k_compact_iv<<<std::min(ncmd, 4096), 128, 0, st>>>(na_.p, P.off_act, nn.p + ncmd, ddst.p + ncmd, t.act_pool.p, ncmd);

@@ -60,6 +60,13 @@ struct DVec {
     cap = nc;
   }
   void resize(size_t want, cudaStream_t s) { reserve(want, s); n = want; }
+  // grow-only scratch: at least `want` elements, contents discarded on growth
+  // (geometric, so repeated calls stop allocating -- and cudaFree, which
+  // synchronises the device, stops being called)
+  void fit(size_t want) {
+    if (want > cap) exact(std::max<size_t>(want, 2 * cap));
+    n = want;
+  }
   void exact(size_t want) {  // allocate exactly, discarding contents
     if (p) cudaFree(p);
     p = nullptr; n = cap = 0;
@@ -161,6 +168,18 @@ struct Scratch {
   DVec<int64_t> uofs, uscr;     // per-unit offsets, scan scratch
 };
 
+// msg_add_commands' device inputs and intermediates (K1), kept across calls
+struct PredScratch {
+  DVec<msg_cmd> cmds;
+  DVec<msg_arg> args;
+  DVec<uint8_t> blob, comp;
+  DVec<msg_range> gt, allocs;
+  DVec<Rule> rules;
+  DVec<int32_t> koff, err;
+  DVec<int64_t> cnt, rawp, rawa, nn, gk, dst;
+  DVec<Iv> np, na;
+};
+
 // Device-side scalar state (one struct in device memory).
 struct DevState {
   int64_t head;         // index of the list head in the current order buffer
@@ -183,6 +202,7 @@ struct Ctx {
   cudaStream_t st_d2h = nullptr, st_h2d = nullptr;
   cudaStream_t st_run = nullptr;      // executed commands (msg_run_command)
   DVec<int4> flush_buf;               // msg_flush_l2's 256 MiB write target (this ctx's device)
+  PredScratch ps;                     // K1 scratch (predict_commands)
   unsigned long long* d_progress = nullptr;   // populate pages landed so far (written by the H2D stream)
   unsigned long long* d_run_acc = nullptr;    // [0] pages read [1] bad tags [2] non-resident
   int64_t installed_total = 0;        // populate pages whose copies have been issued
@@ -253,6 +273,7 @@ struct Ctx {
   bool win_init = false;
   int ms_grid_cap = 0, ms_coop_grid = 0, up_per_sm = -1, nsm = 0;
   uint32_t ms_epoch = 0;
+  int64_t ms_launch_id = 0;           // cooperative multisplit launches (phase-timing build)
   std::vector<int64_t> dbg[4];
   ~Ctx();
 };

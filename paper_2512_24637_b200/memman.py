@@ -45,10 +45,14 @@ class EvictionList:
         self.ctx = _abi.Context(4096, domain_pages, device=device)
         self.ctx.set_domain([(0, domain_pages)])
         self.domain_pages = domain_pages
+        # membership mirror, updated by every mutation from what the device
+        # reports (the order itself lives only on the device): `resident` is
+        # O(1) instead of a read + sort of the whole list
+        self._members = PageSet()
 
     @property
     def resident(self) -> PageSet:
-        return PageSet._raw(_runs_of(sorted(int(p) for p in self.ctx.list_read())))
+        return self._members
 
     def __len__(self) -> int:
         return self.ctx.list_len()
@@ -65,6 +69,7 @@ class EvictionList:
         runs = [(a, b) for a, b in runs if b > a]
         if runs:
             self.ctx.list_append(runs)
+            self._members = self._members | PageSet(runs)
 
     def madvise(self, pages: PageSet):
         if pages and len(self):
@@ -73,11 +78,15 @@ class EvictionList:
     def evict_head(self, n_pages: int) -> list:
         if n_pages <= 0:
             return []
-        return _runs_of(self.ctx.list_evict_head(n_pages))
+        got = _runs_of(self.ctx.list_evict_head(n_pages))
+        if got:
+            self._members = self._members - PageSet(got)
+        return got
 
     def remove(self, pages: PageSet):
         if pages and len(self):
             self.ctx.release(list(pages.runs))
+            self._members = self._members - pages
 
 
 @dataclass

@@ -1,23 +1,20 @@
-"""One replay of a configuration through the GPU path (for ncu / nsys-free profiling)."""
+"""One or more replays of a bench configuration through the GPU path (for ncu
+launch lists and captures).  python tools/prof_replay.py CFG [REPS] [--migrate]"""
 import sys
 import time
 
 sys.path.insert(0, ".")
-from paper_2512_24637_b200 import engine, scenarios  # noqa: E402
+import bench  # noqa: E402
+from paper_2512_24637_b200 import engine  # noqa: E402
 from paper_2512_24637_b200.analyzer import build_descriptors  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
 migrate = "--migrate" in sys.argv
 reps = int(sys.argv[2]) if len(sys.argv) > 2 and sys.argv[2].isdigit() else 1
-if cfg == "cfg3":
-    from paper_2512_24637_b200.workload_extra import config3_mixed
-
-    tasks, hw, pol = config3_mixed(hbm_bytes=16 << 30, ratio=2.0, page_size=4096, task_offset=0, timeslice_s=5e-4)
-else:
-    tasks, hw, pol = {"cfg2": scenarios.config2_llama8b, "cfg1": scenarios.config1_gemm,
-                      "cfg4": scenarios.config4_llama70b}[cfg]()
-descs = {t.id: build_descriptors(t) for t in tasks}
-sim = engine.Simulator(tasks, hw, pol, engine.Mode.proactive(), migrate=migrate, descriptors=descs)
+tasks, hw, pol, _ = bench.workload(cfg, 0)
+mode = bench.workload_mode(cfg)
+descs = {t.id: build_descriptors(t) for t in tasks} if mode.name == "proactive" else None
+sim = engine.Simulator(tasks, hw, pol, mode, migrate=migrate, descriptors=descs)
 for r in range(reps):
     sim.reset()
     t0 = time.perf_counter()
