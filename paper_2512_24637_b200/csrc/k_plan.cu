@@ -285,6 +285,7 @@ struct CombineParams {
   uint64_t* key; int64_t* val; int64_t* E; int32_t* T; int64_t* idx;
   // outputs: covered segments sorted by dense start
   int64_t* seg_lo; int64_t* seg_hi; int32_t* seg_cls; int64_t* nseg_out; int64_t* ncls_out;
+  uint64_t* wide;   // k_window_combine_wide's global scratch (3 x pow2(2M) words) when smem is short
 };
 
 __device__ int64_t dense_at(const CombineParams& P, int64_t a) {
@@ -305,8 +306,10 @@ __device__ __forceinline__ int tuple_cmp(const int32_t* T, int64_t i, int64_t j,
   return 0;
 }
 
-__global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P, int64_t smem_cap) {
+__global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P, int64_t smem_cap,
+                                                             const int32_t* skip) {
   __shared__ int64_t tot_runs_s;
+  if (skip && *skip) return;   // k_window_combine_wide already built the table
   int W = P.nwin;
   // gather all runs' endpoints
   if (threadIdx.x == 0) {
@@ -444,6 +447,178 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P, int
     P.seg_lo[ci] = dense_at(P, P.E[k]);
     P.seg_hi[ci] = P.seg_lo[ci] + (P.E[k + 1] - P.E[k]);
     P.seg_cls[ci] = (int32_t)P.E[nu + k];
+  }
+  if (threadIdx.x == 0) { *P.nseg_out = nc; *P.ncls_out = ndist; }
+}
+
+// Wide variant of the class table for many runs (fragmented windows: hundreds
+// of single-page runs per window).  The per-window classes fold into one
+// 128-bit mixed-radix key per elementary segment (window 0 most significant,
+// radix = max class + 1 per window), painted window by window (runs of one
+// window are disjoint, so no two threads write one segment in a pass); the
+// segments are then sorted by key in shared memory (uncovered segments carry
+// the all-ones key and sort last) and dense-ranked.  Replaces the tuple
+// comparison sort of k_window_combine whenever the radices fit 127 bits.
+typedef unsigned __int128 u128;
+
+__device__ void bitonic_u128(uint64_t* klo, uint64_t* khi, int32_t* idx, int64_t npow2) {
+  for (int64_t k = 2; k <= npow2; k <<= 1) {
+    for (int64_t j = k >> 1; j > 0; j >>= 1) {
+      for (int64_t i = threadIdx.x; i < npow2; i += blockDim.x) {
+        int64_t l = i ^ j;
+        if (l > i) {
+          bool up = (i & k) == 0;
+          bool gt = khi[i] > khi[l] || (khi[i] == khi[l] && klo[i] > klo[l]);
+          if (gt == up) {
+            uint64_t t = klo[i]; klo[i] = klo[l]; klo[l] = t;
+            t = khi[i]; khi[i] = khi[l]; khi[l] = t;
+            int32_t ti = idx[i]; idx[i] = idx[l]; idx[l] = ti;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+__device__ void bitonic_u64(uint64_t* key, int64_t npow2) {
+  for (int64_t k = 2; k <= npow2; k <<= 1) {
+    for (int64_t j = k >> 1; j > 0; j >>= 1) {
+      for (int64_t i = threadIdx.x; i < npow2; i += blockDim.x) {
+        int64_t l = i ^ j;
+        if (l > i) {
+          bool up = (i & k) == 0;
+          if ((key[i] > key[l]) == up) { uint64_t t = key[i]; key[i] = key[l]; key[l] = t; }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// *ok_out = 0 when the radices do not fit 127 bits (the caller then runs
+// k_window_combine); otherwise the outputs of k_window_combine.
+__global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P, int64_t smem_cap, int32_t* ok_out) {
+  __shared__ int64_t tot_runs_s;
+  __shared__ u128 mult_s[64];
+  __shared__ int32_t rad_s[64];
+  __shared__ int ok_s;
+  const int W = P.nwin;
+  if (threadIdx.x < 64) rad_s[threadIdx.x] = 0;
+  if (threadIdx.x == 0) {
+    int64_t t = 0;
+    for (int w = 0; w < W; ++w) t += P.nruns[w];
+    tot_runs_s = t;
+  }
+  __syncthreads();
+  const int64_t M = tot_runs_s;
+  // radix per window: max class + 1
+  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+    int64_t g = i, w = 0;
+    while (g >= P.nruns[w]) { g -= P.nruns[w]; ++w; }
+    int64_t r = P.run_base[w] + g;
+    int32_t cls = P.run_cls ? P.run_cls[r] : (int32_t)(P.nruns[w] - g);
+    atomicMax(&rad_s[w], cls);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    ok_s = W <= 64;
+    u128 m = 1;
+    const u128 lim = ((u128)1) << 127;
+    for (int w = W - 1; w >= 0 && ok_s; --w) {
+      mult_s[w] = m;
+      const u128 rad = (u128)(uint32_t)rad_s[w] + 1;
+      if (m > lim / rad) ok_s = 0;
+      else m *= rad;
+    }
+    *ok_out = ok_s;
+  }
+  __syncthreads();
+  if (!ok_s) return;
+  if (M == 0) {
+    if (threadIdx.x == 0) { *P.nseg_out = 0; *P.ncls_out = 0; }
+    return;
+  }
+  // 1. sorted unique endpoints -> E (global)
+  const int64_t m = 2 * M, mp = pow2_at_least(m);
+  uint64_t* ek = (8 * mp <= smem_cap) ? reinterpret_cast<uint64_t*>(dyn_smem) : P.key;
+  for (int64_t i = threadIdx.x; i < mp; i += blockDim.x) {
+    if (i < m) {
+      int64_t g = i >> 1, w = 0;
+      while (g >= P.nruns[w]) { g -= P.nruns[w]; ++w; }
+      int64_t r = P.run_base[w] + g;
+      ek[i] = (uint64_t)((i & 1) ? P.run_b[r] : P.run_a[r]) ^ 0x8000000000000000ull;
+    } else {
+      ek[i] = ~0ull;
+    }
+  }
+  __syncthreads();
+  bitonic_u64(ek, mp);
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x) P.val[i] = (i == 0 || ek[i] != ek[i - 1]) ? 1 : 0;
+  __syncthreads();
+  const int64_t nu = block_scan_array<int64_t>(P.val, m);
+  for (int64_t i = threadIdx.x; i < m; i += blockDim.x)
+    if (i == 0 || ek[i] != ek[i - 1]) P.E[P.val[i]] = (int64_t)(ek[i] ^ 0x8000000000000000ull);
+  __syncthreads();
+  const int64_t ns = nu - 1, sp = pow2_at_least(ns > 0 ? ns : 1);
+  // 2. per-segment 128-bit keys, painted window by window
+  uint64_t *klo, *khi;
+  int32_t* idx;
+  if (20 * sp <= smem_cap) {
+    klo = reinterpret_cast<uint64_t*>(dyn_smem); khi = klo + sp; idx = reinterpret_cast<int32_t*>(khi + sp);
+  } else {
+    klo = P.wide; khi = P.wide + mp; idx = reinterpret_cast<int32_t*>(P.wide + 2 * mp);
+  }
+  for (int64_t k = threadIdx.x; k < sp; k += blockDim.x) { klo[k] = 0; khi[k] = 0; idx[k] = (int32_t)k; }
+  __syncthreads();
+  int64_t g0 = 0;
+  for (int w = 0; w < W; ++w) {
+    const int64_t nr = P.nruns[w];
+    const u128 mw = mult_s[w];
+    for (int64_t g = threadIdx.x; g < nr; g += blockDim.x) {
+      const int64_t r = P.run_base[w] + g;
+      const int32_t cls = P.run_cls ? P.run_cls[r] : (int32_t)(nr - g);
+      const u128 add = mw * (u128)(uint32_t)cls;
+      const int64_t s0 = lower_bound_i64(P.E, nu, P.run_a[r]), s1 = lower_bound_i64(P.E, nu, P.run_b[r]);
+      for (int64_t k = s0; k < s1; ++k) {
+        u128 v = (((u128)khi[k]) << 64 | klo[k]) + add;
+        klo[k] = (uint64_t)v; khi[k] = (uint64_t)(v >> 64);
+      }
+    }
+    g0 += nr;
+    __syncthreads();
+  }
+  // uncovered segments (key 0) and padding sort last
+  for (int64_t k = threadIdx.x; k < sp; k += blockDim.x)
+    if (k >= ns || (klo[k] == 0 && khi[k] == 0)) { klo[k] = ~0ull; khi[k] = ~0ull; }
+  __syncthreads();
+  bitonic_u128(klo, khi, idx, sp);
+  // 3. dense rank of distinct covered keys; class per segment into E[nu + k]
+  int64_t* rk = P.val;
+  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+    const bool cov = !(klo[i] == ~0ull && khi[i] == ~0ull);
+    rk[i] = cov && (i == 0 || klo[i] != klo[i - 1] || khi[i] != khi[i - 1]) ? 1 : 0;
+  }
+  __syncthreads();
+  const int64_t ndist = block_scan_array<int64_t>(rk, ns);
+  for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
+    const bool cov = !(klo[i] == ~0ull && khi[i] == ~0ull);
+    const bool first = cov && (i == 0 || klo[i] != klo[i - 1] || khi[i] != khi[i - 1]);
+    P.E[nu + idx[i]] = cov ? rk[i] + (first ? 1 : 0) : 0;
+  }
+  __syncthreads();
+  // 4. covered segments in E order -> the class table
+  for (int64_t k = threadIdx.x; k < ns; k += blockDim.x) P.val[k] = P.E[nu + k] > 0 ? 1 : 0;
+  __syncthreads();
+  const int64_t nc = block_scan_array<int64_t>(P.val, ns);
+  for (int64_t k = threadIdx.x; k < ns; k += blockDim.x) {
+    const int64_t cls = P.E[nu + k];
+    if (cls > 0) {
+      const int64_t ci = P.val[k];
+      P.seg_lo[ci] = dense_at(P, P.E[k]);
+      P.seg_hi[ci] = P.seg_lo[ci] + (P.E[k + 1] - P.E[k]);
+      P.seg_cls[ci] = (int32_t)cls;
+    }
   }
   if (threadIdx.x == 0) { *P.nseg_out = nc; *P.ncls_out = ndist; }
 }
@@ -768,6 +943,7 @@ static void win_kernels_init(Ctx& c) {
   if (c.win_init) return;
   MSG_CUDA(cudaFuncSetAttribute(k_window_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
   MSG_CUDA(cudaFuncSetAttribute(k_window_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
+  MSG_CUDA(cudaFuncSetAttribute(k_window_combine_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
   MSG_CUDA(cudaFuncSetAttribute(k_windows_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwSmem)));
   c.win_init = true;
 }
@@ -1174,7 +1350,9 @@ constexpr int MC_THREADS = 1024;
 constexpr int MC_WARPS = MC_THREADS / 32;
 constexpr int MC_BLOCK = 512;                       // entries per fast block (16 per lane)
 constexpr int MC_SMEM = 224 * 1024;
-constexpr int MC_FIXED = 3 * MS_SMEM_SEGS * 4 + MC_WARPS * 256 * 4 + 256 * 8 + 16 * 256 * 4 + 80 + 16;
+constexpr int MC_FIXED = MC_WARPS * 256 * 4 + 256 * 8 + 16 * 256 * 4 + 80 + 16;
+constexpr int MC_TCAP_MIN = MS_SMEM_SEGS;   // class-table segments always kept on chip
+constexpr int MC_TCAP_MAX = 16384;          // more when the staged slice leaves room (fragmented lists)
 
 struct McArgs {
   const int32_t* src0;   // pass 0 source, 16-byte aligned: list entry i is src0[i + a]
@@ -1194,6 +1372,7 @@ struct McArgs {
   unsigned long long* t_first;   // globaltimer of the first CTA to start (atomicMin)
   unsigned long long* t_last;    // globaltimer of the last CTA to finish (atomicMax)
   int32_t dbg_id;                // launch ordinal (phase-timing build)
+  int32_t tcap;                  // class-table segments staged in shared memory (after the slice cache)
 };
 
 // TMA bulk copy global -> shared, completion counted on an mbarrier.
@@ -1219,15 +1398,18 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       " @!p bra MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
-// k-th grid-wide barrier on one monotone counter (zero at launch)
+// k-th grid-wide barrier on one monotone counter (zero at launch): the
+// arrival is a gpu-scope release add (it publishes this CTA's writes, which
+// __syncthreads ordered before it), the wait a gpu-scope acquire poll
 __device__ __forceinline__ void grid_barrier(int32_t* bar, int k) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
-    atomicAdd(bar, 1);
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(bar) : "memory");
     const int32_t target = (k + 1) * (int32_t)gridDim.x;
-    while (*reinterpret_cast<volatile int32_t*>(bar) < target) __nanosleep(64);
-    __threadfence();
+    int32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
+    } while (v < target);
   }
   __syncthreads();
 }
@@ -1273,15 +1455,16 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   MCTS_START;
   if (threadIdx.x == 0) atomicMin(A.t_first, global_ns());   // device-side launch duration (stats)
   extern __shared__ __align__(16) unsigned char mc_raw[];
-  int32_t* lo32 = reinterpret_cast<int32_t*>(mc_raw);
-  int32_t* hi32 = lo32 + MS_SMEM_SEGS;
-  int32_t* cls32 = hi32 + MS_SMEM_SEGS;
-  int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(cls32 + MS_SMEM_SEGS);
+  int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(mc_raw);
   int64_t* base = reinterpret_cast<int64_t*>(cnt + MC_WARPS);
   int32_t* red = reinterpret_cast<int32_t*>(base + 256);          // [16][256]
   int64_t* misc = reinterpret_cast<int64_t*>(red + 16 * 256);     // [0, 8): warp totals; [8]: mbarrier
   int2* info = reinterpret_cast<int2*>(misc + 10);                // chunk records (16-B aligned)
   int32_t* cache = reinterpret_cast<int32_t*>(info + ((A.nch_cap + 1) & ~1));   // 16-B aligned
+  // the class table after the slice (+ 4 entries of TMA rounding slack)
+  int32_t* lo32 = cache + A.vcap + 4;
+  int32_t* hi32 = lo32 + A.tcap;
+  int32_t* cls32 = hi32 + A.tcap;
   // the mbarrier lives for every pass: it must not share a slot with the
   // phase-2 warp totals
   uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 8);
@@ -1307,7 +1490,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     int64_t nn = *A.T.n;
     S.n = (int32_t)nn;
     S.steps = nn > 1 ? 64 - __clzll(nn - 1) : 0;
-    S.small = nn <= MS_SMEM_SEGS;
+    S.small = nn <= A.tcap;
     S.lo = A.T.lo; S.hi = A.T.hi; S.cls = A.T.cls;
     S.lo32 = lo32; S.hi32 = hi32; S.cls32 = cls32;
     if (S.small)
@@ -1367,18 +1550,20 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     for (int32_t b = b0; b < b1; ++b) {
       const int32_t boff = b * MC_BLOCK;
       const bool full = cE + boff >= pa && cE + boff + MC_BLOCK <= nA;
+      // lane reads the 16-byte words lane + 32 t: each load instruction covers
+      // 512 contiguous bytes (no shared-memory bank conflicts)
       int4 q[4];
       if (boff + MC_BLOCK <= m) {
 #pragma unroll
-        for (int t = 0; t < 4; ++t) q[t] = *reinterpret_cast<const int4*>(cache + boff + 16 * lane + 4 * t);
+        for (int t = 0; t < 4; ++t) q[t] = *reinterpret_cast<const int4*>(cache + boff + 4 * lane + 128 * t);
       } else if (cE + boff + MC_BLOCK <= nA) {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
-          q[t] = __ldcs(reinterpret_cast<const int4*>(srcA + cE + boff + 16 * lane + 4 * t));
+          q[t] = __ldcs(reinterpret_cast<const int4*>(srcA + cE + boff + 4 * lane + 128 * t));
       } else {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
-          int32_t o = boff + 16 * lane + 4 * t;
+          int32_t o = boff + 4 * lane + 128 * t;
           q[t].x = valid(o) ? fetch(o) : 0; q[t].y = valid(o + 1) ? fetch(o + 1) : 0;
           q[t].z = valid(o + 2) ? fetch(o + 2) : 0; q[t].w = valid(o + 3) ? fetch(o + 3) : 0;
         }
@@ -1387,7 +1572,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       bool ok = full;
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
-        int32_t e = v0 + 16 * lane + 4 * t;
+        int32_t e = v0 + 4 * lane + 128 * t;
         ok = ok && q[t].x == e && q[t].y == e + 1 && q[t].z == e + 2 && q[t].w == e + 3;
       }
       int d = __all_sync(0xffffffffu, ok) ? run_digit(v0, MC_BLOCK) : -1;
@@ -1658,7 +1843,13 @@ static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes) {
   int64_t E = (nA + coop_grid - 1) / coop_grid;
   E = (E + MC_BLOCK - 1) / MC_BLOCK * MC_BLOCK;
   const int64_t nch = E / MS_CHUNK;
-  int64_t vcap = ((int64_t)MC_SMEM - MC_FIXED - 8 * (nch + 1)) / 4 - 4;   // + 16-B over-read slack
+  // shared memory after the fixed part and the chunk records: the slice
+  // cache (+ 4 entries of TMA rounding slack) and the class table (12 B per
+  // segment; at least MC_TCAP_MIN, up to MC_TCAP_MAX when the slice is short)
+  const int64_t avail = (int64_t)MC_SMEM - MC_FIXED - 8 * (((nch + 1) + 1) & ~int64_t(1)) - 16;
+  int64_t tcap = (avail - 4 * (E + 4)) / 12;
+  tcap = std::max<int64_t>(MC_TCAP_MIN, std::min<int64_t>(tcap, MC_TCAP_MAX)) & ~int64_t(3);
+  int64_t vcap = (avail - 12 * tcap) / 4 - 4;
   vcap = std::min<int64_t>(vcap, E) & ~int64_t(3);
   if (vcap < 0) return false;
   if ((int64_t)c.ms_hist.n < 256 * ((int64_t)coop_grid + 2)) {
@@ -1685,7 +1876,7 @@ static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes) {
   MSG_CUDA(cudaEventRecord(e0, c.st));
   McArgs A{src0 - a, c.order[c.cur].p, c.order[c.cur ^ 1].p, n, a, T, c.ms_hist.p,
            c.ms_hist.p + 256 * (int64_t)coop_grid, c.ms_tot_par, next_barrier(c), E, (int32_t)vcap, (int32_t)nch,
-           passes, tf, tl, (int32_t)(c.ms_launch_id++)};
+           passes, tf, tl, (int32_t)(c.ms_launch_id++), (int32_t)tcap};
   void* args[] = {&A};
   MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS), args,
                                        MC_SMEM, c.st));
@@ -1913,6 +2104,22 @@ struct WinBuild {
   std::vector<int64_t> win_base;
 };
 
+// The cross-window class table for the general (non-fused) path: the
+// 128-bit-key kernel, then the tuple-comparison kernel, which exits at once
+// unless the first found the radices too wide (decided on the device; no
+// host round trip).  M_ub bounds the total run count.
+static void launch_combine(Ctx& c, CombineParams P, int64_t M_ub) {
+  const int64_t mp = pow2_at_least(2 * std::max<int64_t>(M_ub, 1));
+  c.s.wide.resize(3 * mp + 2, c.st);
+  P.wide = reinterpret_cast<uint64_t*>(c.s.wide.p);
+  int32_t* ok = reinterpret_cast<int32_t*>(c.s.wide.p + 3 * mp);
+  win_kernels_init(c);
+  k_window_combine_wide<<<1, 1024, kWinSmem, c.st>>>(P, kWinSmem, ok);
+  k_window_combine<<<1, 1024, kWinSmem, c.st>>>(P, kWinSmem, ok);
+  MSG_CHECK_LAUNCH();
+  add_launches(2);
+}
+
 static bool build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild& wb, const RangeOut* dem = nullptr) {
   std::vector<WinDesc> wd(nwin);
   int64_t off = 0;
@@ -1998,9 +2205,7 @@ static bool build_windows(Ctx& c, const msg_window* win, int32_t nwin, WinBuild&
     add_launches(1);
     return F.R.nr != nullptr;
   }
-  k_window_combine<<<1, 1024, kWinSmem, st>>>(P, kWinSmem);
-  MSG_CHECK_LAUNCH();
-  add_launches(1);
+  launch_combine(c, P, M);
   return false;
 }
 
@@ -2181,10 +2386,7 @@ void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_
   P.seg_cls = c.s.i32c.p;
   P.nseg_out = P.seg_hi + 2 * Mb;
   P.ncls_out = P.nseg_out + 1;
-  win_kernels_init(c);
-  k_window_combine<<<1, 1024, kWinSmem, st>>>(P, kWinSmem);
-  MSG_CHECK_LAUNCH();
-  add_launches(1);
+  launch_combine(c, P, Mb);
   MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, P.ncls_out, 8, cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaStreamSynchronize(st));
   SegTab T{P.seg_lo, P.seg_hi, P.seg_cls, P.nseg_out};

@@ -149,11 +149,12 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
     for (int i = t; i < P.ntags; i += UP_THREADS) __stcg(P.hist + G + (int64_t)b * P.ntags + i, tagc[i]);
   // ---- grid barrier
   __syncthreads();
-  if (t == 0) {
-    __threadfence();
-    atomicAdd(P.bar, 1);
-    while (*reinterpret_cast<volatile int32_t*>(P.bar) < G) __nanosleep(32);
-    __threadfence();
+  if (t == 0) {   // release arrival / acquire poll at gpu scope (see k_plan.cu grid_barrier)
+    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.bar) : "memory");
+    int32_t v;
+    do {
+      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(P.bar) : "memory");
+    } while (v < G);
   }
   __syncthreads();
   // ---- phase 2: offsets, totals, scalars, per-tag totals

@@ -166,6 +166,7 @@ struct Scratch {
   RangeBuf rdem, ract;          // window-0 demand runs; actual sets of a command range
   DVec<int32_t> ucnt;           // per-unit counts
   DVec<int64_t> uofs, uscr;     // per-unit offsets, scan scratch
+  DVec<int64_t> wide;           // k_window_combine_wide global scratch + its ok flag
 };
 
 // msg_add_commands' device inputs and intermediates (K1), kept across calls

@@ -79,6 +79,9 @@ def to_msim_tasks(mc, tasks) -> list:
 
 def b200_simulator_class(E):
     """E: the reference's `msim.engine` module."""
+    import importlib
+
+    MM = importlib.import_module(E.__name__.rsplit(".", 1)[0] + ".memman")   # ReorderStats, madvise_cost_s
 
     class B200Simulator(E.Simulator):
         """msim.engine.Simulator with the hot path on a B200 (see module doc).
@@ -154,7 +157,7 @@ def b200_simulator_class(E):
             for (ti, _, _), n in zip(reversed(windows), reversed(list(win_pages))):
                 tid = self.tasks[ti].id
                 adv[tid] = adv.get(tid, 0) + int(n)
-            return E.ReorderStats(pages_advised=adv)
+            return MM.ReorderStats(pages_advised=adv)
 
         def _prepare_slice(self, entry, timeline):
             windows = self._windows(timeline)
@@ -166,7 +169,7 @@ def b200_simulator_class(E):
                 return None
             stats = self._stats(windows, win_pages)
             if self.mode.name == "proactive":
-                self._charge(E.madvise_cost_s(self.hw, stats), "madvise_s")
+                self._charge(MM.madvise_cost_s(self.hw, stats), "madvise_s")
             free = int(out.free_before)
             n_pop, n_ev = int(out.populate), int(out.evict)
             if out.truncated:
@@ -249,7 +252,7 @@ def b200_simulator_class(E):
                                                st["windows"][0][2] if st["windows"] else cur + 1, is_h2d)
             if over > 0:
                 if name == "proactive":
-                    dt = E.madvise_cost_s(self.hw, self._stats(wins, win_pages))
+                    dt = MM.madvise_cost_s(self.hw, self._stats(wins, win_pages))
                     self.metrics.madvise_s += dt
                     stall += dt
                 self.metrics.evicted_capacity_pages += int(out.evicted)

@@ -28,7 +28,7 @@ def sims():
     """Reference-generated simulations: make_golden.py, make_golden_extra.py,
     make_golden_edge.py."""
     out = _load("sims.json.gz")
-    for extra in ("sims_extra.json.gz", "sims_edge.json.gz"):
+    for extra in ("sims_extra.json.gz", "sims_edge.json.gz", "sims_frag.json.gz"):
         if os.path.exists(os.path.join(HERE, extra)):
             out = out + _load(extra)
     return out

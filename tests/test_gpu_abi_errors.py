@@ -106,7 +106,7 @@ def test_add_commands_rejects_tables_outside_their_arrays():
     base = 1 << 40
     ctx = Context(4096, 64)
     try:
-        ctx.set_domain([(base >> 12, 64)])
+        ctx.set_domain([(base >> 12, (base >> 12) + 64)])
         ctx.add_task(0, [(base, 64 * 4096)])
         cmds = [Command(CommandKind.KERNEL, 1e-5, "k", (Arg(base, 64), Arg(0, 64, raw=base.to_bytes(8, "little"))),
                         ground_truth_access=(ByteRange(base, 8192),)),
