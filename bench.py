@@ -64,6 +64,7 @@ def parse(argv=None):
     ap.add_argument("--skip-cfg2", action="store_true", help="skip the config-2 sub-object (and its execute leg)")
     ap.add_argument("--skip-large", action="store_true", help="skip the config-4-size multisplit probe")
     ap.add_argument("--skip-execute", action="store_true", help="skip the executed-commands (early-start) leg")
+    ap.add_argument("--skip-frag", action="store_true", help="skip the fragmented-configuration sub-object")
     ap.add_argument("--no-numa", action="store_true", help="do not bind the rank to its GPU's NUMA node")
     return ap.parse_args(argv)
 
@@ -684,6 +685,9 @@ def main(argv=None):
             execute = execute_leg(torch, dev, local, ws, t2, h2, p2, mode2, descs2, pool_for(t2, h2), args)
     elif not args.skip_execute and migrate:
         execute = execute_leg(torch, dev, local, ws, tasks, hw, pol, mode, descs, pool_pages, args)
+    frag = None
+    if not args.skip_frag and args.config != "frag" and migrate:
+        frag = frag_leg(torch, dev, local, ws, args, pk, peak_all, pool_for)
     if rank != 0:
         if ws > 1:
             torch.distributed.destroy_process_group()
@@ -713,6 +717,7 @@ def main(argv=None):
         "migration": mig,
         "plan_only": plan_only,
         "cfg2": cfg2,
+        "frag": frag,
         "execute": execute,
         "cpu_baseline": cpu,
         "e2e": e2e,
@@ -725,6 +730,54 @@ def main(argv=None):
     if ws > 1:
         torch.distributed.destroy_process_group()
     return 0
+
+
+def frag_leg(torch, dev, local, ws, args, pk, peak_all, pool_for):
+    """The fragmented regime the reference collapses on:
+    scattered single pages, one eviction-list run per page, the migration on
+    the SM gather/scatter kernel.  Parity at full size is out of the CPU's
+    reach (the reference's run-list madvise is O(pages^2.3)); it is checked
+    here at a reduced size against the oracle port (and in tests against the
+    reference's own goldens, tests/golden/sims_frag.json.gz)."""
+    from oracle import msched_port as port
+    from paper_2512_24637_b200.workload_extra import fragmented_mix
+
+    tasks, hw, pol, desc = workload("frag", int(os.environ.get("RANK", "0")))
+    mode = workload_mode("frag")
+    lg = Leg(torch, dev, local, ws, tasks, hw, pol, mode, None, migrate=True, host_pool_pages=pool_for(tasks, hw))
+    f_times, f_m, fst, _ = lg.timed(min(args.steps, 3), 1)
+    lg.close()
+    f_ms = max_over_ranks(torch, statistics.mean(f_times), ws, dev)
+    f_pages = sum_over_ranks(torch, f_m.planned_pages, ws, dev)
+    f_link = sum_over_ranks(torch, fst["h2d_bytes"] + fst["d2h_bytes"], ws, dev)
+    out = {"description": desc, "value": f_pages / (f_ms / 1e3), "unit": UNIT, "ms_per_step": f_ms,
+           "steps": len(f_times), "switches": f_m.context_switches,
+           "roofline": multisplit_roofline(fst, load_peaks().get("hbm_gbs", 6550.0)),
+           "migration": migration_summary(fst, f_ms, pk, ws, {"bytes": f_link, "peak": peak_all}),
+           "gather_gbs": {"h2d": fst["h2d_bytes"] / (fst["h2d_busy_ms"] * 1e6) if fst["h2d_busy_ms"] else None,
+                          "d2h": fst["d2h_bytes"] / (fst["d2h_busy_ms"] * 1e6) if fst["d2h_busy_ms"] else None,
+                          "note": "k_sm_copy (one warp per 4 KiB page, 16-byte accesses over mapped pinned memory), "
+                                  "busy time by CUDA events around the gather/scatter launches"}}
+    # the CPU reference at full size, bounded
+    cpu, _ = cpu_baseline(argparse.Namespace(cpu_sample=1, cpu_budget_s=min(args.cpu_budget_s, 20.0)), "frag", 0)
+    out["cpu_baseline"] = cpu
+    # parity at the reduced size of the golden `frag_s` case
+    small = dict(npages=2048, ncmds=60, capacity_pages=1024)
+    st_, sh, sp = fragmented_mix(**small)
+    from paper_2512_24637_b200 import engine
+
+    sim = engine.Simulator(st_, sh, sp, mode, migrate=True, verify=True, device=local)
+    try:
+        mg = sim.run()
+        bad = sim.ctx.verify()
+    finally:
+        sim.close()
+    mc = port.PortSim(st_, sh, sp, mode).run()
+    keys = ("migrated_in_pages", "migrated_out_pages", "fault_pages", "total_time_s", "context_switches")
+    out["parity"] = {"metrics_equal_oracle": {k: getattr(mg, k) for k in keys} == {k: getattr(mc, k) for k in keys},
+                     "payloads_verified": bad == 0, "size": small,
+                     "note": "full size exceeds the CPU budget; the reduced size is the golden frag_s case"}
+    return out
 
 
 def execute_leg(torch, dev, local, ws, tasks, hw, pol, mode, descs, pool_pages, args):

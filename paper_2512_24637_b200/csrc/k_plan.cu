@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine(CombineParams P, int
 // the all-ones key and sort last) and dense-ranked.  Replaces the tuple
 // comparison sort of k_window_combine whenever the radices fit 127 bits.
 typedef unsigned __int128 u128;
+constexpr int64_t kWideSmem = 224 * 1024;   // + ~1.6 KB static: within the 227 KB opt-in
 
 __device__ void bitonic_u128(uint64_t* klo, uint64_t* khi, int32_t* idx, int64_t npow2) {
   for (int64_t k = 2; k <= npow2; k <<= 1) {
@@ -512,6 +513,10 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
   }
   __syncthreads();
   const int64_t M = tot_runs_s;
+  if (W > 64) {   // beyond the radix table: the tuple-comparison kernel takes it
+    if (threadIdx.x == 0) *ok_out = 0;
+    return;
+  }
   // radix per window: max class + 1
   for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
     int64_t g = i, w = 0;
@@ -539,9 +544,14 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
     if (threadIdx.x == 0) { *P.nseg_out = 0; *P.ncls_out = 0; }
     return;
   }
-  // 1. sorted unique endpoints -> E (global)
+  // 1. sorted unique endpoints -> E.  On chip when the segment sort (20 B per
+  // padded segment, <= mp) and E (8 B per endpoint) fit: the endpoint sort
+  // runs in the segment-sort region, E after it, so every search below is a
+  // shared-memory search.
   const int64_t m = 2 * M, mp = pow2_at_least(m);
-  uint64_t* ek = (8 * mp <= smem_cap) ? reinterpret_cast<uint64_t*>(dyn_smem) : P.key;
+  const bool on_chip = 20 * mp + 8 * m <= smem_cap;
+  uint64_t* ek = on_chip ? reinterpret_cast<uint64_t*>(dyn_smem) : P.key;
+  int64_t* E = on_chip ? reinterpret_cast<int64_t*>(dyn_smem + 20 * mp) : P.E;
   for (int64_t i = threadIdx.x; i < mp; i += blockDim.x) {
     if (i < m) {
       int64_t g = i >> 1, w = 0;
@@ -558,13 +568,13 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
   __syncthreads();
   const int64_t nu = block_scan_array<int64_t>(P.val, m);
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x)
-    if (i == 0 || ek[i] != ek[i - 1]) P.E[P.val[i]] = (int64_t)(ek[i] ^ 0x8000000000000000ull);
+    if (i == 0 || ek[i] != ek[i - 1]) E[P.val[i]] = (int64_t)(ek[i] ^ 0x8000000000000000ull);
   __syncthreads();
   const int64_t ns = nu - 1, sp = pow2_at_least(ns > 0 ? ns : 1);
   // 2. per-segment 128-bit keys, painted window by window
   uint64_t *klo, *khi;
   int32_t* idx;
-  if (20 * sp <= smem_cap) {
+  if (on_chip) {
     klo = reinterpret_cast<uint64_t*>(dyn_smem); khi = klo + sp; idx = reinterpret_cast<int32_t*>(khi + sp);
   } else {
     klo = P.wide; khi = P.wide + mp; idx = reinterpret_cast<int32_t*>(P.wide + 2 * mp);
@@ -579,7 +589,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       const int64_t r = P.run_base[w] + g;
       const int32_t cls = P.run_cls ? P.run_cls[r] : (int32_t)(nr - g);
       const u128 add = mw * (u128)(uint32_t)cls;
-      const int64_t s0 = lower_bound_i64(P.E, nu, P.run_a[r]), s1 = lower_bound_i64(P.E, nu, P.run_b[r]);
+      const int64_t s0 = lower_bound_i64(E, nu, P.run_a[r]), s1 = lower_bound_i64(E, nu, P.run_b[r]);
       for (int64_t k = s0; k < s1; ++k) {
         u128 v = (((u128)khi[k]) << 64 | klo[k]) + add;
         klo[k] = (uint64_t)v; khi[k] = (uint64_t)(v >> 64);
@@ -601,10 +611,14 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
   }
   __syncthreads();
   const int64_t ndist = block_scan_array<int64_t>(rk, ns);
+  // class per segment (0 = uncovered; global P.E[nu + k]): every slot first, since sorted
+  // positions below ns may hold padding entries whose index is >= ns
+  for (int64_t k = threadIdx.x; k < ns; k += blockDim.x) P.E[nu + k] = 0;
+  __syncthreads();
   for (int64_t i = threadIdx.x; i < ns; i += blockDim.x) {
     const bool cov = !(klo[i] == ~0ull && khi[i] == ~0ull);
     const bool first = cov && (i == 0 || klo[i] != klo[i - 1] || khi[i] != khi[i - 1]);
-    P.E[nu + idx[i]] = cov ? rk[i] + (first ? 1 : 0) : 0;
+    if (cov) P.E[nu + idx[i]] = rk[i] + (first ? 1 : 0);
   }
   __syncthreads();
   // 4. covered segments in E order -> the class table
@@ -615,8 +629,8 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
     const int64_t cls = P.E[nu + k];
     if (cls > 0) {
       const int64_t ci = P.val[k];
-      P.seg_lo[ci] = dense_at(P, P.E[k]);
-      P.seg_hi[ci] = P.seg_lo[ci] + (P.E[k + 1] - P.E[k]);
+      P.seg_lo[ci] = dense_at(P, E[k]);
+      P.seg_hi[ci] = P.seg_lo[ci] + (E[k + 1] - E[k]);
       P.seg_cls[ci] = (int32_t)cls;
     }
   }
@@ -943,7 +957,7 @@ static void win_kernels_init(Ctx& c) {
   if (c.win_init) return;
   MSG_CUDA(cudaFuncSetAttribute(k_window_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
   MSG_CUDA(cudaFuncSetAttribute(k_window_combine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
-  MSG_CUDA(cudaFuncSetAttribute(k_window_combine_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWinSmem));
+  MSG_CUDA(cudaFuncSetAttribute(k_window_combine_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kWideSmem));
   MSG_CUDA(cudaFuncSetAttribute(k_windows_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(FwSmem)));
   c.win_init = true;
 }
@@ -1350,7 +1364,8 @@ constexpr int MC_THREADS = 1024;
 constexpr int MC_WARPS = MC_THREADS / 32;
 constexpr int MC_BLOCK = 512;                       // entries per fast block (16 per lane)
 constexpr int MC_SMEM = 224 * 1024;
-constexpr int MC_FIXED = MC_WARPS * 256 * 4 + 256 * 8 + 16 * 256 * 4 + 80 + 16;
+constexpr int MC_PIECES = 4;                // TMA pieces of a slice, one mbarrier each
+constexpr int MC_FIXED = MC_WARPS * 256 * 4 + 256 * 8 + 16 * 256 * 4 + 8 * (8 + MC_PIECES) + 16;
 constexpr int MC_TCAP_MIN = MS_SMEM_SEGS;   // class-table segments always kept on chip
 constexpr int MC_TCAP_MAX = 16384;          // more when the staged slice leaves room (fragmented lists)
 
@@ -1458,31 +1473,41 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(mc_raw);
   int64_t* base = reinterpret_cast<int64_t*>(cnt + MC_WARPS);
   int32_t* red = reinterpret_cast<int32_t*>(base + 256);          // [16][256]
-  int64_t* misc = reinterpret_cast<int64_t*>(red + 16 * 256);     // [0, 8): warp totals; [8]: mbarrier
-  int2* info = reinterpret_cast<int2*>(misc + 10);                // chunk records (16-B aligned)
+  int64_t* misc = reinterpret_cast<int64_t*>(red + 16 * 256);     // [0, 8): warp totals; [8, 12): mbarriers
+  int2* info = reinterpret_cast<int2*>(misc + 8 + MC_PIECES);     // chunk records (16-B aligned)
   int32_t* cache = reinterpret_cast<int32_t*>(info + ((A.nch_cap + 1) & ~1));   // 16-B aligned
   // the class table after the slice (+ 4 entries of TMA rounding slack)
   int32_t* lo32 = cache + A.vcap + 4;
   int32_t* hi32 = lo32 + A.tcap;
   int32_t* cls32 = hi32 + A.tcap;
-  // the mbarrier lives for every pass: it must not share a slot with the
-  // phase-2 warp totals
+  // the mbarriers live for every pass: they must not share a slot with the
+  // phase-2 warp totals.  The staged slice arrives in MC_PIECES block-aligned
+  // pieces, one mbarrier each, so a warp starts on its blocks as soon as the
+  // piece holding them has landed instead of waiting for the whole slice.
   uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 8);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = (1u << lane) - 1u;
   const int passes = A.passes;
   const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
+  auto piece_len = [](int32_t m) { return (m + MC_PIECES * MC_BLOCK - 1) / (MC_PIECES * MC_BLOCK) * MC_BLOCK; };
+  auto issue = [&](const int32_t* src, int32_t m) {   // thread 0
+    const int32_t P4 = piece_len(m);
+    for (int k = 0; k < MC_PIECES; ++k) {
+      const int32_t lo = k * P4, hi = lo + P4 < m ? lo + P4 : m;
+      const int32_t cntk = hi > lo ? hi - lo : 0;
+      const uint32_t bytes = (uint32_t)(((int64_t)cntk * 4 + 15) & ~int64_t(15));
+      mbar_expect_tx(bar + k, bytes);
+      if (cntk > 0) tma_bulk_g2s(cache + lo, src + cE + lo, bytes, bar + k);
+    }
+  };
   if (tid == 0) {
     // pass 0's slice goes to shared memory first, so the copy overlaps the
     // class-table load below
-    mbar_init(bar, 1);
+    for (int k = 0; k < MC_PIECES; ++k) mbar_init(bar + k, 1);
     const int64_t nA0 = A.n + A.a;
     const int64_t cEnd0 = cE + A.E < nA0 ? cE + A.E : nA0;
     const int64_t len0 = cEnd0 > cE ? cEnd0 - cE : 0;
-    const int32_t m0 = (int32_t)(len0 < A.vcap ? len0 : A.vcap);
-    const uint32_t bytes = (uint32_t)(((int64_t)m0 * 4 + 15) & ~int64_t(15));
-    mbar_expect_tx(bar, bytes);
-    if (m0 > 0) tma_bulk_g2s(cache, A.src0 + cE, bytes, bar);
+    issue(A.src0, (int32_t)(len0 < A.vcap ? len0 : A.vcap));
   }
   // class table -> smem (once for all passes)
   SegView S;
@@ -1511,18 +1536,24 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     const int64_t lenA = cEnd > cE ? cEnd - cE : 0;
     const int32_t m = (int32_t)(lenA < A.vcap ? lenA : A.vcap);      // staged entries
     if (tid == 0 && pass > 0) {   // (pass 0's copy was issued at kernel start)
-      // the previous pass's generic-proxy writes (this CTA's shared reads,
-      // every CTA's global scatter, ordered by the grid barrier) before the
-      // async-proxy copy
+      // every piece of the previous pass has landed (each was waited on by a
+      // warp; this makes re-arming safe regardless), then the previous pass's
+      // generic-proxy writes (this CTA's shared reads, every CTA's global
+      // scatter, ordered by the grid barrier) before the async-proxy copy
+      for (int k = 0; k < MC_PIECES; ++k) mbar_wait(bar + k, (pass - 1) & 1);
       asm volatile("fence.proxy.async;" ::: "memory");
-      const uint32_t bytes = (uint32_t)(((int64_t)m * 4 + 15) & ~int64_t(15));
-      mbar_expect_tx(bar, bytes);
-      if (m > 0) tma_bulk_g2s(cache, srcA + cE, bytes, bar);
+      issue(srcA, m);
     }
     for (int i = lane; i < 256; i += 32) cnt[warp][i] = 0;
     __syncthreads();
-    mbar_wait(bar, pass & 1);
     if (pass == 0) MCTS(1);
+    const int32_t P4 = piece_len(m);
+    int waited = -1;   // the highest piece this warp has waited for in this pass
+    auto need = [&](int32_t boff) {   // the block at boff may read the staged slice
+      if (boff >= m) return;
+      const int pc = boff / P4;
+      if (pc > waited) { for (int k = waited + 1; k <= pc; ++k) mbar_wait(bar + k, pass & 1); waited = pc; }
+    };
     auto valid = [&](int32_t off) { int64_t ia = cE + off; return ia >= pa && ia < nA; };
     auto fetch = [&](int32_t off) -> int32_t { return off < m ? cache[off] : __ldcs(srcA + cE + off); };
     const int32_t nblk = (int32_t)((lenA + MC_BLOCK - 1) / MC_BLOCK);
@@ -1549,6 +1580,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     // ---- phase 1: classify and count
     for (int32_t b = b0; b < b1; ++b) {
       const int32_t boff = b * MC_BLOCK;
+      need(boff);
       const bool full = cE + boff >= pa && cE + boff + MC_BLOCK <= nA;
       // lane reads the 16-byte words lane + 32 t: each load instruction covers
       // 512 contiguous bytes (no shared-memory bank conflicts)
@@ -1640,11 +1672,25 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       if (tid < 256 && red[1024 + tid] > 0) dl[atomicAdd(&red[2304], 1)] = tid;
       __syncthreads();
       const int nd = red[2304], me = (int)blockIdx.x;
-      for (int k = tid; k < nd * me; k += MC_THREADS) {
-        const int j = k / me, c2 = k - j * me;
-        const int d = dl[j];
-        const int32_t v = __ldcg(A.hist + (int64_t)c2 * 256 + d);
-        if (v) atomicAdd(&red[d], v);
+      if (nd <= 16) {
+        for (int k = tid; k < nd * me; k += MC_THREADS) {
+          const int j = k / me, c2 = k - j * me;
+          const int d = dl[j];
+          const int32_t v = __ldcg(A.hist + (int64_t)c2 * 256 + d);
+          if (v) atomicAdd(&red[d], v);
+        }
+      } else {
+        // many digits (fragmented lists): whole columns, four threads per
+        // digit each summing a quarter of the earlier rows (coalesced rows,
+        // independent loads, no shared-memory atomics)
+        const int d = tid & 255, q = tid >> 8;
+        const int r0 = me * q / 4, r1 = me * (q + 1) / 4;
+        int32_t acc = 0;
+#pragma unroll 8
+        for (int c2 = r0; c2 < r1; ++c2) acc += __ldcg(A.hist + (int64_t)c2 * 256 + d);
+        red[2560 + q * 256 + d] = acc;
+        __syncthreads();
+        if (tid < 256) red[tid] = red[2560 + tid] + red[2816 + tid] + red[3072 + tid] + red[3328 + tid];
       }
     }
     __syncthreads();
@@ -2083,6 +2129,19 @@ __global__ void k_table_from_ranges(const int64_t* lo, const int64_t* len, int64
 
 static DevState& hs(Ctx& c) { return *c.hstate; }
 
+// host phase clock (MSG_HOST_PHASES=1): mark(i) adds the time since the
+// previous mark to phase i of call kind k
+struct PhaseClock {
+  Ctx& c; int k; std::chrono::steady_clock::time_point t;
+  PhaseClock(Ctx& c_, int k_) : c(c_), k(k_), t(std::chrono::steady_clock::now()) { if (c.host_phases) ++c.hp_n[k]; }
+  void mark(int i) {
+    if (!c.host_phases) return;
+    auto n = std::chrono::steady_clock::now();
+    c.hp_sum[k][i] += std::chrono::duration<double>(n - t).count();
+    t = n;
+  }
+};
+
 void pull_state(Ctx& c) {
   MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, c.st));
   MSG_CUDA(cudaStreamSynchronize(c.st));
@@ -2114,7 +2173,7 @@ static void launch_combine(Ctx& c, CombineParams P, int64_t M_ub) {
   P.wide = reinterpret_cast<uint64_t*>(c.s.wide.p);
   int32_t* ok = reinterpret_cast<int32_t*>(c.s.wide.p + 3 * mp);
   win_kernels_init(c);
-  k_window_combine_wide<<<1, 1024, kWinSmem, c.st>>>(P, kWinSmem, ok);
+  k_window_combine_wide<<<1, 1024, kWideSmem, c.st>>>(P, kWideSmem, ok);
   k_window_combine<<<1, 1024, kWinSmem, c.st>>>(P, kWinSmem, ok);
   MSG_CHECK_LAUNCH();
   add_launches(2);
@@ -2405,6 +2464,7 @@ static void touch_counts(Ctx& c, TaskTab& t, int32_t lo, int32_t hi) {
 void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_always, msg_switch_out* out,
                  int64_t* win_pages, int64_t* prefix, int64_t* touch_cnt) {
   if (nwin < 1) throw Error(MSG_E_INVAL, "need at least one window");
+  PhaseClock pc(c, 0);
   fold_events(c, c.event_bound);
   cudaStream_t st = c.st;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -2421,6 +2481,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   RangeOut dem_out = c.s.rdem.out();
   WinBuild wb;
   const bool dem_done = build_windows(c, win, nwin, wb, &dem_out);
+  pc.mark(0);   // window launch (host)
   WinPtrs wp = win_ptrs(c, nwin, wb);
   c.s.uscr.resize(512 + ncw, st);
   int64_t* pref_d = c.s.uscr.p + 512;   // per-command gating counts
@@ -2444,12 +2505,14 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   }
   // missing = demand - resident, gating counts, plan scalars, populate list
   units_plan(c, R, units_cap, ncw ? pref_d : nullptr, ncw, c.C, poplist.p, c.C, total_d);
+  pc.mark(1);   // plan launch (host)
   int64_t* hb = c.hbuf.p;
   MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(hb + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   if (ncw) MSG_CUDA(cudaMemcpyAsync(hb + nwin + 1, pref_d, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaStreamSynchronize(st));
+  pc.mark(2);   // first sync (device phase A)
   DevState S = hs(c);
   for (int w = 0; w < nwin; ++w) win_pages[w] = hb[w];
   for (int k = 0; k < ncw; ++k) prefix[k] = hb[nwin + 1 + k];
@@ -2470,6 +2533,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     // count taken on the device, measured no faster: the gap between the
     // planner events and the kernel is the cooperative launch itself)
     multisplit(c, wp.tab, passes_for(ncls));
+    pc.mark(3);   // multisplit launch (host)
     if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     out->free_before = c.C - c.len;
     int64_t* mig = mig_buf(c, ev + pop);
@@ -2482,7 +2546,9 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     evict_head_n(c, ev, mig);
     compact_if_needed(c);
     install_pages(c, poplist.p, pop, mig ? mig + ev : nullptr);
+    pc.mark(4);   // apply launches (host)
     if (mig) migrate_batch(c, ev, pop, out->free_before, true);
+    pc.mark(5);   // migration issue (host, incl. its segment sync)
   }
   // ---- MSG_F_EXECUTE: what each command of the slice physically needs landed
   const bool gates = (c.cfg.flags & MSG_F_EXECUTE) && ncw > 0;
@@ -2511,7 +2577,9 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   touch_counts(c, t0, c0, c1);
   if (ncw) MSG_CUDA(cudaMemcpyAsync(hb, c.s.tc.p, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaEventRecord(e1, st));
+  pc.mark(6);   // gates + touch scan launches (host)
   MSG_CUDA(cudaStreamSynchronize(st));
+  pc.mark(7);   // final sync (device phase B)
   out->first_missing = -1;
   out->first_missing_pages = 0;
   for (int k = 0; k < ncw; ++k) {
@@ -2530,6 +2598,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
 
 void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_window* win, int32_t nwin,
                 int32_t scan_end, bool write_tags, msg_touch_out* out, int64_t* win_pages) {
+  PhaseClock pc(c, 1);
   fold_events(c, c.event_bound);
   if (task < 0 || task >= (int32_t)c.tasks.size() || !c.tasks[task]) throw Error(MSG_E_INVAL, "unknown task");
   TaskTab& t = *c.tasks[task];
@@ -2561,7 +2630,9 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     MSG_CUDA(cudaMemcpyAsync(hb + 1, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     MSG_CUDA(cudaMemcpyAsync(hb + 1 + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   }
+  pc.mark(0);   // missing-set + window launches (host)
   if (has_iv || refresh) MSG_CUDA(cudaStreamSynchronize(st));
+  pc.mark(1);   // first sync
   const int64_t n = has_iv ? hb[0] : 0;
   const int64_t ncls = refresh ? hb[1 + nwin] : 0;
   if (refresh)
@@ -2589,9 +2660,12 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     if (evict <= 0) c.dbg[1].clear();
     dump_dense(c, c.s.miss.p, n, c.dbg[2]);
   }
+  pc.mark(2);   // multisplit + evict launches (host)
   compact_if_needed(c);
   install_pages(c, c.s.miss.p, n, mig ? mig + ev_done : nullptr);
+  pc.mark(3);   // install launch (host)
   if (mig) migrate_batch(c, ev_done, n, free_before, !write_tags);
+  pc.mark(4);
   if (n) { c.fault_task = task; c.fault_cmd = cmd; c.fault_total = c.installed_total; }
   out->resident_after = c.len;
   // rescan (cmd, scan_end)
@@ -2601,11 +2675,15 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   if (hi > lo) {
     touch_counts(c, t, lo, hi);
     MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, c.s.tc.p, (hi - lo) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    pc.mark(5);
     MSG_CUDA(cudaStreamSynchronize(st));
+    pc.mark(6);   // final sync
     for (int k = 0; k < hi - lo; ++k)
       if (c.hbuf.p[k]) { out->next_missing = lo + k; out->next_missing_pages = c.hbuf.p[k]; break; }
   } else {
+    pc.mark(5);
     MSG_CUDA(cudaStreamSynchronize(st));
+    pc.mark(6);
   }
 }
 

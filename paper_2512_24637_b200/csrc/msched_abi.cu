@@ -28,6 +28,15 @@ __global__ void k_flush(int4* p, int64_t n) {
 
 Ctx::~Ctx() {
   cudaSetDevice(device);
+  if (host_phases) {
+    const char* nm[2] = {"plan_switch", "touch"};
+    for (int k = 0; k < 2; ++k) {
+      if (!hp_n[k]) continue;
+      std::fprintf(stderr, "[msg host phases] %s n=%lld us/call:", nm[k], (long long)hp_n[k]);
+      for (int i = 0; i < 8; ++i) std::fprintf(stderr, " %.1f", hp_sum[k][i] * 1e6 / hp_n[k]);
+      std::fprintf(stderr, "\n");
+    }
+  }
   if (st) cudaStreamSynchronize(st);
   if (st_d2h) cudaStreamSynchronize(st_d2h);
   if (st_h2d) cudaStreamSynchronize(st_h2d);
@@ -166,6 +175,7 @@ int msg_create(const msg_cfg* cfg, msg_ctx** out) {
       if (v.find("onesweep") != std::string::npos) c.fallback |= 2;
       if (v.find("demand") != std::string::npos) c.fallback |= 4;
     }
+    if (const char* f = std::getenv("MSG_HOST_PHASES")) c.host_phases = f[0] == '1';
     // test hook: MSG_EVENT_BOUND=n folds the context's events past n (fold_events)
     if (const char* f = std::getenv("MSG_EVENT_BOUND")) c.event_bound = (size_t)std::max(1ll, std::atoll(f));
   });

@@ -7,6 +7,7 @@
 #include <string>
 #include <vector>
 #include <stdexcept>
+#include <chrono>
 
 #include "../../include/msched_b200.h"
 
@@ -204,6 +205,11 @@ struct Ctx {
   cudaStream_t st_run = nullptr;      // executed commands (msg_run_command)
   DVec<int4> flush_buf;               // msg_flush_l2's 256 MiB write target (this ctx's device)
   PredScratch ps;                     // K1 scratch (predict_commands)
+  // host-side phase clock of msg_plan_switch / msg_touch (MSG_HOST_PHASES=1
+  // prints the sums when the context is destroyed): [call][phase] seconds
+  bool host_phases = false;
+  double hp_sum[2][8] = {};
+  int64_t hp_n[2] = {};
   unsigned long long* d_progress = nullptr;   // populate pages landed so far (written by the H2D stream)
   unsigned long long* d_run_acc = nullptr;    // [0] pages read [1] bad tags [2] non-resident
   int64_t installed_total = 0;        // populate pages whose copies have been issued

@@ -159,3 +159,30 @@ def test_cfg4_eight_tenants_matches_oracle():
     got = dataclasses.asdict(engine.simulate(tasks, hw, pol, engine.Mode.proactive()))
     got.pop("normalized_throughput")
     assert got == want
+
+
+@pytest.mark.parametrize("name", ["frag_s", "frag_m"])
+def test_fragmented_migration_uses_the_gather_kernel(name):
+    """The fragmented regime (scattered single pages):
+    the reference's own goldens, replayed with real copies.  Segments average
+    one page, so every batch goes through the SM gather/scatter kernel
+    (k_sm_copy) rather than the copy engines; payload tags must survive."""
+    case = loader.sim_case(name)
+    want = case["runs"]["ideal"]
+    tasks = [loader.dec_task(t) for t in case["tasks"]]
+    from paper_2512_24637_b200.model import HwConfig
+    from paper_2512_24637_b200.scheduler import Policy
+
+    sim = engine.Simulator(tasks, HwConfig(**case["hw"]), Policy(**case["policy"]), engine.Mode(**want["mode"]),
+                           migrate=True, verify=True)
+    try:
+        m = sim.run()
+        assert sim.ctx.verify() == 0
+        st = sim.ctx.stats()
+    finally:
+        sim.close()
+    assert st["sm_batches"] > 0 and st["ce_batches"] == 0, st
+    assert st["h2d_bytes"] >= m.migrated_in_pages * m.page_size_bytes
+    got = dataclasses.asdict(m)
+    got.pop("normalized_throughput")
+    assert got == want["metrics"]
