@@ -1049,6 +1049,7 @@ constexpr int MS_MAX_PASSES = 4;
 
 struct SegTab {
   const int64_t* lo; const int64_t* hi; const int32_t* cls; const int64_t* n;
+  int64_t cap = 0;   // allocated entries of lo/hi/cls when known (0: unknown)
 };
 
 // Segment table staged in shared memory as 32-bit dense bounds (dense ids
@@ -1388,6 +1389,13 @@ struct McArgs {
   unsigned long long* t_last;    // globaltimer of the last CTA to finish (atomicMax)
   int32_t dbg_id;                // launch ordinal (phase-timing build)
   int32_t tcap;                  // class-table segments staged in shared memory (after the slice cache)
+  // device-decided pass count (the async switch path, no host round trip):
+  // passes = digits of *ncls_dev, 0 when *missing_dev == 0 and !reorder_always;
+  // CTA 0 publishes it to *passes_out
+  const int64_t* ncls_dev;
+  const int64_t* missing_dev;
+  int32_t reorder_always;
+  int64_t* passes_out;
 };
 
 // TMA bulk copy global -> shared, completion counted on an mbarrier.
@@ -1487,7 +1495,18 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 8);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  const int passes = A.passes;
+  int passes = A.passes;
+  if (A.ncls_dev) {
+    const bool skip = A.missing_dev && *A.missing_dev == 0 && !A.reorder_always;
+    int64_t nc = skip ? 0 : *A.ncls_dev;
+    passes = 0;
+    while (nc > 0) { ++passes; nc >>= 8; }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *A.passes_out = passes;
+    if (passes == 0) {   // uniform over the grid: no barrier is entered
+      if (threadIdx.x == 0) atomicMax(A.t_last, global_ns());
+      return;
+    }
+  }
   const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
   auto piece_len = [](int32_t m) { return (m + MC_PIECES * MC_BLOCK - 1) / (MC_PIECES * MC_BLOCK) * MC_BLOCK; };
   auto issue = [&](const int32_t* src, int32_t m) {   // thread 0
@@ -1509,16 +1528,25 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     const int64_t len0 = cEnd0 > cE ? cEnd0 - cE : 0;
     issue(A.src0, (int32_t)(len0 < A.vcap ? len0 : A.vcap));
   }
-  // class table -> smem (once for all passes)
+  // class table -> smem (once for all passes).  When the host knows the
+  // table's allocated length, every entry up to it is loaded without waiting
+  // for the segment count, so the count's load and the entries' loads are one
+  // round trip instead of two (entries past the count are never searched).
   SegView S;
   {
-    int64_t nn = *A.T.n;
+    const int64_t nn = *A.T.n;
+    if (A.T.cap > 0) {
+      const int64_t lim = A.T.cap < A.tcap ? A.T.cap : A.tcap;
+      for (int64_t i = tid; i < lim; i += MC_THREADS) {
+        lo32[i] = (int32_t)A.T.lo[i]; hi32[i] = (int32_t)A.T.hi[i]; cls32[i] = A.T.cls[i];
+      }
+    }
     S.n = (int32_t)nn;
     S.steps = nn > 1 ? 64 - __clzll(nn - 1) : 0;
     S.small = nn <= A.tcap;
     S.lo = A.T.lo; S.hi = A.T.hi; S.cls = A.T.cls;
     S.lo32 = lo32; S.hi32 = hi32; S.cls32 = cls32;
-    if (S.small)
+    if (S.small && A.T.cap <= 0)
       for (int64_t i = tid; i < nn; i += MC_THREADS) {
         lo32[i] = (int32_t)A.T.lo[i]; hi32[i] = (int32_t)A.T.hi[i]; cls32[i] = A.T.cls[i];
       }
@@ -1878,7 +1906,28 @@ static void ms_init(Ctx& c) {
 // Launch the cooperative multisplit of the current list, all digit passes in
 // one launch (a grid barrier between passes).  Returns false when the list
 // does not fit the on-chip path (the caller falls back).
-static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes) {
+// whether the cooperative multisplit can take the current list (the same
+// geometry test ms_coop_launch makes), without launching it
+static bool ms_coop_fits(Ctx& c) {
+  ms_init(c);
+  const int coop_grid = c.ms_coop_grid;
+  if (c.len == 0 || coop_grid <= 0 || (c.debug & 8) || (c.fallback & 2)) return c.len == 0;
+  const int64_t nA = c.len + 3;
+  int64_t E = (nA + coop_grid - 1) / coop_grid;
+  E = (E + MC_BLOCK - 1) / MC_BLOCK * MC_BLOCK;
+  const int64_t nch = E / MS_CHUNK;
+  const int64_t avail = (int64_t)MC_SMEM - MC_FIXED - 8 * (((nch + 1) + 1) & ~int64_t(1)) - 16;
+  return (avail - 12 * (int64_t)MC_TCAP_MIN) / 4 - 4 >= 0;
+}
+
+struct DevPasses {   // the async path: pass count decided on the device
+  const int64_t* ncls = nullptr;
+  const int64_t* missing = nullptr;
+  int reorder_always = 0;
+  int64_t* out = nullptr;
+};
+
+static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes, DevPasses dp = DevPasses{}) {
   ms_init(c);
   const int64_t n = c.len;
   const int coop_grid = c.ms_coop_grid;
@@ -1922,7 +1971,8 @@ static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes) {
   MSG_CUDA(cudaEventRecord(e0, c.st));
   McArgs A{src0 - a, c.order[c.cur].p, c.order[c.cur ^ 1].p, n, a, T, c.ms_hist.p,
            c.ms_hist.p + 256 * (int64_t)coop_grid, c.ms_tot_par, next_barrier(c), E, (int32_t)vcap, (int32_t)nch,
-           passes, tf, tl, (int32_t)(c.ms_launch_id++), (int32_t)tcap};
+           passes, tf, tl, (int32_t)(c.ms_launch_id++), (int32_t)tcap, dp.ncls, dp.missing, dp.reorder_always,
+           dp.out};
   void* args[] = {&A};
   MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS), args,
                                        MC_SMEM, c.st));
@@ -2019,8 +2069,9 @@ __device__ __forceinline__ void bits_update(uint32_t* bits, int32_t p, bool vali
   }
 }
 
-__global__ void k_evict_head(const int32_t* __restrict__ order, int64_t n, uint32_t* bits, int32_t* frame,
-                             int32_t* fifo, int64_t fifo_tail, int64_t C, int64_t* mig, Epochs ep) {
+__device__ __forceinline__ void evict_body(const int32_t* __restrict__ order, int64_t n, uint32_t* bits,
+                                           int32_t* frame, int32_t* fifo, int64_t fifo_tail, int64_t C, int64_t* mig,
+                                           Epochs ep) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int dep = -1;
   for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < n; e0 += stride) {
@@ -2046,11 +2097,15 @@ __global__ void k_evict_head(const int32_t* __restrict__ order, int64_t n, uint3
     if ((threadIdx.x & 31) == 0 && dep >= 0) atomicMax(&ep.dep[0], dep);
   }
 }
+__global__ void k_evict_head(const int32_t* __restrict__ order, int64_t n, uint32_t* bits, int32_t* frame,
+                             int32_t* fifo, int64_t fifo_tail, int64_t C, int64_t* mig, Epochs ep) {
+  evict_body(order, n, bits, frame, fifo, fifo_tail, C, mig, ep);
+}
 
-__global__ void k_install(const int32_t* __restrict__ pages, const int64_t* np_dev, int64_t np_host, uint32_t* bits,
-                          int32_t* frame, const int32_t* __restrict__ fifo, int64_t fifo_head, int64_t C,
-                          int32_t* order_tail, int64_t* mig, Epochs ep, int64_t old_free) {
-  const int64_t n = np_dev ? *np_dev : np_host;
+__device__ __forceinline__ void install_body(const int32_t* __restrict__ pages, int64_t n, uint32_t* bits,
+                                             int32_t* frame, const int32_t* __restrict__ fifo, int64_t fifo_head,
+                                             int64_t C, int32_t* order_tail, int64_t* mig, Epochs ep,
+                                             int64_t old_free) {
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int dep = -1;
   for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
@@ -2075,6 +2130,46 @@ __global__ void k_install(const int32_t* __restrict__ pages, const int64_t* np_d
     dep = __reduce_max_sync(0xffffffffu, dep);
     if ((threadIdx.x & 31) == 0 && dep >= 0) atomicMax(&ep.dep[1], dep);
   }
+}
+__global__ void k_install(const int32_t* __restrict__ pages, const int64_t* np_dev, int64_t np_host, uint32_t* bits,
+                          int32_t* frame, const int32_t* __restrict__ fifo, int64_t fifo_head, int64_t C,
+                          int32_t* order_tail, int64_t* mig, Epochs ep, int64_t old_free) {
+  install_body(pages, np_dev ? *np_dev : np_host, bits, frame, fifo, fifo_head, C, order_tail, mig, ep, old_free);
+}
+
+// The async switch path (no host round trip between plan and apply): the
+// list's position after the multisplit and the evict / populate counts are
+// read on the device.  ListSel: where the live list starts -- the other
+// buffer at 0 after an odd number of multisplit passes, this buffer at 0
+// after an even nonzero number, unchanged when no pass ran.
+struct ListSel {
+  int32_t* cur; int32_t* other; int64_t head; const int64_t* passes_dev;
+};
+__device__ __forceinline__ int32_t* sel_base(const ListSel& L) {
+  const int64_t p = L.passes_dev ? *L.passes_dev : 0;
+  return p > 0 ? ((p & 1) ? L.other : L.cur) : L.cur + L.head;
+}
+// the plan fits (populate <= free frames + evictions, engine.py:338-339);
+// otherwise nothing is applied and the host reports the error
+__device__ __forceinline__ bool plan_fits(const DevState* S, int64_t C, int64_t len0) {
+  return S->populate <= C - len0 + S->evict;
+}
+// S != nullptr: the switch plan's counts (S->evict / S->populate), applied
+// only when the plan fits; S == nullptr (touch installs): n_host evictions
+// and *np_dev installs
+__global__ void k_evict_head_dev(ListSel L, const DevState* S, int64_t n_host, int64_t len0, uint32_t* bits,
+                                 int32_t* frame, int32_t* fifo, int64_t fifo_tail, int64_t C) {
+  if (S && !plan_fits(S, C, len0)) return;
+  evict_body(sel_base(L), S ? S->evict : n_host, bits, frame, fifo, fifo_tail, C, nullptr,
+             Epochs{nullptr, nullptr, 0, nullptr});
+}
+__global__ void k_install_dev(const int32_t* __restrict__ pages, ListSel L, const DevState* S, const int64_t* np_dev,
+                              int64_t len0, uint32_t* bits, int32_t* frame, const int32_t* __restrict__ fifo,
+                              int64_t fifo_head, int64_t C) {
+  if (S && !plan_fits(S, C, len0)) return;
+  // after evicting e pages from the head the tail sits at head + e + (len0 - e)
+  install_body(pages, S ? S->populate : *np_dev, bits, frame, fifo, fifo_head, C, sel_base(L) + len0, nullptr,
+               Epochs{nullptr, nullptr, 0, nullptr}, 0);
 }
 
 // MSG_F_EXECUTE: populate position of every page installed by this switch,
@@ -2289,6 +2384,7 @@ static WinPtrs win_ptrs(Ctx& c, int32_t nwin, const WinBuild& wb) {
   int64_t* seg_hi = seg_lo + 2 * M;
   p.tab.lo = seg_lo; p.tab.hi = seg_hi; p.tab.cls = c.s.i32c.p;
   p.tab.n = seg_hi + 2 * M;
+  p.tab.cap = 2 * M;
   p.ncls = seg_hi + 2 * M + 1;
   return p;
 }
@@ -2448,7 +2544,7 @@ void list_reorder(Ctx& c, const int64_t* first, const int64_t* end, const int32_
   launch_combine(c, P, Mb);
   MSG_CUDA(cudaMemcpyAsync(c.hbuf.p, P.ncls_out, 8, cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaStreamSynchronize(st));
-  SegTab T{P.seg_lo, P.seg_hi, P.seg_cls, P.nseg_out};
+  SegTab T{P.seg_lo, P.seg_hi, P.seg_cls, P.nseg_out, 2 * Mb};
   multisplit(c, T, passes_for(c.hbuf.p[0]));
   MSG_CUDA(cudaStreamSynchronize(st));
 }
@@ -2507,6 +2603,83 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   units_plan(c, R, units_cap, ncw ? pref_d : nullptr, ncw, c.C, poplist.p, c.C, total_d);
   pc.mark(1);   // plan launch (host)
   int64_t* hb = c.hbuf.p;
+  // ---- async path: plain replays (no copies, no executed commands, no
+  // debug dumps) run phase B straight behind phase A on the device -- the
+  // multisplit decides its pass count and the apply kernels their counts
+  // from device state -- and the host syncs once, at the end
+  if (!(c.cfg.flags & (MSG_F_MIGRATE | MSG_F_VERIFY_TAGS | MSG_F_EXECUTE)) && !c.debug && ms_coop_fits(c)) {
+    compact_if_needed(c);
+    const int64_t len0 = c.len, head0 = c.head, fifo_head0 = c.fifo_head, fifo_len0 = c.fifo_len;
+    const int cur0 = c.cur;
+    int64_t* passes_d = &c.dstate->aux[2];
+    MSG_CUDA(cudaMemsetAsync(passes_d, 0, sizeof(int64_t), st));
+    if (len0 > 0)
+      ms_coop_launch(c, wp.tab, 0, DevPasses{wp.ncls, &c.dstate->missing, reorder_always ? 1 : 0, passes_d});
+    pc.mark(3);
+    const ListSel L{c.order[cur0].p, c.order[cur0 ^ 1].p, head0, passes_d};
+    if (len0 > 0) {
+      k_evict_head_dev<<<grid_for(len0, 256), 256, 0, st>>>(L, c.dstate, 0, len0, c.bits.p, c.frame.p, c.fifo.p,
+                                                            fifo_head0 + fifo_len0, c.C);
+      add_launches(1);
+    }
+    k_install_dev<<<grid_for(std::min<int64_t>(32 * units_cap, c.C), 256), 256, 0, st>>>(
+        poplist.p, L, c.dstate, nullptr, len0, c.bits.p, c.frame.p, c.fifo.p, fifo_head0, c.C);
+    MSG_CHECK_LAUNCH();
+    add_launches(1);
+    pc.mark(4);
+    touch_counts(c, t0, c0, c1);
+    MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+    MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (ncw) {
+      MSG_CUDA(cudaMemcpyAsync(hb + nwin, pref_d, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      MSG_CUDA(cudaMemcpyAsync(hb + nwin + ncw, c.s.tc.p, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    }
+    MSG_CUDA(cudaEventRecord(e1, st));
+    pc.mark(6);
+    MSG_CUDA(cudaStreamSynchronize(st));
+    pc.mark(7);
+    const DevState S = hs(c);
+    for (int w = 0; w < nwin; ++w) win_pages[w] = hb[w];
+    for (int k = 0; k < ncw; ++k) prefix[k] = hb[nwin + k];
+    out->missing = S.missing;
+    out->nwin = nwin;
+    out->early_exit = S.missing == 0 && !reorder_always;
+    c.switch_base = c.installed_total;
+    c.fault_task = -1;
+    out->populate = out->evict = out->truncated = 0;
+    const int64_t passes = S.aux[2];
+    if (passes > 0) {   // ms_coop_done
+      c.cur ^= (int)(passes & 1);
+      c.head = 0;
+      c.ms_tot_par ^= (int)(passes & 1);
+      c.stats.ms_passes += passes;
+      c.stats.ms_bytes += 8 * len0 * passes;
+    }
+    out->free_before = c.C - c.len;
+    if (!out->early_exit) {
+      const int64_t pop = S.populate, ev = S.evict;
+      out->populate = pop; out->evict = ev; out->truncated = S.truncated;
+      if (pop > c.C - len0 + ev) throw Error(MSG_E_CAPACITY, "migration plan overflowed HBM capacity");
+      c.batch_old_free = c.fifo_len;
+      c.head += ev; c.len -= ev; c.fifo_len += ev;                          // evict_head_n
+      c.fifo_head = (c.fifo_head + pop) % c.C; c.fifo_len -= pop; c.len += pop;   // install_pages
+    }
+    out->first_missing = -1;
+    out->first_missing_pages = 0;
+    for (int k = 0; k < ncw; ++k) {
+      touch_cnt[k] = hb[nwin + ncw + k];
+      if (touch_cnt[k] && out->first_missing < 0) { out->first_missing = c0 + k; out->first_missing_pages = touch_cnt[k]; }
+    }
+    c.gate_task = -1;
+    c.gate_c0 = c0;
+    c.gate_need.clear();
+    out->resident_after = c.len;
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    c.stats.plan_ms += ms;
+    cudaEventDestroy(e0); cudaEventDestroy(e1);
+    return;
+  }
   MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(hb + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -2631,6 +2804,63 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     MSG_CUDA(cudaMemcpyAsync(hb + 1 + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   }
   pc.mark(0);   // missing-set + window launches (host)
+  // ---- async path (see plan_switch): refresh, evict and install follow on
+  // the device with counts read there; one host sync at the end
+  if (!(c.cfg.flags & (MSG_F_MIGRATE | MSG_F_VERIFY_TAGS | MSG_F_EXECUTE)) && !c.debug && ms_coop_fits(c)) {
+    compact_if_needed(c);
+    const int64_t len0 = c.len, head0 = c.head, fifo_head0 = c.fifo_head, fifo_len0 = c.fifo_len;
+    const int cur0 = c.cur;
+    int64_t* passes_d = &c.dstate->aux[2];
+    MSG_CUDA(cudaMemsetAsync(passes_d, 0, sizeof(int64_t), st));
+    if (evict > 0 && refresh && len0 > 0) ms_coop_launch(c, wp.tab, 0, DevPasses{wp.ncls, nullptr, 0, passes_d});
+    const ListSel L{c.order[cur0].p, c.order[cur0 ^ 1].p, head0, passes_d};
+    const int64_t ev_done = evict > 0 ? std::min(evict, len0) : 0;
+    if (ev_done > 0) {
+      k_evict_head_dev<<<grid_for(ev_done, 256), 256, 0, st>>>(L, nullptr, ev_done, len0, c.bits.p, c.frame.p,
+                                                               c.fifo.p, fifo_head0 + fifo_len0, c.C);
+      add_launches(1);
+    }
+    if (has_iv) {
+      const int64_t nu = t.act_units[cmd + 1] - t.act_units[cmd];
+      k_install_dev<<<grid_for(std::max<int64_t>(32 * nu, 1), 256), 256, 0, st>>>(
+          c.s.miss.p, L, nullptr, c.s.uscr.p + 400, len0, c.bits.p, c.frame.p, c.fifo.p, fifo_head0, c.C);
+      add_launches(1);
+    }
+    MSG_CHECK_LAUNCH();
+    pc.mark(2);
+    const int32_t lo = cmd + 1, hi = scan_end;
+    if (hi > lo) touch_counts(c, t, lo, hi);
+    MSG_CUDA(cudaMemcpyAsync(hb + 2 + nwin, passes_d, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (hi > lo)
+      MSG_CUDA(cudaMemcpyAsync(hb + 3 + nwin, c.s.tc.p, (hi - lo) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    pc.mark(5);
+    MSG_CUDA(cudaStreamSynchronize(st));
+    pc.mark(6);
+    const int64_t n = has_iv ? hb[0] : 0;
+    if (refresh)
+      for (int w = 0; w < nwin; ++w) win_pages[w] = hb[1 + w];
+    out->missing = n;
+    out->refreshed = evict > 0 && refresh ? 1 : 0;
+    out->evicted = ev_done;
+    const int64_t passes = hb[2 + nwin];
+    if (passes > 0) {   // ms_coop_done
+      c.cur ^= (int)(passes & 1);
+      c.head = 0;
+      c.ms_tot_par ^= (int)(passes & 1);
+      c.stats.ms_passes += passes;
+      c.stats.ms_bytes += 8 * len0 * passes;
+    }
+    c.batch_old_free = c.fifo_len;
+    c.head += ev_done; c.len -= ev_done; c.fifo_len += ev_done;                  // evict_head_n
+    c.fifo_head = (c.fifo_head + n) % c.C; c.fifo_len -= n; c.len += n;          // install_pages
+    if (n) { c.fault_task = task; c.fault_cmd = cmd; c.fault_total = c.installed_total; }
+    out->resident_after = c.len;
+    out->next_missing = -1;
+    out->next_missing_pages = 0;
+    for (int k = 0; k < hi - lo; ++k)
+      if (hb[3 + nwin + k]) { out->next_missing = lo + k; out->next_missing_pages = hb[3 + nwin + k]; break; }
+    return;
+  }
   if (has_iv || refresh) MSG_CUDA(cudaStreamSynchronize(st));
   pc.mark(1);   // first sync
   const int64_t n = has_iv ? hb[0] : 0;

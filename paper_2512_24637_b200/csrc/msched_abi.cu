@@ -437,6 +437,8 @@ int msg_reset(msg_ctx* ctx, int32_t keep_tasks) {
     if (c.st_h2d) MSG_CUDA(cudaStreamSynchronize(c.st_h2d));
     if (c.st_run) MSG_CUDA(cudaStreamSynchronize(c.st_run));
     c.installed_total = 0; c.switch_base = 0; c.fault_task = -1; c.run_used = false;
+    std::memset(c.hp_sum, 0, sizeof(c.hp_sum));   // the phase clock covers the replays since the last reset
+    std::memset(c.hp_n, 0, sizeof(c.hp_n));
     if (c.d_progress) MSG_CUDA(cudaMemsetAsync(c.d_progress, 0, 8, c.st));
     if (c.d_run_acc) MSG_CUDA(cudaMemsetAsync(c.d_run_acc, 0, 4 * 8, c.st));
     c.busy_run.clear();
