@@ -499,6 +499,70 @@ __device__ void bitonic_u64(uint64_t* key, int64_t npow2) {
 
 // *ok_out = 0 when the radices do not fit 127 bits (the caller then runs
 // k_window_combine); otherwise the outputs of k_window_combine.
+// Stable block-wide LSD radix sort (8-bit digits, 1024 threads) of n
+// elements held in shared memory as SoA: NW 64-bit key words (k0 = low word,
+// k1 = high word when NW == 2) and an optional int32 payload.  Warp w owns
+// the contiguous elements [w * per, (w + 1) * per): counting and scattering
+// walk them in order, so equal digits keep their relative order.  The sort
+// ping-pongs between buffers a and b; returns true when the result is in b.
+template <int NW>
+__device__ bool block_radix_sort(uint64_t* a0, uint64_t* a1, int32_t* av, uint64_t* b0, uint64_t* b1, int32_t* bv,
+                                 int n, int nbits, int32_t (*cnt)[256], int32_t* warp_s) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  const int per = ((n + 31) / 32 + 31) & ~31;
+  const int lo = w * per, hi = lo + per < n ? lo + per : n;
+  bool in_b = false;
+  for (int sh = 0; sh < nbits; sh += 8) {
+    uint64_t* s0 = in_b ? b0 : a0; uint64_t* s1 = in_b ? b1 : a1; int32_t* sv = in_b ? bv : av;
+    uint64_t* d0 = in_b ? a0 : b0; uint64_t* d1 = in_b ? a1 : b1; int32_t* dv = in_b ? av : bv;
+    auto digit = [&](int i) -> int {
+      const uint64_t word = (NW == 2 && sh >= 64) ? s1[i] : s0[i];
+      return (int)((word >> (sh & 63)) & 255);
+    };
+    for (int j = lane; j < 256; j += 32) cnt[w][j] = 0;
+    __syncwarp();
+    for (int i0 = lo; i0 < hi; i0 += 32) {
+      const int i = i0 + lane;
+      const int d = i < hi ? digit(i) : 256;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      if (d < 256 && lane == __ffs(peers) - 1) cnt[w][d] += __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+    // exclusive offsets in (digit, warp) order: thread t owns digit t/4, warps 8(t%4) .. +8
+    {
+      const int d = threadIdx.x >> 2, wq = (threadIdx.x & 3) * 8;
+      int32_t sum = 0;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sum += cnt[wq + j][d];
+      int32_t tot;
+      int32_t run = block_excl_scan<int32_t>(sum, warp_s, &tot);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) { const int32_t c = cnt[wq + j][d]; cnt[wq + j][d] = run; run += c; }
+    }
+    __syncthreads();
+    for (int i0 = lo; i0 < hi; i0 += 32) {
+      const int i = i0 + lane;
+      const int d = i < hi ? digit(i) : 256;
+      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      const int32_t before = d < 256 ? cnt[w][d] : 0;
+      __syncwarp();
+      if (d < 256) {
+        const int o = before + __popc(peers & lt);
+        d0[o] = s0[i];
+        if (NW == 2) d1[o] = s1[i];
+        if (sv) dv[o] = sv[i];
+        if (lane == __ffs(peers) - 1) cnt[w][d] = before + __popc(peers);
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    in_b = !in_b;
+  }
+  return in_b;
+}
+
 __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P, int64_t smem_cap, int32_t* ok_out) {
   __shared__ int64_t tot_runs_s;
   __shared__ u128 mult_s[64];
@@ -543,6 +607,136 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
   if (M == 0) {
     if (threadIdx.x == 0) { *P.nseg_out = 0; *P.ncls_out = 0; }
     return;
+  }
+  const int64_t m0 = 2 * M;
+  // ---- on-chip radix path: shared memory holds R0 [0, 16m) (endpoint sort,
+  // then the per-segment keys, then one sort buffer) | E [16m, 24m) | digit
+  // counters (32 KB) | X (the covered segments, 20 B each)
+  {
+    const int64_t e_off = 16 * m0, cnt_off = 24 * m0, x_off = 24 * m0 + 32 * 256 * 4;
+    __shared__ unsigned long long mn_s, mx_s, klo_max_s, khi_max_s;
+    __shared__ int32_t rwarp_s[32];
+    __shared__ int64_t nc_s;
+    if (x_off <= smem_cap && m0 < (1ll << 30)) {
+      const int m = (int)m0;
+      uint64_t* ea = reinterpret_cast<uint64_t*>(dyn_smem);
+      uint64_t* eb = ea + m;
+      int64_t* E = reinterpret_cast<int64_t*>(dyn_smem + e_off);
+      int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(dyn_smem + cnt_off);
+      if (threadIdx.x == 0) { mn_s = ~0ull; mx_s = 0; klo_max_s = 0; khi_max_s = 0; }
+      __syncthreads();
+      for (int i = threadIdx.x; i < m; i += blockDim.x) {
+        int64_t g = i >> 1, w = 0;
+        while (g >= P.nruns[w]) { g -= P.nruns[w]; ++w; }
+        const int64_t r = P.run_base[w] + g;
+        const uint64_t v = (uint64_t)((i & 1) ? P.run_b[r] : P.run_a[r]);
+        ea[i] = v;
+        atomicMin(&mn_s, (unsigned long long)v);
+        atomicMax(&mx_s, (unsigned long long)v);
+      }
+      __syncthreads();
+      const uint64_t mn = mn_s;
+      for (int i = threadIdx.x; i < m; i += blockDim.x) ea[i] -= mn;
+      const int ebits = mx_s > mn ? 64 - __clzll((long long)(mx_s - mn)) : 0;
+      __syncthreads();
+      const bool ein_b = block_radix_sort<1>(ea, nullptr, nullptr, eb, nullptr, nullptr, m, ebits, cnt, rwarp_s);
+      const uint64_t* es = ein_b ? eb : ea;
+      int32_t* fl = reinterpret_cast<int32_t*>(ein_b ? ea : eb);   // the free buffer: unique flags -> positions
+      for (int i = threadIdx.x; i < m; i += blockDim.x) fl[i] = (i == 0 || es[i] != es[i - 1]) ? 1 : 0;
+      __syncthreads();
+      const int nu = block_scan_array<int32_t>(fl, m);
+      for (int i = threadIdx.x; i < m; i += blockDim.x)
+        if (i == 0 || es[i] != es[i - 1]) E[fl[i]] = (int64_t)(es[i] + mn);
+      __syncthreads();
+      const int ns = nu - 1;
+      // per-segment 128-bit keys in R0 (the endpoint buffers are dead)
+      uint64_t* klo = ea;
+      uint64_t* khi = ea + ns;
+      for (int k = threadIdx.x; k < ns; k += blockDim.x) { klo[k] = 0; khi[k] = 0; }
+      __syncthreads();
+      for (int w = 0; w < W; ++w) {
+        const int64_t nr = P.nruns[w];
+        const u128 mw = mult_s[w];
+        for (int64_t g = threadIdx.x; g < nr; g += blockDim.x) {
+          const int64_t r = P.run_base[w] + g;
+          const int32_t cls = P.run_cls ? P.run_cls[r] : (int32_t)(nr - g);
+          const u128 add = mw * (u128)(uint32_t)cls;
+          const int64_t s0 = lower_bound_i64(E, nu, P.run_a[r]), s1 = lower_bound_i64(E, nu, P.run_b[r]);
+          for (int64_t k = s0; k < s1; ++k) {
+            const u128 v = (((u128)khi[k]) << 64 | klo[k]) + add;
+            klo[k] = (uint64_t)v; khi[k] = (uint64_t)(v >> 64);
+          }
+        }
+        __syncthreads();
+      }
+      // covered segments -> X (key lo, key hi, segment index), in segment order
+      int nc = 0;
+      for (int base = 0; base < ns; base += blockDim.x) {
+        const int k = base + threadIdx.x;
+        nc += __syncthreads_count(k < ns && (klo[k] | khi[k]) != 0);
+      }
+      if (20ll * nc > 16 * m0 || x_off + 20ll * nc > smem_cap) {
+        // the covered set does not fit on chip: the tuple-comparison kernel takes it
+        if (threadIdx.x == 0) *ok_out = 0;
+        return;
+      }
+      uint64_t* xlo = reinterpret_cast<uint64_t*>(dyn_smem + x_off);
+      uint64_t* xhi = xlo + nc;
+      int32_t* xid = reinterpret_cast<int32_t*>(xhi + nc);
+      int64_t carry = 0;
+      for (int base = 0; base < ns; base += blockDim.x) {
+        const int k = base + threadIdx.x;
+        const bool cov = k < ns && (klo[k] | khi[k]) != 0;
+        int32_t tot;
+        const int32_t ex = block_excl_scan<int32_t>(cov ? 1 : 0, rwarp_s, &tot);
+        if (cov) {
+          const int o = (int)(carry + ex);
+          xlo[o] = klo[k]; xhi[o] = khi[k]; xid[o] = k;
+          atomicMax(&khi_max_s, (unsigned long long)khi[k]);
+          atomicMax(&klo_max_s, (unsigned long long)klo[k]);
+        }
+        carry += tot;
+      }
+      __syncthreads();
+      const int kbits = khi_max_s ? 128 - __clzll((long long)khi_max_s) : (klo_max_s ? 64 - __clzll((long long)klo_max_s) : 0);
+      // the sort's second buffer in R0 (the per-segment keys are dead)
+      uint64_t* ylo = ea;
+      uint64_t* yhi = ylo + nc;
+      int32_t* yid = reinterpret_cast<int32_t*>(yhi + nc);
+      const bool kin_b = block_radix_sort<2>(xlo, xhi, xid, ylo, yhi, yid, nc, kbits, cnt, rwarp_s);
+      const uint64_t* slo = kin_b ? ylo : xlo;
+      const uint64_t* shi = kin_b ? yhi : xhi;
+      const int32_t* sid = kin_b ? yid : xid;
+      // dense rank of the distinct keys; class per segment (0 = uncovered) in P.E[nu + k]
+      for (int k = threadIdx.x; k < ns; k += blockDim.x) P.E[nu + k] = 0;
+      int64_t rcarry = 0;
+      for (int base = 0; base < nc; base += blockDim.x) {
+        const int i = base + threadIdx.x;
+        const bool first = i < nc && (i == 0 || slo[i] != slo[i - 1] || shi[i] != shi[i - 1]);
+        int32_t tot;
+        const int32_t ex = block_excl_scan<int32_t>(first ? 1 : 0, rwarp_s, &tot);
+        if (i < nc) P.E[nu + sid[i]] = rcarry + ex + (first ? 1 : 0);
+        rcarry += tot;
+      }
+      __syncthreads();
+      // covered segments in E order -> the class table
+      int64_t oc = 0;
+      for (int base = 0; base < ns; base += blockDim.x) {
+        const int k = base + threadIdx.x;
+        const int64_t cls = k < ns ? P.E[nu + k] : 0;
+        int32_t tot;
+        const int32_t ex = block_excl_scan<int32_t>(cls > 0 ? 1 : 0, rwarp_s, &tot);
+        if (cls > 0) {
+          const int64_t ci = oc + ex;
+          P.seg_lo[ci] = dense_at(P, E[k]);
+          P.seg_hi[ci] = P.seg_lo[ci] + (E[k + 1] - E[k]);
+          P.seg_cls[ci] = (int32_t)cls;
+        }
+        oc += tot;
+      }
+      if (threadIdx.x == 0) { *P.nseg_out = nc; *P.ncls_out = rcarry; }
+      return;
+    }
   }
   // 1. sorted unique endpoints -> E.  On chip when the segment sort (20 B per
   // padded segment, <= mp) and E (8 B per endpoint) fit: the endpoint sort
