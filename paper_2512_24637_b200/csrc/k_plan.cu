@@ -887,8 +887,44 @@ struct FwSmem {
 // payload is a unique index) and threads count..n-1 must hold padding that
 // sorts last.  Strides < 32 use shuffles; wider ones exchange through shared
 // memory (every thread reaches the barriers; only t < max(n, 32) computes).
+constexpr int FW_RANK_SORT_MAX = 128;
+
+// Small inputs (n <= FW_RANK_SORT_MAX): each thread counts the keys below its
+// own (ties broken by payload, else by thread index) with independent
+// broadcast shared loads, then stores itself at that rank -- three barriers
+// instead of the network's log^2 stages of dependent exchanges.
+template <bool HI, bool PAY>
+__device__ __forceinline__ void fw_rank_sortT(uint64_t& hi, uint64_t& lo, int32_t& v, FwSmem& s, int n) {
+  const int t = threadIdx.x;
+  __syncthreads();   // callers' earlier uses of the exchange buffers are done
+  if (t < n) { if (HI) s.xk[t] = hi; s.xk2[t] = lo; if (PAY) s.xv[t] = v; }
+  __syncthreads();
+  if (t < n) {
+    int r = 0;
+#pragma unroll 8
+    for (int i = 0; i < n; ++i) {
+      const uint64_t ol = s.xk2[i];
+      bool less;
+      if (HI) {
+        const uint64_t oh = s.xk[i];
+        less = oh < hi || (oh == hi && (ol < lo || (ol == lo && (PAY ? s.xv[i] < v : i < t))));
+      } else {
+        less = ol < lo || (ol == lo && (PAY ? s.xv[i] < v : i < t));
+      }
+      r += less ? 1 : 0;
+    }
+    if (HI) s.yk[r] = hi;
+    s.yk2[r] = lo;
+    if (PAY) s.yv[r] = v;
+  }
+  __syncthreads();
+  if (t < n) { if (HI) hi = s.yk[t]; lo = s.yk2[t]; if (PAY) v = s.yv[t]; }
+  __syncthreads();   // the reads above, before callers reuse the buffers
+}
+
 template <bool HI, bool PAY>
 __device__ __forceinline__ void fw_sortT(uint64_t& hi, uint64_t& lo, int32_t& v, FwSmem& s, int n) {
+  if (n <= FW_RANK_SORT_MAX) { fw_rank_sortT<HI, PAY>(hi, lo, v, s, n); return; }
   const int t = threadIdx.x;
   const bool act = t < (n < 32 ? 32 : n);
   int buf = 0;   // wide stages alternate exchange buffers, so one barrier each suffices
@@ -1696,10 +1732,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     passes = 0;
     while (nc > 0) { ++passes; nc >>= 8; }
     if (blockIdx.x == 0 && threadIdx.x == 0) *A.passes_out = passes;
-    if (passes == 0) {   // uniform over the grid: no barrier is entered
-      if (threadIdx.x == 0) atomicMax(A.t_last, global_ns());
-      return;
-    }
+    if (passes == 0) return;   // uniform over the grid: no barrier is entered (t_last stays unset)
   }
   const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
   auto piece_len = [](int32_t m) { return (m + MC_PIECES * MC_BLOCK - 1) / (MC_PIECES * MC_BLOCK) * MC_BLOCK; };
@@ -2075,9 +2108,10 @@ void ms_harvest(Ctx& c) {
   std::vector<unsigned long long> h(2 * R);
   MSG_CUDA(cudaMemcpyAsync(h.data(), c.ms_tring.p, h.size() * 8, cudaMemcpyDeviceToHost, c.st));
   MSG_CUDA(cudaStreamSynchronize(c.st));
+  // launches that ran no pass (the async path's early exits) leave their
+  // last-CTA stamp unset and are not counted
   for (int64_t k = c.ms_tbase; k < c.ms_tslot; ++k)
-    if (h[R + k] > h[k]) c.ms_dev_ms_acc += (double)(h[R + k] - h[k]) * 1e-6;
-  c.stats.ms_dev_launches += c.ms_tslot - c.ms_tbase;
+    if (h[R + k] > h[k]) { c.ms_dev_ms_acc += (double)(h[R + k] - h[k]) * 1e-6; ++c.stats.ms_dev_launches; }
   c.ms_tbase = c.ms_tslot;
 }
 
