@@ -1685,6 +1685,9 @@ __device__ __forceinline__ unsigned long long global_ns() {
 __device__ unsigned long long g_mc_min[16], g_mc_max[16], g_mc_sum[16], g_mc_n;
 // per-CTA absolute stamps of the last 256 launches: [launch & 255][cta][stamp]
 __device__ unsigned long long g_mc_cta[256][160][8];
+// per-warp phase-1 profile of the last 64 launches: [launch & 63][cta][warp] =
+// (globaltimer ns spent in phase 1 after the warp's first piece wait) << 32 | slow chunks << 16 | blocks
+__device__ unsigned long long g_mc_warp[64][160][32];
 __device__ __forceinline__ unsigned long long mc_now() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -1725,15 +1728,6 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   uint64_t* bar = reinterpret_cast<uint64_t*>(misc + 8);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t lt = (1u << lane) - 1u;
-  int passes = A.passes;
-  if (A.ncls_dev) {
-    const bool skip = A.missing_dev && *A.missing_dev == 0 && !A.reorder_always;
-    int64_t nc = skip ? 0 : *A.ncls_dev;
-    passes = 0;
-    while (nc > 0) { ++passes; nc >>= 8; }
-    if (blockIdx.x == 0 && threadIdx.x == 0) *A.passes_out = passes;
-    if (passes == 0) return;   // uniform over the grid: no barrier is entered (t_last stays unset)
-  }
   const int64_t cE = (int64_t)blockIdx.x * A.E;                    // aligned index of the slice start
   auto piece_len = [](int32_t m) { return (m + MC_PIECES * MC_BLOCK - 1) / (MC_PIECES * MC_BLOCK) * MC_BLOCK; };
   auto issue = [&](const int32_t* src, int32_t m) {   // thread 0
@@ -1747,9 +1741,11 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     }
   };
   if (tid == 0) {
-    // pass 0's slice goes to shared memory first, so the copy overlaps the
-    // class-table load below
-    for (int k = 0; k < MC_PIECES; ++k) mbar_init(bar + k, 1);
+    // pass 0's slice goes to shared memory first -- before the pass count
+    // and the class table are read -- so the copy overlaps those loads
+    for (int k = 0; k < MC_PIECES; ++k)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar + k)), "r"(1) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     const int64_t nA0 = A.n + A.a;
     const int64_t cEnd0 = cE + A.E < nA0 ? cE + A.E : nA0;
     const int64_t len0 = cEnd0 > cE ? cEnd0 - cE : 0;
@@ -1777,6 +1773,20 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       for (int64_t i = tid; i < nn; i += MC_THREADS) {
         lo32[i] = (int32_t)A.T.lo[i]; hi32[i] = (int32_t)A.T.hi[i]; cls32[i] = A.T.cls[i];
       }
+  }
+  int passes = A.passes;
+  if (A.ncls_dev) {
+    const bool skip = A.missing_dev && *A.missing_dev == 0 && !A.reorder_always;
+    int64_t nc = skip ? 0 : *A.ncls_dev;
+    passes = 0;
+    while (nc > 0) { ++passes; nc >>= 8; }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *A.passes_out = passes;
+    if (passes == 0) {   // uniform over the grid: no barrier is entered (t_last stays unset)
+      // the staged copy is in flight into this CTA's shared memory: let it land first
+      if (tid == 0)
+        for (int k = 0; k < MC_PIECES; ++k) mbar_wait(bar + k, 0);
+      return;
+    }
   }
   __syncthreads();   // the initialised mbarrier and the class table, before any use
   int nbar = 0;
@@ -1833,9 +1843,16 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       return v + (len - 1) < c_hi ? c_d : -1;
     };
     // ---- phase 1: classify and count
+#ifdef MSG_MC_PHASE_TS
+    unsigned long long wp_t0 = 0;
+    int wp_slow = 0;
+#endif
     for (int32_t b = b0; b < b1; ++b) {
       const int32_t boff = b * MC_BLOCK;
       need(boff);
+#ifdef MSG_MC_PHASE_TS
+      if (!wp_t0) wp_t0 = mc_now();
+#endif
       const bool full = cE + boff >= pa && cE + boff + MC_BLOCK <= nA;
       // lane reads the 16-byte words lane + 32 t: each load instruction covers
       // 512 contiguous bytes (no shared-memory bank conflicts)
@@ -1892,6 +1909,9 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
           continue;
         }
         if (lane == 0) info[4 * b + j] = make_int2(0, -1);
+#ifdef MSG_MC_PHASE_TS
+        ++wp_slow;
+#endif
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           int dk = valid(coff + 32 * k + lane) ? lane_digit(x[k]) : 256;
@@ -1902,6 +1922,13 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       }
     }
     __syncthreads();
+#ifdef MSG_MC_PHASE_TS
+    if (pass == 0 && lane == 0 && blockIdx.x < 160) {
+      const unsigned long long t1 = mc_now();
+      g_mc_warp[A.dbg_id & 63][blockIdx.x][warp] = ((t1 - (wp_t0 ? wp_t0 : t1)) << 32) | ((unsigned long long)wp_slow << 16) |
+                                                   (unsigned long long)(b1 - b0);
+    }
+#endif
     if (pass == 0) MCTS(2);
     // ---- CTA histogram; exclusive warp offsets; digit totals by atomics
     int32_t* tot = A.totb + 256 * ((A.par + pass) & 1);
@@ -3555,6 +3582,10 @@ extern "C" void msg_dbg_mc_ts(unsigned long long* out) {
   cudaMemcpyFromSymbol(out + 16, msg::g_mc_max, 16 * 8);
   cudaMemcpyFromSymbol(out + 32, msg::g_mc_sum, 16 * 8);
   cudaMemcpyFromSymbol(out + 48, msg::g_mc_n, 8);
+}
+extern "C" void msg_dbg_mc_warp(unsigned long long* out) {   // 64 x 160 x 32 per-warp records
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, msg::g_mc_warp, sizeof(msg::g_mc_warp));
 }
 extern "C" void msg_dbg_mc_cta(unsigned long long* out) {   // 256 x 160 x 8 stamps
   cudaDeviceSynchronize();

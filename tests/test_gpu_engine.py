@@ -163,3 +163,30 @@ def test_single_command_over_capacity_raises(mode):        # :295-316
                                   launch_args=(Arg(base),), ground_truth_access=(ByteRange(base, size),))])
     with pytest.raises(SimulationError):
         simulate([task], HW.with_capacity(4 * PAGE), POLICY, getattr(Mode, mode)())
+
+
+@pytest.mark.parametrize("name", ["llm_2.0", "stream_ind", "frag", "cfg3_2.0", "edge_capacity_plus_one"])
+def test_async_switch_path_equals_synchronous_path(name):
+    """Plain replays run the plan's apply on the device without a host round
+    trip (the multisplit decides its pass count, the apply kernels their counts);
+    a recorder forces the synchronous path.  Both must leave the same metrics,
+    events and final eviction order."""
+    from paper_2512_24637_b200.model import HwConfig
+    from tests.golden import loader
+
+    case = loader.sim_case(name)
+    for mode_name, want in case["runs"].items():
+        if "error" in want:
+            continue
+        out = []
+        for rec in (None, []):
+            tasks = [loader.dec_task(t) for t in case["tasks"]]
+            sim = Simulator(tasks, HwConfig(**case["hw"]), Policy(**case["policy"]), Mode(**want["mode"]),
+                            record_events=True, recorder=rec)
+            try:
+                m = sim.run()
+                out.append((dataclasses.asdict(m), [(e.t, e.kind, e.task_id, e.pages) for e in sim.events],
+                            sim.eviction_order()))
+            finally:
+                sim.close()
+        assert out[0] == out[1], (name, mode_name)
