@@ -10,6 +10,8 @@
 // command, bitonic sort in shared memory), compact into the task's CSR.
 #include "msched_internal.cuh"
 
+#include <cstring>
+
 namespace msg {
 
 typedef __int128 i128;
@@ -390,26 +392,30 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
   // ByteRange rejects empty and negative lengths (core.py:52-54)
   for (int64_t j = 0; j < ngt; ++j)
     if (gt[j].len <= 0) throw Error(MSG_E_INVAL, "zero or negative length range");
-  // device copies of the inputs (the context's grow-only K1 scratch)
+  // the inputs, packed into one pinned staging buffer (16-byte aligned
+  // parts) and moved with one copy into the context's grow-only K1 scratch
   PredScratch& S = c.ps;
-  auto& d_cmds = S.cmds; d_cmds.fit(ncmd);
-  auto& d_args = S.args; d_args.fit(std::max<int64_t>(nargs, 1));
-  auto& d_blob = S.blob; d_blob.fit(std::max<int64_t>(blob_len, 1));
-  auto& d_gt = S.gt; d_gt.fit(std::max<int64_t>(ngt, 1));
-  auto& d_rules = S.rules; d_rules.fit(std::max<size_t>(t.rules.size(), 1));
-  auto& d_koff = S.koff; d_koff.fit(t.kern_off.size());
-  auto& d_allocs = S.allocs; d_allocs.fit(std::max<size_t>(t.allocs.size(), 1));
-  MSG_CUDA(cudaMemcpyAsync(d_cmds.p, cmds, ncmd * sizeof(msg_cmd), cudaMemcpyHostToDevice, st));
-  if (nargs) MSG_CUDA(cudaMemcpyAsync(d_args.p, args, nargs * sizeof(msg_arg), cudaMemcpyHostToDevice, st));
-  if (blob_len) MSG_CUDA(cudaMemcpyAsync(d_blob.p, blob, blob_len, cudaMemcpyHostToDevice, st));
-  if (ngt) MSG_CUDA(cudaMemcpyAsync(d_gt.p, gt, ngt * sizeof(msg_range), cudaMemcpyHostToDevice, st));
-  if (!t.rules.empty())
-    MSG_CUDA(cudaMemcpyAsync(d_rules.p, t.rules.data(), t.rules.size() * sizeof(Rule), cudaMemcpyHostToDevice, st));
-  MSG_CUDA(cudaMemcpyAsync(d_koff.p, t.kern_off.data(), t.kern_off.size() * sizeof(int32_t),
-                           cudaMemcpyHostToDevice, st));
-  if (!t.allocs.empty())
-    MSG_CUDA(cudaMemcpyAsync(d_allocs.p, t.allocs.data(), t.allocs.size() * sizeof(msg_range),
-                             cudaMemcpyHostToDevice, st));
+  const void* part_src[7] = {cmds, args, blob, gt, t.rules.data(), t.kern_off.data(), t.allocs.data()};
+  const size_t part_len[7] = {ncmd * sizeof(msg_cmd), (size_t)nargs * sizeof(msg_arg), (size_t)blob_len,
+                              (size_t)ngt * sizeof(msg_range), t.rules.size() * sizeof(Rule),
+                              t.kern_off.size() * sizeof(int32_t), t.allocs.size() * sizeof(msg_range)};
+  size_t part_off[7], total_in = 0;
+  for (int k = 0; k < 7; ++k) { part_off[k] = total_in; total_in += (part_len[k] + 16 + 15) & ~size_t(15); }
+  S.hin.reserve(total_in);
+  S.din.fit(total_in);
+  for (int k = 0; k < 7; ++k)
+    if (part_len[k]) std::memcpy(S.hin.p + part_off[k], part_src[k], part_len[k]);
+  MSG_CUDA(cudaMemcpyAsync(S.din.p, S.hin.p, total_in, cudaMemcpyHostToDevice, st));
+  struct { msg_cmd* p; } d_cmds{reinterpret_cast<msg_cmd*>(S.din.p + part_off[0])};
+  struct { msg_arg* p; } d_args{reinterpret_cast<msg_arg*>(S.din.p + part_off[1])};
+  struct { uint8_t* p; } d_blob{S.din.p + part_off[2]};
+  struct { msg_range* p; } d_gt{reinterpret_cast<msg_range*>(S.din.p + part_off[3])};
+  struct { Rule* p; } d_rules{reinterpret_cast<Rule*>(S.din.p + part_off[4])};
+  struct { int32_t* p; } d_koff{reinterpret_cast<int32_t*>(S.din.p + part_off[5])};
+  struct { msg_range* p; } d_allocs{reinterpret_cast<msg_range*>(S.din.p + part_off[6])};
+  // pinned host side of the small count / offset round trips
+  S.hio.reserve(8 * (16 * (size_t)ncmd + 16));
+  int64_t* hio = reinterpret_cast<int64_t*>(S.hio.p);
 
   auto& cnt = S.cnt; cnt.fit(4 * (int64_t)ncmd + 2);   // cnt_pred | cnt_act | off_pred | off_act
   auto& comp = S.comp; comp.fit(ncmd);
@@ -426,18 +432,25 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
   k_pred_pass<<<grid, 128, 0, st>>>(P, 0);
   MSG_CHECK_LAUNCH(); add_launches(1);
 
-  std::vector<int64_t> hc(2 * (size_t)ncmd);
-  int32_t herr[2];
-  MSG_CUDA(cudaMemcpyAsync(hc.data(), cnt.p, 2 * ncmd * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  MSG_CUDA(cudaMemcpyAsync(herr, err.p, sizeof(herr), cudaMemcpyDeviceToHost, st));
-  if (complete_out) MSG_CUDA(cudaMemcpyAsync(complete_out, comp.p, ncmd, cudaMemcpyDeviceToHost, st));
+  // pinned layout: hc [0, 2n) | herr [2n, 2n+1) | off [2n+2, 4n+2) | hn [4n+2, 10n+2) | dst [10n+2, 12n+2) |
+  // complete bytes [12n+2, ...)
+  const int64_t n2 = 2 * (int64_t)ncmd;
+  int64_t* hc = hio;
+  int32_t* herr = reinterpret_cast<int32_t*>(hio + n2);
+  int64_t* off = hio + n2 + 2;
+  int64_t* hn = off + n2;
+  int64_t* dst = hn + 3 * n2;
+  uint8_t* hcomp = reinterpret_cast<uint8_t*>(dst + n2);
+  MSG_CUDA(cudaMemcpyAsync(hc, cnt.p, n2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaMemcpyAsync(herr, err.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (complete_out) MSG_CUDA(cudaMemcpyAsync(hcomp, comp.p, ncmd, cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaStreamSynchronize(st));
   if (herr[0]) throw Error(MSG_E_DOMAIN, "rule arithmetic overflow or page id out of range");
+  if (complete_out) std::memcpy(complete_out, hcomp, ncmd);
 
-  std::vector<int64_t> off(2 * (size_t)ncmd);
   int64_t tp = 0, ta = 0;
   for (int i = 0; i < ncmd; ++i) { off[i] = tp; tp += hc[i]; off[ncmd + i] = ta; ta += hc[ncmd + i]; }
-  MSG_CUDA(cudaMemcpyAsync(cnt.p + 2 * ncmd, off.data(), 2 * ncmd * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  MSG_CUDA(cudaMemcpyAsync(cnt.p + 2 * ncmd, off, n2 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   auto& rawp = S.rawp; auto& rawa = S.rawa;
   rawp.fit(2 * std::max<int64_t>(tp, 1)); rawa.fit(2 * std::max<int64_t>(ta, 1));
   P.off_pred = cnt.p + 2 * ncmd; P.off_act = cnt.p + 3 * ncmd; P.raw_pred = rawp.p; P.raw_act = rawa.p;
@@ -461,14 +474,12 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
   N.npages = nn.p + 5 * ncmd;
   k_normalize<<<ncmd, kNormThreads, 0, st>>>(N);
   MSG_CHECK_LAUNCH(); add_launches(2);
-  std::vector<int64_t> hn(6 * (size_t)ncmd);
-  MSG_CUDA(cudaMemcpyAsync(hn.data(), nn.p, 6 * ncmd * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-  MSG_CUDA(cudaMemcpyAsync(herr, err.p, sizeof(herr), cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaMemcpyAsync(hn, nn.p, 3 * n2 * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  MSG_CUDA(cudaMemcpyAsync(herr, err.p, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaStreamSynchronize(st));
   if (herr[0] == 2) throw Error(MSG_E_DOMAIN, "predicted or accessed page outside the dense page map");
 
   // append to the task CSR and the global pools
-  std::vector<int64_t> dst(2 * (size_t)ncmd);
   int64_t pp = t.pred_off.back(), pa = t.act_off.back();
   for (int i = 0; i < ncmd; ++i) {
     dst[i] = pp; pp += hn[i];
@@ -484,7 +495,7 @@ void predict_commands(Ctx& c, TaskTab& t, int32_t ncmd, const msg_cmd* cmds, con
   t.pred_pool.resize(std::max<int64_t>(pp, 1), st);
   t.act_pool.resize(std::max<int64_t>(pa, 1), st);
   auto& ddst = S.dst; ddst.fit(2 * (int64_t)ncmd);
-  MSG_CUDA(cudaMemcpyAsync(ddst.p, dst.data(), 2 * ncmd * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+  MSG_CUDA(cudaMemcpyAsync(ddst.p, dst, n2 * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   k_compact_iv<<<std::min(ncmd, 4096), 128, 0, st>>>(np_.p, P.off_pred, nn.p, ddst.p, t.pred_pool.p, ncmd);
   k_compact_iv<<<std::min(ncmd, 4096), 128, 0, st>>>(na_.p, P.off_act, nn.p + ncmd, ddst.p + ncmd, t.act_pool.p, ncmd);
   MSG_CHECK_LAUNCH(); add_launches(2);

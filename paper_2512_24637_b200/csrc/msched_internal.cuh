@@ -172,14 +172,12 @@ struct Scratch {
 
 // msg_add_commands' device inputs and intermediates (K1), kept across calls
 struct PredScratch {
-  DVec<msg_cmd> cmds;
-  DVec<msg_arg> args;
-  DVec<uint8_t> blob, comp;
-  DVec<msg_range> gt, allocs;
-  DVec<Rule> rules;
-  DVec<int32_t> koff, err;
+  DVec<uint8_t> comp;
+  DVec<int32_t> err;
   DVec<int64_t> cnt, rawp, rawa, nn, gk, dst;
   DVec<Iv> np, na;
+  DVec<uint8_t> din;        // all inputs of one call, one H2D copy
+  HVec<uint8_t> hin, hio;   // pinned staging: the packed inputs; counts / offsets in and out
 };
 
 // Device-side scalar state (one struct in device memory).
