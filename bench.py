@@ -686,7 +686,10 @@ def main(argv=None):
     # command (early start) leg on it
     cfg2 = None
     execute = None
-    if not args.skip_cfg2 and args.config != "cfg2" and migrate:
+    # the sub-objects (config 2, executed commands, fragmented) are single-GPU
+    # evidence: a scaling run (N > 1) times the headline and plan-only only
+    sub_legs = ws == 1
+    if sub_legs and not args.skip_cfg2 and args.config != "cfg2" and migrate:
         t2, h2, p2, d2 = workload("cfg2", rank, args.page_size)
         descs2 = {t.id: build_descriptors(t) for t in t2}
         mode2 = workload_mode("cfg2")
@@ -710,10 +713,10 @@ def main(argv=None):
                              "roofline": multisplit_roofline(qst, load_peaks().get("hbm_gbs", 6550.0))}
         if not args.skip_execute:
             execute = execute_leg(torch, dev, local, ws, t2, h2, p2, mode2, descs2, pool_for(t2, h2), args)
-    elif not args.skip_execute and migrate:
+    elif sub_legs and not args.skip_execute and migrate:
         execute = execute_leg(torch, dev, local, ws, tasks, hw, pol, mode, descs, pool_pages, args)
     frag = None
-    if not args.skip_frag and args.config != "frag" and migrate:
+    if sub_legs and not args.skip_frag and args.config != "frag" and migrate:
         frag = frag_leg(torch, dev, local, ws, args, pk, peak_all, pool_for)
     if rank != 0:
         if ws > 1:

@@ -1654,6 +1654,14 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       " @!p bra MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity) : "memory");
 }
 
+// cp.async (16-byte global -> shared, L2 only) with per-thread groups
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // k-th grid-wide barrier on one monotone counter (zero at launch): the
 // arrival is a gpu-scope release add (it publishes this CTA's writes, which
 // __syncthreads ordered before it), the wait a gpu-scope acquire poll
@@ -1752,7 +1760,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     const int64_t nA0 = A.n + A.a;
     const int64_t cEnd0 = cE + A.E < nA0 ? cE + A.E : nA0;
     const int64_t len0 = cEnd0 > cE ? cEnd0 - cE : 0;
-    issue(A.src0, (int32_t)(len0 < A.vcap ? len0 : A.vcap));
+    issue(A.src0, (int32_t)(len0 <= A.vcap ? len0 : 0));   // a slice is staged whole or streamed (below)
   }
   // class table -> smem (once for all passes).  When the host knows the
   // table's allocated length, every entry up to it is loaded without waiting
@@ -1802,7 +1810,11 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     const int64_t nA = A.n + pa;
     const int64_t cEnd = cE + A.E < nA ? cE + A.E : nA;
     const int64_t lenA = cEnd > cE ? cEnd - cE : 0;
-    const int32_t m = (int32_t)(lenA < A.vcap ? lenA : A.vcap);      // staged entries
+    const int32_t m = (int32_t)(lenA <= A.vcap ? lenA : 0);        // staged entries (all or none)
+    // a slice larger than the cache streams through it instead: every warp
+    // double-buffers its own blocks with cp.async (two 2 KB buffers per warp),
+    // so two blocks per warp are in flight instead of one
+    const bool stream = m == 0 && lenA > 0 && A.vcap >= 2 * MC_BLOCK * MC_WARPS;
     if (tid == 0 && pass > 0) {   // (pass 0's copy was issued at kernel start)
       // every piece of the previous pass has landed (each was waited on by a
       // warp; this makes re-arming safe regardless), then the previous pass's
@@ -1850,6 +1862,16 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     unsigned long long wp_t0 = 0;
     int wp_slow = 0;
 #endif
+    int32_t* const wbuf = cache + warp * 2 * MC_BLOCK;
+    auto gfull = [&](int32_t b) { return cE + (int64_t)(b + 1) * MC_BLOCK <= nA; };
+    auto prefetch = [&](int32_t b) {
+      int32_t* d = wbuf + (b & 1) * MC_BLOCK;
+      const int32_t* s = srcA + cE + (int64_t)b * MC_BLOCK;
+#pragma unroll
+      for (int t = 0; t < 4; ++t) cp_async16(d + 4 * lane + 128 * t, s + 4 * lane + 128 * t);
+      cp_async_commit();
+    };
+    if (stream && b0 < b1 && gfull(b0)) prefetch(b0);
     for (int32_t b = b0; b < b1; ++b) {
       const int32_t boff = b * MC_BLOCK;
       need(boff);
@@ -1863,6 +1885,13 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
       if (boff + MC_BLOCK <= m) {
 #pragma unroll
         for (int t = 0; t < 4; ++t) q[t] = *reinterpret_cast<const int4*>(cache + boff + 4 * lane + 128 * t);
+      } else if (stream && gfull(b)) {
+        // block b was prefetched (before the loop, or in the previous iteration)
+        const bool nxt = b + 1 < b1 && gfull(b + 1);
+        if (nxt) { prefetch(b + 1); cp_async_wait<1>(); } else { cp_async_wait<0>(); }
+        const int32_t* s = wbuf + (b & 1) * MC_BLOCK;   // each lane reads the 16-byte words it copied
+#pragma unroll
+        for (int t = 0; t < 4; ++t) q[t] = *reinterpret_cast<const int4*>(s + 4 * lane + 128 * t);
       } else if (cE + boff + MC_BLOCK <= nA) {
 #pragma unroll
         for (int t = 0; t < 4; ++t)
