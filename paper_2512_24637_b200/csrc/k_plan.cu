@@ -2359,24 +2359,37 @@ __device__ __forceinline__ void bits_update(uint32_t* bits, int32_t p, bool vali
 __device__ __forceinline__ void evict_body(const int32_t* __restrict__ order, int64_t n, uint32_t* bits,
                                            int32_t* frame, int32_t* fifo, int64_t fifo_tail, int64_t C, int64_t* mig,
                                            Epochs ep) {
+  // EV_ILP elements per thread per step, their loads issued together: the
+  // order -> frame chain is paid once per step, not once per element
+  constexpr int EV_ILP = 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int dep = -1;
-  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < n; e0 += stride) {
-    const int64_t e = e0 + threadIdx.x;
-    const bool valid = e < n;
-    const int32_t p = valid ? order[e] : 0;
-    bits_update(bits, p, valid, false);
-    if (!valid) continue;
-    const int32_t f = frame[p];
-    frame[p] = -1;
-    int64_t q = fifo_tail + e;
-    if (q >= C) q -= C;
-    if (q >= C) q -= C;
-    fifo[q] = f;
-    if (mig) mig[e] = ((int64_t)p << 32) | (uint32_t)f;
-    if (ep.inst_ep) {
-      dep = max(dep, ep.inst_ep[f]);
-      ep.free_ep[f] = ep.batch;
+  for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x; e0 < n; e0 += EV_ILP * stride) {
+    int32_t p[EV_ILP], f[EV_ILP];
+    bool v[EV_ILP];
+#pragma unroll
+    for (int k = 0; k < EV_ILP; ++k) {
+      const int64_t e = e0 + k * stride + threadIdx.x;
+      v[k] = e < n;
+      p[k] = v[k] ? order[e] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < EV_ILP; ++k) f[k] = v[k] ? frame[p[k]] : -1;
+#pragma unroll
+    for (int k = 0; k < EV_ILP; ++k) {
+      bits_update(bits, p[k], v[k], false);
+      if (!v[k]) continue;
+      const int64_t e = e0 + k * stride + threadIdx.x;
+      frame[p[k]] = -1;
+      int64_t q = fifo_tail + e;
+      if (q >= C) q -= C;
+      if (q >= C) q -= C;
+      fifo[q] = f[k];
+      if (mig) mig[e] = ((int64_t)p[k] << 32) | (uint32_t)f[k];
+      if (ep.inst_ep) {
+        dep = max(dep, ep.inst_ep[f[k]]);
+        ep.free_ep[f[k]] = ep.batch;
+      }
     }
   }
   if (ep.inst_ep) {
@@ -2393,24 +2406,34 @@ __device__ __forceinline__ void install_body(const int32_t* __restrict__ pages, 
                                              int32_t* frame, const int32_t* __restrict__ fifo, int64_t fifo_head,
                                              int64_t C, int32_t* order_tail, int64_t* mig, Epochs ep,
                                              int64_t old_free) {
+  constexpr int IN_ILP = 4;   // as in evict_body: the loads of several elements in flight together
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   int dep = -1;
-  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n; j0 += stride) {
-    const int64_t j = j0 + threadIdx.x;
-    const bool valid = j < n;
-    const int32_t p = valid ? pages[j] : 0;
-    bits_update(bits, p, valid, true);
-    if (!valid) continue;
-    int64_t q = fifo_head + j;
-    if (q >= C) q -= C;
-    if (q >= C) q -= C;
-    const int32_t f = fifo[q];
-    frame[p] = f;
-    order_tail[j] = p;
-    if (mig) mig[j] = ((int64_t)p << 32) | (uint32_t)f;
-    if (ep.inst_ep) {
-      if (j < old_free) dep = max(dep, ep.free_ep[f]);
-      ep.inst_ep[f] = ep.batch;
+  for (int64_t j0 = (int64_t)blockIdx.x * blockDim.x; j0 < n; j0 += IN_ILP * stride) {
+    int32_t p[IN_ILP], f[IN_ILP];
+    bool v[IN_ILP];
+#pragma unroll
+    for (int k = 0; k < IN_ILP; ++k) {
+      const int64_t j = j0 + k * stride + threadIdx.x;
+      v[k] = j < n;
+      p[k] = v[k] ? pages[j] : 0;
+      int64_t q = fifo_head + j;
+      if (q >= C) q -= C;
+      if (q >= C) q -= C;
+      f[k] = v[k] ? fifo[q] : -1;
+    }
+#pragma unroll
+    for (int k = 0; k < IN_ILP; ++k) {
+      bits_update(bits, p[k], v[k], true);
+      if (!v[k]) continue;
+      const int64_t j = j0 + k * stride + threadIdx.x;
+      frame[p[k]] = f[k];
+      order_tail[j] = p[k];
+      if (mig) mig[j] = ((int64_t)p[k] << 32) | (uint32_t)f[k];
+      if (ep.inst_ep) {
+        if (j < old_free) dep = max(dep, ep.free_ep[f[k]]);
+        ep.inst_ep[f[k]] = ep.batch;
+      }
     }
   }
   if (ep.inst_ep) {

@@ -1,4 +1,3 @@
-timeout 1800 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/r2_pytest_gpu18.txt 2>&1; tail -3 gpurun_out/r2_pytest_gpu18.txt; grep -E "^FAILED|^E " gpurun_out/r2_pytest_gpu18.txt | head
-timeout 900 python bench.py --config cfg4 --steps 3 --warmup 2 --skip-e2e --skip-execute --skip-large --skip-frag --skip-cfg2 --no-migrate > gpurun_out/r2_bench_cfg4_po.jsonl 2>/dev/null; python -c "
-import json; d=json.loads(open('gpurun_out/r2_bench_cfg4_po.jsonl').read()); r=d['roofline']; print(d['ms_per_step'], r['frac'], r['avg_launch_ms'], r['device_timed'])"
-timeout 600 python tools/ms_bench.py 2>&1 | tail -6
+timeout 1800 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/r2_pytest_gpu20.txt 2>&1; tail -3 gpurun_out/r2_pytest_gpu20.txt; grep -E "^FAILED|^E " gpurun_out/r2_pytest_gpu20.txt | head
+for c in cfg2 cfg4; do timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_${c}_v20.csv python tools/prof_replay.py $c 1 > /dev/null 2>&1; python tools/launch_summary.py gpurun_out/launches_${c}_v20.csv | head -8; done
+timeout 300 python tools/prof_replay.py cfg2 3 | tail -1; timeout 300 python tools/prof_replay.py cfg4 2 | tail -1
