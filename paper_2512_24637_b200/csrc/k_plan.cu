@@ -26,6 +26,24 @@
 
 namespace msg {
 
+#ifdef MSG_MC_PHASE_TS
+// k_windows_fused phase stamps: [phase] summed ns since the kernel's first stamp, and launches
+__device__ unsigned long long g_fw_sum[10], g_fw_n;
+#define FWTS(i)                                                                   \
+  do {                                                                            \
+    __syncthreads();                                                              \
+    if (threadIdx.x == 0) {                                                       \
+      unsigned long long t_;                                                      \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                       \
+      if ((i) == 0) fw_t0 = t_;                                                   \
+      atomicAdd(&g_fw_sum[i], t_ - fw_t0);                                        \
+      if ((i) == 9) atomicAdd(&g_fw_n, 1ull);                                     \
+    }                                                                             \
+  } while (0)
+#else
+#define FWTS(i) do {} while (0)
+#endif
+
 static int64_t g_launches = 0;
 int64_t kernel_launches() { return g_launches; }
 void add_launches(int64_t n) { g_launches += n; }
@@ -985,6 +1003,10 @@ __device__ __forceinline__ int32_t fw_lb(const uint64_t* a, int32_t n, uint64_t 
 }
 
 __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
+#ifdef MSG_MC_PHASE_TS
+  unsigned long long fw_t0 = 0;
+#endif
+  FWTS(0);
   extern __shared__ __align__(16) unsigned char fw_raw[];
   FwSmem& s = *reinterpret_cast<FwSmem*>(fw_raw);
   const int t = threadIdx.x;
@@ -1001,6 +1023,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   __syncthreads();
   const int32_t N = (int32_t)s.ioff[W];
   const int64_t NC = s.coff[W];
+  FWTS(1);
   // ---- intervals and their commands
   for (int64_t k = t; k < NC; k += blockDim.x) {
     int w = 0;
@@ -1017,6 +1040,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     s.ia[t] = v.a; s.ib[t] = v.b; s.iw[t] = w;
   }
   __syncthreads();
+  FWTS(2);
   // ---- unique window-tagged endpoints
   {
     uint64_t k = ~0ull;
@@ -1037,6 +1061,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   s.isb[t] = 0;
   __syncthreads();
   const int32_t nu = s.nu;
+  FWTS(3);
   // ---- first-access label per elementary segment (memman.py:187-193)
   if (t < N) {
     uint64_t tag = (uint64_t)s.iw[t] << 48;
@@ -1044,6 +1069,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     for (int32_t k = s0; k < s1; ++k) atomicMin(&s.L[k], s.icmd[t]);
   }
   __syncthreads();
+  FWTS(4);
   // ---- maximal runs of one label (consecutive covered segments share a window)
   {
     const int32_t k = t;
@@ -1059,6 +1085,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   }
   __syncthreads();
   const int32_t R = s.R;
+  FWTS(5);
   // ---- runs in first-access order per window: (window, label, start)
   {
     uint64_t k = ~0ull;
@@ -1094,6 +1121,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     while (lo < hi) { int32_t mid = (lo + hi) >> 1; if (s.span_first[mid] <= a) lo = mid + 1; else hi = mid; }
     return s.span_dense[lo - 1] + (a - s.span_first[lo - 1]);
   };
+  FWTS(6);
   // ---- window 0 demand runs: not self-populating, dense, first-access order
   if (P.R.nr) {
     const int32_t K0 = W > 0 ? s.K[0] : 0;
@@ -1114,6 +1142,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     }
     if (t == 0) { *P.R.nr = tot; P.R.uoff[tot] = utot; }
   }
+  FWTS(7);
   // ---- cross-window class table: elementary segments of all run boundaries
   {
     uint64_t k = ~0ull;
@@ -1171,6 +1200,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     if (t == 0) *P.ncls_out = tot;
   }
   __syncthreads();
+  FWTS(8);
   // ---- covered segments in position order, dense
   {
     const int32_t k = t;
@@ -1184,6 +1214,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     }
     if (t == 0) *P.nseg_out = tot;
   }
+  FWTS(9);
 }
 
 static void win_kernels_init(Ctx& c) {
@@ -2534,6 +2565,22 @@ __global__ void k_table_from_ranges(const int64_t* lo, const int64_t* len, int64
 
 static DevState& hs(Ctx& c) { return *c.hstate; }
 
+// One launch that gathers a call's small results (DevState, per-window and
+// per-command counts) from device buffers straight into the pinned readback
+// buffer (mapped), in place of one device-to-host copy per buffer.
+struct PackSeg { const int64_t* src; int32_t words; int32_t dst_word; };
+struct PackArgs { PackSeg seg[6]; int32_t nseg; int64_t* dst; };
+__global__ void k_pack(PackArgs A) {
+  for (int s = 0; s < A.nseg; ++s)
+    for (int i = threadIdx.x; i < A.seg[s].words; i += blockDim.x) A.dst[A.seg[s].dst_word + i] = A.seg[s].src[i];
+}
+static void pack_to_host(Ctx& c, PackArgs& A) {
+  MSG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&A.dst), c.hbuf.p, 0));
+  k_pack<<<1, 256, 0, c.st>>>(A);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+}
+
 // host phase clock (MSG_HOST_PHASES=1): mark(i) adds the time since the
 // previous mark to phase i of call kind k
 struct PhaseClock {
@@ -2938,17 +2985,22 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     add_launches(1);
     pc.mark(4);
     touch_counts(c, t0, c0, c1);
-    MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
-    MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    // results: win pages | prefix | touch counts | DevState, one gather launch
+    constexpr int kStateWords = (int)(sizeof(DevState) / sizeof(int64_t));
+    static_assert(sizeof(DevState) % sizeof(int64_t) == 0, "DevState packs as 64-bit words");
+    PackArgs PA{};
+    PA.seg[PA.nseg++] = PackSeg{wp.pages, nwin, 0};
     if (ncw) {
-      MSG_CUDA(cudaMemcpyAsync(hb + nwin, pref_d, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-      MSG_CUDA(cudaMemcpyAsync(hb + nwin + ncw, c.s.tc.p, ncw * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      PA.seg[PA.nseg++] = PackSeg{pref_d, ncw, nwin};
+      PA.seg[PA.nseg++] = PackSeg{c.s.tc.p, ncw, nwin + ncw};
     }
+    PA.seg[PA.nseg++] = PackSeg{reinterpret_cast<const int64_t*>(c.dstate), kStateWords, nwin + 2 * ncw};
+    pack_to_host(c, PA);
     MSG_CUDA(cudaEventRecord(e1, st));
     pc.mark(6);
     MSG_CUDA(cudaStreamSynchronize(st));
     pc.mark(7);
-    const DevState S = hs(c);
+    const DevState S = *reinterpret_cast<const DevState*>(hb + nwin + 2 * ncw);
     for (int w = 0; w < nwin; ++w) win_pages[w] = hb[w];
     for (int k = 0; k < ncw; ++k) prefix[k] = hb[nwin + k];
     out->missing = S.missing;
@@ -3094,6 +3146,9 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   // launches the reorder, so the multisplit starts on a busy stream.
   const bool has_iv = t.act_off[cmd + 1] != t.act_off[cmd];
   const bool refresh = evict > 0 && nwin > 0;
+  // the async path gathers its results with one launch at the end
+  const bool async = !(c.cfg.flags & (MSG_F_MIGRATE | MSG_F_VERIFY_TAGS | MSG_F_EXECUTE)) && !c.debug &&
+                     ms_coop_fits(c);
   RangeSet R{};
   int64_t* hb = c.hbuf.p;
   if (has_iv) {
@@ -3103,20 +3158,22 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     c.s.miss.resize(std::max<int64_t>(32 * nu, 1), st);
     R = c.s.ract.set();
     units_plan(c, R, nu, nullptr, 0, -1, c.s.miss.p, -1, c.s.uscr.p + 400);
-    MSG_CUDA(cudaMemcpyAsync(hb, c.s.uscr.p + 400, 8, cudaMemcpyDeviceToHost, st));
+    if (!async) MSG_CUDA(cudaMemcpyAsync(hb, c.s.uscr.p + 400, 8, cudaMemcpyDeviceToHost, st));
   }
   WinBuild wb;
   WinPtrs wp{};
   if (refresh) {
     build_windows(c, win, nwin, wb);
     wp = win_ptrs(c, nwin, wb);
-    MSG_CUDA(cudaMemcpyAsync(hb + 1, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    MSG_CUDA(cudaMemcpyAsync(hb + 1 + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (!async) {
+      MSG_CUDA(cudaMemcpyAsync(hb + 1, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+      MSG_CUDA(cudaMemcpyAsync(hb + 1 + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    }
   }
   pc.mark(0);   // missing-set + window launches (host)
   // ---- async path (see plan_switch): refresh, evict and install follow on
   // the device with counts read there; one host sync at the end
-  if (!(c.cfg.flags & (MSG_F_MIGRATE | MSG_F_VERIFY_TAGS | MSG_F_EXECUTE)) && !c.debug && ms_coop_fits(c)) {
+  if (async) {
     compact_if_needed(c);
     const int64_t len0 = c.len, head0 = c.head, fifo_head0 = c.fifo_head, fifo_len0 = c.fifo_len;
     const int cur0 = c.cur;
@@ -3140,9 +3197,13 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     pc.mark(2);
     const int32_t lo = cmd + 1, hi = scan_end;
     if (hi > lo) touch_counts(c, t, lo, hi);
-    MSG_CUDA(cudaMemcpyAsync(hb + 2 + nwin, passes_d, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    if (hi > lo)
-      MSG_CUDA(cudaMemcpyAsync(hb + 3 + nwin, c.s.tc.p, (hi - lo) * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    // results (one gather launch): n | win pages | ncls slot (unused) | passes | touch counts
+    PackArgs PA{};
+    if (has_iv) PA.seg[PA.nseg++] = PackSeg{c.s.uscr.p + 400, 1, 0};
+    if (refresh) PA.seg[PA.nseg++] = PackSeg{wp.pages, nwin, 1};
+    PA.seg[PA.nseg++] = PackSeg{passes_d, 1, 2 + nwin};
+    if (hi > lo) PA.seg[PA.nseg++] = PackSeg{c.s.tc.p, hi - lo, 3 + nwin};
+    pack_to_host(c, PA);
     pc.mark(5);
     MSG_CUDA(cudaStreamSynchronize(st));
     pc.mark(6);
@@ -3646,6 +3707,11 @@ extern "C" void msg_dbg_mc_cta(unsigned long long* out) {   // 256 x 160 x 8 sta
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, msg::g_mc_cta, sizeof(msg::g_mc_cta));
 }
+extern "C" void msg_dbg_fw_ts(unsigned long long* out) {   // 10 phase sums + launches
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, msg::g_fw_sum, 10 * 8);
+  cudaMemcpyFromSymbol(out + 10, msg::g_fw_n, 8);
+}
 extern "C" void msg_dbg_mc_reset() {
   unsigned long long lo[16], hi[16] = {0}, z[16] = {0}, zn = 0;
   for (int i = 0; i < 16; ++i) lo[i] = ~0ull;
@@ -3653,5 +3719,8 @@ extern "C" void msg_dbg_mc_reset() {
   cudaMemcpyToSymbol(msg::g_mc_max, hi, 128);
   cudaMemcpyToSymbol(msg::g_mc_sum, z, 128);
   cudaMemcpyToSymbol(msg::g_mc_n, &zn, 8);
+  unsigned long long zf[10] = {0};
+  cudaMemcpyToSymbol(msg::g_fw_sum, zf, sizeof(zf));
+  cudaMemcpyToSymbol(msg::g_fw_n, &zn, 8);
 }
 #endif
