@@ -2513,6 +2513,81 @@ __global__ void k_install_dev(const int32_t* __restrict__ pages, ListSel L, cons
                Epochs{nullptr, nullptr, 0, nullptr}, 0);
 }
 
+// results gathered into the pinned readback buffer (see k_pack / k_apply_coop)
+struct PackSeg { const int64_t* src; int32_t words; int32_t dst_word; };
+struct PackArgs { PackSeg seg[6]; int32_t nseg; int64_t* dst; };
+
+// The async path's apply as ONE cooperative launch (in place of evict,
+// install, the touch-count memset + scan and the result gather): evict the
+// head, grid barrier, install the populate list, grid barrier, count the
+// missing pages of the slice's commands against the new residency, grid
+// barrier, and block 0 writes the call's results into the pinned readback
+// buffer.  Counts come from DevState (a switch plan: applied only when it
+// fits) or from the host / *np_dev (a touch).
+struct ApplyArgs {
+  ListSel L;
+  const DevState* S;          // plan counts, or nullptr
+  int64_t ev_host;            // touch: evictions
+  const int64_t* np_dev;      // touch: installs (the missing count)
+  int64_t len0;
+  uint32_t* bits; int32_t* frame; int32_t* fifo;
+  int64_t fifo_tail, fifo_head, C;
+  const int32_t* pages;
+  // touch scan of commands [tc_c0, tc_c0 + tc_n) of one task
+  const Iv* act_pool; const int64_t* act_off; int32_t tc_c0, tc_n;
+  unsigned long long* tc;     // tc_n counters (zeroed here)
+  int32_t* bar;               // grid barrier counter (zero at launch)
+  PackArgs pack;              // results -> pinned readback (pack.dst == nullptr: none)
+};
+constexpr int AP_SPLIT = 8;   // blocks' worth of work per command in the touch scan
+
+__global__ void __launch_bounds__(256) k_apply_coop(ApplyArgs A) {
+  if (blockIdx.x == 0)
+    for (int i = threadIdx.x; i < A.tc_n; i += blockDim.x) A.tc[i] = 0;
+  const bool fits = A.S == nullptr || plan_fits(A.S, A.C, A.len0);
+  const int64_t ev = A.S ? (fits ? A.S->evict : 0) : A.ev_host;
+  int32_t* base = sel_base(A.L);
+  evict_body(base, ev, A.bits, A.frame, A.fifo, A.fifo_tail, A.C, nullptr, Epochs{nullptr, nullptr, 0, nullptr});
+  grid_barrier(A.bar, 0);
+  const int64_t np = A.S ? (fits ? A.S->populate : 0) : *A.np_dev;
+  install_body(A.pages, np, A.bits, A.frame, A.fifo, A.fifo_head, A.C, base + A.len0, nullptr,
+               Epochs{nullptr, nullptr, 0, nullptr}, 0);
+  grid_barrier(A.bar, 1);
+  // touch scan: (command, split) work items over the blocks; each item strides
+  // the command's bitmap words like k_touch_counts' blockIdx.x
+  __shared__ unsigned long long red[8];
+  for (int item = blockIdx.x; item < A.tc_n * AP_SPLIT; item += gridDim.x) {
+    const int32_t cmd = A.tc_c0 + item / AP_SPLIT, split = item % AP_SPLIT;
+    const int64_t i0 = A.act_off[cmd], i1 = A.act_off[cmd + 1];
+    const int64_t T = (int64_t)AP_SPLIT * blockDim.x, me = (int64_t)split * blockDim.x + threadIdx.x;
+    unsigned long long acc = 0;
+    int64_t skip = 0;
+    for (int64_t i = i0; i < i1; ++i) {
+      const Iv v = A.act_pool[i];
+      const int64_t lo = v.d, hi = v.d + (v.b - v.a), w0 = lo >> 5, nw = ((hi + 31) >> 5) - w0;
+      int64_t k = (me - skip) % T;
+      if (k < 0) k += T;
+      for (; k < nw; k += T) acc += __popc(~A.bits[w0 + k] & unit_mask(lo, hi, w0 + k));
+      skip += nw;
+    }
+    acc = __reduce_add_sync(0xffffffffu, (unsigned)acc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long s = 0;
+      for (int k = 0; k < (int)(blockDim.x >> 5); ++k) s += red[k];
+      if (s) atomicAdd(&A.tc[item / AP_SPLIT], s);
+    }
+    __syncthreads();
+  }
+  if (A.pack.dst == nullptr) return;
+  grid_barrier(A.bar, 2);
+  if (blockIdx.x == 0)
+    for (int s = 0; s < A.pack.nseg; ++s)
+      for (int i = threadIdx.x; i < A.pack.seg[s].words; i += blockDim.x)
+        A.pack.dst[A.pack.seg[s].dst_word + i] = A.pack.seg[s].src[i];
+}
+
 // MSG_F_EXECUTE: populate position of every page installed by this switch,
 // and per command of the slice the populate prefix its actual set needs
 __global__ void k_pos_scatter(const int32_t* __restrict__ pages, int64_t n, int64_t tag, int64_t* pos_of) {
@@ -2568,8 +2643,6 @@ static DevState& hs(Ctx& c) { return *c.hstate; }
 // One launch that gathers a call's small results (DevState, per-window and
 // per-command counts) from device buffers straight into the pinned readback
 // buffer (mapped), in place of one device-to-host copy per buffer.
-struct PackSeg { const int64_t* src; int32_t words; int32_t dst_word; };
-struct PackArgs { PackSeg seg[6]; int32_t nseg; int64_t* dst; };
 __global__ void k_pack(PackArgs A) {
   for (int s = 0; s < A.nseg; ++s)
     for (int i = threadIdx.x; i < A.seg[s].words; i += blockDim.x) A.dst[A.seg[s].dst_word + i] = A.seg[s].src[i];
@@ -2577,6 +2650,25 @@ __global__ void k_pack(PackArgs A) {
 static void pack_to_host(Ctx& c, PackArgs& A) {
   MSG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&A.dst), c.hbuf.p, 0));
   k_pack<<<1, 256, 0, c.st>>>(A);
+  MSG_CHECK_LAUNCH();
+  add_launches(1);
+}
+
+// the cooperative apply (evict, install, touch scan, result gather), with a
+// grid sized to the work and bounded by co-residency
+static void apply_coop(Ctx& c, ApplyArgs& A, int64_t work_ub) {
+  if (!c.ap_grid) {
+    int per_sm = 0;
+    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_coop, 256, 0));
+    if (!c.nsm) MSG_CUDA(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, c.device));
+    c.ap_grid = std::max(1, per_sm) * std::max(1, c.nsm);
+  }
+  const int64_t want = std::max<int64_t>((work_ub + 4 * 256 - 1) / (4 * 256), (int64_t)A.tc_n * AP_SPLIT);
+  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c.ap_grid));
+  A.bar = next_barrier(c);
+  if (A.pack.nseg) MSG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&A.pack.dst), c.hbuf.p, 0));
+  void* args[] = {&A};
+  MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_apply_coop), dim3(grid), dim3(256), args, 0, c.st));
   MSG_CHECK_LAUNCH();
   add_launches(1);
 }
@@ -2974,28 +3066,26 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
       ms_coop_launch(c, wp.tab, 0, DevPasses{wp.ncls, &c.dstate->missing, reorder_always ? 1 : 0, passes_d});
     pc.mark(3);
     const ListSel L{c.order[cur0].p, c.order[cur0 ^ 1].p, head0, passes_d};
-    if (len0 > 0) {
-      k_evict_head_dev<<<grid_for(len0, 256), 256, 0, st>>>(L, c.dstate, 0, len0, c.bits.p, c.frame.p, c.fifo.p,
-                                                            fifo_head0 + fifo_len0, c.C);
-      add_launches(1);
-    }
-    k_install_dev<<<grid_for(std::min<int64_t>(32 * units_cap, c.C), 256), 256, 0, st>>>(
-        poplist.p, L, c.dstate, nullptr, len0, c.bits.p, c.frame.p, c.fifo.p, fifo_head0, c.C);
-    MSG_CHECK_LAUNCH();
-    add_launches(1);
-    pc.mark(4);
-    touch_counts(c, t0, c0, c1);
-    // results: win pages | prefix | touch counts | DevState, one gather launch
+    // evict, install, the slice's touch scan and the result gather: one launch
+    // (results: win pages | prefix | touch counts | DevState)
     constexpr int kStateWords = (int)(sizeof(DevState) / sizeof(int64_t));
     static_assert(sizeof(DevState) % sizeof(int64_t) == 0, "DevState packs as 64-bit words");
-    PackArgs PA{};
-    PA.seg[PA.nseg++] = PackSeg{wp.pages, nwin, 0};
+    c.s.tc.resize(std::max(ncw, 1), st);
+    ApplyArgs AA{};
+    AA.L = L; AA.S = c.dstate; AA.len0 = len0;
+    AA.bits = c.bits.p; AA.frame = c.frame.p; AA.fifo = c.fifo.p;
+    AA.fifo_tail = fifo_head0 + fifo_len0; AA.fifo_head = fifo_head0; AA.C = c.C;
+    AA.pages = poplist.p;
+    AA.act_pool = t0.act_pool.p; AA.act_off = t0.d_act_off.p; AA.tc_c0 = c0; AA.tc_n = ncw;
+    AA.tc = reinterpret_cast<unsigned long long*>(c.s.tc.p);
+    AA.pack.seg[AA.pack.nseg++] = PackSeg{wp.pages, nwin, 0};
     if (ncw) {
-      PA.seg[PA.nseg++] = PackSeg{pref_d, ncw, nwin};
-      PA.seg[PA.nseg++] = PackSeg{c.s.tc.p, ncw, nwin + ncw};
+      AA.pack.seg[AA.pack.nseg++] = PackSeg{pref_d, ncw, nwin};
+      AA.pack.seg[AA.pack.nseg++] = PackSeg{c.s.tc.p, ncw, nwin + ncw};
     }
-    PA.seg[PA.nseg++] = PackSeg{reinterpret_cast<const int64_t*>(c.dstate), kStateWords, nwin + 2 * ncw};
-    pack_to_host(c, PA);
+    AA.pack.seg[AA.pack.nseg++] = PackSeg{reinterpret_cast<const int64_t*>(c.dstate), kStateWords, nwin + 2 * ncw};
+    apply_coop(c, AA, std::max(len0, std::min<int64_t>(32 * units_cap, c.C)));
+    pc.mark(4);
     MSG_CUDA(cudaEventRecord(e1, st));
     pc.mark(6);
     MSG_CUDA(cudaStreamSynchronize(st));
@@ -3182,28 +3272,27 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     if (evict > 0 && refresh && len0 > 0) ms_coop_launch(c, wp.tab, 0, DevPasses{wp.ncls, nullptr, 0, passes_d});
     const ListSel L{c.order[cur0].p, c.order[cur0 ^ 1].p, head0, passes_d};
     const int64_t ev_done = evict > 0 ? std::min(evict, len0) : 0;
-    if (ev_done > 0) {
-      k_evict_head_dev<<<grid_for(ev_done, 256), 256, 0, st>>>(L, nullptr, ev_done, len0, c.bits.p, c.frame.p,
-                                                               c.fifo.p, fifo_head0 + fifo_len0, c.C);
-      add_launches(1);
-    }
-    if (has_iv) {
-      const int64_t nu = t.act_units[cmd + 1] - t.act_units[cmd];
-      k_install_dev<<<grid_for(std::max<int64_t>(32 * nu, 1), 256), 256, 0, st>>>(
-          c.s.miss.p, L, nullptr, c.s.uscr.p + 400, len0, c.bits.p, c.frame.p, c.fifo.p, fifo_head0, c.C);
-      add_launches(1);
-    }
-    MSG_CHECK_LAUNCH();
-    pc.mark(2);
     const int32_t lo = cmd + 1, hi = scan_end;
-    if (hi > lo) touch_counts(c, t, lo, hi);
-    // results (one gather launch): n | win pages | ncls slot (unused) | passes | touch counts
-    PackArgs PA{};
-    if (has_iv) PA.seg[PA.nseg++] = PackSeg{c.s.uscr.p + 400, 1, 0};
-    if (refresh) PA.seg[PA.nseg++] = PackSeg{wp.pages, nwin, 1};
-    PA.seg[PA.nseg++] = PackSeg{passes_d, 1, 2 + nwin};
-    if (hi > lo) PA.seg[PA.nseg++] = PackSeg{c.s.tc.p, hi - lo, 3 + nwin};
-    pack_to_host(c, PA);
+    // evict, install, the rescan and the result gather: one launch
+    // (results: n | win pages | ncls slot (unused) | passes | touch counts)
+    c.s.tc.resize(std::max(hi - lo, 1), st);
+    if (!has_iv) {
+      c.s.uscr.resize(512, st);
+      MSG_CUDA(cudaMemsetAsync(c.s.uscr.p + 400, 0, sizeof(int64_t), st));
+    }
+    ApplyArgs AA{};
+    AA.L = L; AA.S = nullptr; AA.ev_host = ev_done; AA.np_dev = c.s.uscr.p + 400; AA.len0 = len0;
+    AA.bits = c.bits.p; AA.frame = c.frame.p; AA.fifo = c.fifo.p;
+    AA.fifo_tail = fifo_head0 + fifo_len0; AA.fifo_head = fifo_head0; AA.C = c.C;
+    AA.pages = c.s.miss.p;
+    AA.act_pool = t.act_pool.p; AA.act_off = t.d_act_off.p; AA.tc_c0 = lo; AA.tc_n = std::max(hi - lo, 0);
+    AA.tc = reinterpret_cast<unsigned long long*>(c.s.tc.p);
+    if (has_iv) AA.pack.seg[AA.pack.nseg++] = PackSeg{c.s.uscr.p + 400, 1, 0};
+    if (refresh) AA.pack.seg[AA.pack.nseg++] = PackSeg{wp.pages, nwin, 1};
+    AA.pack.seg[AA.pack.nseg++] = PackSeg{passes_d, 1, 2 + nwin};
+    if (hi > lo) AA.pack.seg[AA.pack.nseg++] = PackSeg{c.s.tc.p, hi - lo, 3 + nwin};
+    const int64_t nu = has_iv ? t.act_units[cmd + 1] - t.act_units[cmd] : 0;
+    apply_coop(c, AA, std::max(ev_done, 32 * nu));
     pc.mark(5);
     MSG_CUDA(cudaStreamSynchronize(st));
     pc.mark(6);

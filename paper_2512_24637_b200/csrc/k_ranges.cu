@@ -14,13 +14,6 @@
 
 namespace msg {
 
-__device__ __forceinline__ uint32_t unit_mask(int64_t lo, int64_t hi, int64_t w) {
-  int64_t p0 = w << 5;
-  uint32_t m = ~0u;
-  if (p0 < lo) m &= ~0u << (lo - p0);
-  if (p0 + 32 > hi) m &= (hi - p0) >= 32 ? ~0u : ((1u << (hi - p0)) - 1u);
-  return m;
-}
 
 
 // Ranges = the actual intervals of commands [c0, c1) of one task; tag = command - c0.

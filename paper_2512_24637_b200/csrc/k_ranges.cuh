@@ -4,6 +4,15 @@
 
 namespace msg {
 
+// bits of bitmap word w that lie in the dense page range [lo, hi)
+__device__ __forceinline__ uint32_t unit_mask(int64_t lo, int64_t hi, int64_t w) {
+  int64_t p0 = w << 5;
+  uint32_t m = ~0u;
+  if (p0 < lo) m &= ~0u << (lo - p0);
+  if (p0 + 32 > hi) m &= (hi - p0) >= 32 ? ~0u : ((1u << (hi - p0)) - 1u);
+  return m;
+}
+
 __device__ __forceinline__ int64_t block_scan_excl_i64(int64_t v, int64_t* smem_warp, int64_t* total) {
   int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int64_t x = v;
