@@ -3061,7 +3061,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     const int64_t len0 = c.len, head0 = c.head, fifo_head0 = c.fifo_head, fifo_len0 = c.fifo_len;
     const int cur0 = c.cur;
     int64_t* passes_d = &c.dstate->aux[2];
-    MSG_CUDA(cudaMemsetAsync(passes_d, 0, sizeof(int64_t), st));
+    // (units_plan zeroed the pass-count slot with the plan scalars)
     if (len0 > 0)
       ms_coop_launch(c, wp.tab, 0, DevPasses{wp.ncls, &c.dstate->missing, reorder_always ? 1 : 0, passes_d});
     pc.mark(3);

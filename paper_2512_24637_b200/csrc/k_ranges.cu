@@ -192,6 +192,7 @@ __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
       int64_t ev = pop - (P.C - P.len);
       S->evict = ev > 0 ? ev : 0;
       S->skip = all_tot == 0;
+      S->aux[2] = 0;   // the switch's multisplit pass count, until the multisplit publishes it
     }
   }
   if (!P.out) return;
