@@ -1660,6 +1660,7 @@ struct McArgs {
   const int64_t* missing_dev;
   int32_t reorder_always;
   int64_t* passes_out;
+  int32_t force_stream;          // test / tuning hook (MSG_MS_STREAM=1): stream even slices that fit
 };
 
 // TMA bulk copy global -> shared, completion counted on an mbarrier.
@@ -1791,7 +1792,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     const int64_t nA0 = A.n + A.a;
     const int64_t cEnd0 = cE + A.E < nA0 ? cE + A.E : nA0;
     const int64_t len0 = cEnd0 > cE ? cEnd0 - cE : 0;
-    issue(A.src0, (int32_t)(len0 <= A.vcap ? len0 : 0));   // a slice is staged whole or streamed (below)
+    issue(A.src0, (int32_t)(len0 <= A.vcap && !A.force_stream ? len0 : 0));   // staged whole or streamed (below)
   }
   // class table -> smem (once for all passes).  When the host knows the
   // table's allocated length, every entry up to it is loaded without waiting
@@ -1841,7 +1842,7 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     const int64_t nA = A.n + pa;
     const int64_t cEnd = cE + A.E < nA ? cE + A.E : nA;
     const int64_t lenA = cEnd > cE ? cEnd - cE : 0;
-    const int32_t m = (int32_t)(lenA <= A.vcap ? lenA : 0);        // staged entries (all or none)
+    const int32_t m = (int32_t)(lenA <= A.vcap && !A.force_stream ? lenA : 0);   // staged entries (all or none)
     // a slice larger than the cache streams through it instead: every warp
     // double-buffers its own blocks with cp.async (two 2 KB buffers per warp),
     // so two blocks per warp are in flight instead of one
@@ -2262,8 +2263,10 @@ static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes, DevPasses dp = D
   const int64_t avail = (int64_t)MC_SMEM - MC_FIXED - 8 * (((nch + 1) + 1) & ~int64_t(1)) - 16;
   int64_t tcap = (avail - 4 * (E + 4)) / 12;
   tcap = std::max<int64_t>(MC_TCAP_MIN, std::min<int64_t>(tcap, MC_TCAP_MAX)) & ~int64_t(3);
+  if (c.ms_force_stream) tcap = MC_TCAP_MIN;   // the whole cache for the per-warp stream buffers
   int64_t vcap = (avail - 12 * tcap) / 4 - 4;
-  vcap = std::min<int64_t>(vcap, E) & ~int64_t(3);
+  if (!c.ms_force_stream) vcap = std::min<int64_t>(vcap, E);
+  vcap &= ~int64_t(3);
   if (vcap < 0) return false;
   if ((int64_t)c.ms_hist.n < 256 * ((int64_t)coop_grid + 2)) {
     c.ms_hist.exact(256 * ((int64_t)coop_grid + 2));   // rows + two digit-total rows
@@ -2290,7 +2293,7 @@ static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes, DevPasses dp = D
   McArgs A{src0 - a, c.order[c.cur].p, c.order[c.cur ^ 1].p, n, a, T, c.ms_hist.p,
            c.ms_hist.p + 256 * (int64_t)coop_grid, c.ms_tot_par, next_barrier(c), E, (int32_t)vcap, (int32_t)nch,
            passes, tf, tl, (int32_t)(c.ms_launch_id++), (int32_t)tcap, dp.ncls, dp.missing, dp.reorder_always,
-           dp.out};
+           dp.out, c.ms_force_stream};
   void* args[] = {&A};
   MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS), args,
                                        MC_SMEM, c.st));

@@ -176,6 +176,7 @@ int msg_create(const msg_cfg* cfg, msg_ctx** out) {
       if (v.find("demand") != std::string::npos) c.fallback |= 4;
     }
     if (const char* f = std::getenv("MSG_HOST_PHASES")) c.host_phases = f[0] == '1';
+    if (const char* f = std::getenv("MSG_MS_STREAM")) c.ms_force_stream = f[0] == '1';
     // test hook: MSG_EVENT_BOUND=n folds the context's events past n (fold_events)
     if (const char* f = std::getenv("MSG_EVENT_BOUND")) c.event_bound = (size_t)std::max(1ll, std::atoll(f));
   });

@@ -277,6 +277,7 @@ struct Ctx {
   // per-device kernel setup (dynamic shared memory attributes are per device)
   bool win_init = false;
   int ms_grid_cap = 0, ms_coop_grid = 0, up_per_sm = -1, nsm = 0, ap_grid = 0;
+  int ms_force_stream = 0;            // MSG_MS_STREAM=1 (tuning / test hook)
   uint32_t ms_epoch = 0;
   int64_t ms_launch_id = 0;           // cooperative multisplit launches (phase-timing build)
   std::vector<int64_t> dbg[4];
