@@ -547,22 +547,35 @@ class Leg:
 
 
 def multisplit_roofline(st, hbm_peak, traffic=None, traffic_src=None):
-    ms_kernel_ms = st["ms_ms"] / max(st["ms_passes"], 1)
     ms_bytes = st["ms_bytes"] / max(st["ms_passes"], 1)
-    achieved = ms_bytes / (ms_kernel_ms * 1e6) if ms_kernel_ms else 0.0
     dev_timed = None
     if st.get("ms_dev_launches"):
         dms = st["ms_dev_ms"] / st["ms_dev_launches"]
         dev_timed = {"avg_launch_ms": dms, "achieved": ms_bytes / (dms * 1e6),
                      "frac": ms_bytes / (dms * 1e6) / hbm_peak, "launches_per_step": st["ms_dev_launches"]}
+    ev_passes = st.get("ms_ev_passes", st["ms_passes"])
+    if ev_passes:
+        # standalone launches (the synchronous, migrating path): CUDA events around each launch
+        ms_kernel_ms = st["ms_ms"] / ev_passes
+        timing = "CUDA events on the planner stream around each launch, averaged over the timed steps"
+        launches = ev_passes
+    elif dev_timed:
+        # the async path runs the multisplit as a phase of its per-switch cooperative kernel: there is no
+        # launch of its own to bracket with events, so the device clock is the timing
+        ms_kernel_ms = dev_timed["avg_launch_ms"]
+        timing = ("%globaltimer on the device, first CTA start to last CTA end of the multisplit phase inside "
+                  "the per-switch cooperative kernel (k_switch_coop), averaged over the timed steps")
+        launches = st["ms_dev_launches"]
+    else:
+        ms_kernel_ms, timing, launches = 0.0, "no multisplit ran", 0
+    achieved = ms_bytes / (ms_kernel_ms * 1e6) if ms_kernel_ms else 0.0
     return {"bound": "hbm", "kernel": "reorder multisplit (k_ms_coop: TMA-staged, one grid barrier per pass)",
             "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
             "frac": achieved / hbm_peak if hbm_peak else None, "traffic": traffic, "traffic_source": traffic_src,
             "algorithmic_bytes_per_launch": ms_bytes,
             "algorithmic_bytes_per_unit": "8 B per list entry (4 B id read + 4 B written) per digit pass",
-            "avg_launch_ms": ms_kernel_ms, "launches_per_step": st["ms_passes"],
-            "timing": "CUDA events on the planner stream around each launch, averaged over the timed steps",
-            "device_timed": dev_timed}
+            "avg_launch_ms": ms_kernel_ms, "launches_per_step": launches,
+            "timing": timing, "device_timed": dev_timed}
 
 
 def migration_summary(st, ms_step, pk, ws, link_all):
@@ -678,7 +691,8 @@ def main(argv=None):
         pl.close()
         p_ms = max_over_ranks(torch, statistics.mean(p_times), ws, dev)
         plan_only = {"value": pages_step / (p_ms / 1e3), "unit": UNIT, "ms_per_step": p_ms,
-                     "multisplit_ms_per_step": pst["ms_ms"], "planner_stream_ms_per_step": pst["plan_ms"],
+                     "multisplit_ms_per_step": pst["ms_ms"] if pst.get("ms_ev_passes") else pst["ms_dev_ms"],
+                     "planner_stream_ms_per_step": pst["plan_ms"],
                      "gpu_launches_per_step": p_launch // max(args.steps, 1),
                      "roofline": multisplit_roofline(pst, load_peaks().get("hbm_gbs", 6550.0)),
                      "note": "replay with migration off: the reference's own work (plans + modeled timing)"}

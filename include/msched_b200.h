@@ -175,6 +175,10 @@ typedef struct {
    * latency */
   int64_t ms_dev_launches;
   double ms_dev_ms;
+  /* passes whose launch ms_ms brackets with CUDA events (standalone
+   * multisplit launches); the async switch path runs the multisplit as a
+   * phase of its per-switch kernel, timed on the device only */
+  int64_t ms_ev_passes;
 } msg_stats;
 
 /* Forget all residency (bitmap, list, frames); keep the task tables and the

@@ -66,7 +66,8 @@ class Stats(C.Structure):
                 ("plan_ms", C.c_double), ("ms_passes", C.c_int64), ("ms_ms", C.c_double),
                 ("ms_bytes", C.c_int64), ("run_cmds", C.c_int64), ("run_pages", C.c_int64),
                 ("run_bad_tags", C.c_int64), ("run_missing", C.c_int64), ("run_ms", C.c_double),
-                ("ms_dev_launches", C.c_int64), ("ms_dev_ms", C.c_double)]
+                ("ms_dev_launches", C.c_int64), ("ms_dev_ms", C.c_double),
+                ("ms_ev_passes", C.c_int64)]
 
     def as_dict(self):
         return {f: getattr(self, f) for f, _ in self._fields_}

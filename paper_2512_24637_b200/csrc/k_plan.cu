@@ -27,21 +27,43 @@
 namespace msg {
 
 #ifdef MSG_MC_PHASE_TS
-// k_windows_fused phase stamps: [phase] summed ns since the kernel's first stamp, and launches
-__device__ unsigned long long g_fw_sum[10], g_fw_n;
+// k_windows_fused phase stamps: [phase] summed SM cycles since the kernel's first stamp, and launches
+__device__ unsigned long long g_fw_sum[16], g_fw_n;
 #define FWTS(i)                                                                   \
   do {                                                                            \
     __syncthreads();                                                              \
     if (threadIdx.x == 0) {                                                       \
-      unsigned long long t_;                                                      \
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                       \
+      const unsigned long long t_ = (unsigned long long)clock64();  /* one CTA: SM cycles */ \
       if ((i) == 0) fw_t0 = t_;                                                   \
       atomicAdd(&g_fw_sum[i], t_ - fw_t0);                                        \
-      if ((i) == 9) atomicAdd(&g_fw_n, 1ull);                                     \
+      if ((i) == 15) atomicAdd(&g_fw_n, 1ull);                                     \
+    }                                                                             \
+  } while (0)
+// k_switch_coop phase stamps (block 0, after each grid barrier: every CTA is
+// past the previous phase): [phase] summed ns since the kernel's start, and launches
+__device__ unsigned long long g_sw_sum[8], g_sw_n;
+// gap from the window kernel's last stamp to the switch kernel's first
+// (launches that directly follow a window kernel): sum, count
+__device__ unsigned long long g_fw_end, g_gap_sum, g_gap_n;
+__shared__ unsigned long long sw_t0;
+#define SWTS(i)                                                                   \
+  do {                                                                            \
+    if (blockIdx.x == 0 && threadIdx.x == 0) {                                    \
+      unsigned long long t_;                                                      \
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));                       \
+      if ((i) == 0) {                                                             \
+        sw_t0 = t_;                                                               \
+        const unsigned long long fe_ = *(volatile unsigned long long*)&g_fw_end;  \
+        if (fe_ && t_ > fe_) { atomicAdd(&g_gap_sum, t_ - fe_); atomicAdd(&g_gap_n, 1ull); } \
+        *(volatile unsigned long long*)&g_fw_end = 0;                             \
+      }                                                                           \
+      atomicAdd(&g_sw_sum[i], t_ - sw_t0);                                        \
+      if ((i) == 7) atomicAdd(&g_sw_n, 1ull);                                     \
     }                                                                             \
   } while (0)
 #else
 #define FWTS(i) do {} while (0)
+#define SWTS(i) do {} while (0)
 #endif
 
 static int64_t g_launches = 0;
@@ -865,6 +887,8 @@ constexpr int FW_MAX_WIN = 16;
 constexpr int FW_MAX_IV = 512;   // 2 x 512 endpoints: one per thread of a 1024-thread CTA
 constexpr int FW_MAX_SPANS = 1024;
 constexpr uint64_t FW_POS = (1ull << 48) - 1;
+constexpr int FW_SP_CAP = 4096;    // window-0 commands whose self-populating flags are staged
+constexpr int FW_LAB_SCAN = 128;   // up to this many intervals, labels are a per-segment scan (else atomics)
 
 struct FusedWinParams {
   WinDesc wd[FW_MAX_WIN];
@@ -899,6 +923,7 @@ struct FwSmem {
   int32_t wfirst[FW_MAX_WIN], K[FW_MAX_WIN];
   unsigned long long pages[FW_MAX_WIN];
   unsigned __int128 M[FW_MAX_WIN];
+  uint8_t sp0[FW_SP_CAP];       // window 0's self-populating flags, prefetched with the intervals
   int32_t nu, R, nu2;
 };
 
@@ -922,17 +947,17 @@ __device__ __forceinline__ void fw_rank_sortT(uint64_t& hi, uint64_t& lo, int32_
   __syncthreads();
   if (t < n) {
     int r = 0;
+    const int32_t me = PAY ? v : t;
+    // every operand loaded unconditionally and combined with bitwise ops: a
+    // short-circuit chain compiles to dependent load-compare-branch steps
 #pragma unroll 8
     for (int i = 0; i < n; ++i) {
       const uint64_t ol = s.xk2[i];
-      bool less;
-      if (HI) {
-        const uint64_t oh = s.xk[i];
-        less = oh < hi || (oh == hi && (ol < lo || (ol == lo && (PAY ? s.xv[i] < v : i < t))));
-      } else {
-        less = ol < lo || (ol == lo && (PAY ? s.xv[i] < v : i < t));
-      }
-      r += less ? 1 : 0;
+      const uint64_t oh = HI ? s.xk[i] : 0;
+      const int32_t ov = PAY ? s.xv[i] : i;
+      const bool lt = (ol < lo) | ((ol == lo) & (ov < me));
+      const bool less = HI ? ((oh < hi) | ((oh == hi) & lt)) : lt;
+      r += (int)less;
     }
     if (HI) s.yk[r] = hi;
     s.yk2[r] = lo;
@@ -1019,12 +1044,16 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     }
   }
   if (t < FW_MAX_WIN) { s.wfirst[t] = 0x7fffffff; s.K[t] = 0; s.pages[t] = 0; }
-  for (int i = t; i < P.nspans; i += blockDim.x) { s.span_first[i] = P.span_first[i]; s.span_dense[i] = P.span_dense[i]; }
   __syncthreads();
   const int32_t N = (int32_t)s.ioff[W];
   const int64_t NC = s.coff[W];
   FWTS(1);
-  // ---- intervals and their commands
+  // ---- every global input in one round: spans, intervals and their
+  // commands, window 0's self-populating flags (independent loads)
+  for (int i = t; i < P.nspans; i += blockDim.x) { s.span_first[i] = P.span_first[i]; s.span_dense[i] = P.span_dense[i]; }
+  const int32_t ncw0 = W > 0 ? P.wd[0].c1 - P.wd[0].c0 : 0;
+  if (P.R.nr && ncw0 <= FW_SP_CAP)
+    for (int i = t; i < ncw0; i += blockDim.x) s.sp0[i] = P.wd[0].selfpop[P.wd[0].c0 + i];
   for (int64_t k = t; k < NC; k += blockDim.x) {
     int w = 0;
     while (k >= s.coff[w + 1]) ++w;
@@ -1063,10 +1092,28 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   const int32_t nu = s.nu;
   FWTS(3);
   // ---- first-access label per elementary segment (memman.py:187-193)
-  if (t < N) {
-    uint64_t tag = (uint64_t)s.iw[t] << 48;
-    int32_t s0 = fw_lb(s.E, nu, tag | (uint64_t)s.ia[t]), s1 = fw_lb(s.E, nu, tag | (uint64_t)s.ib[t]);
-    for (int32_t k = s0; k < s1; ++k) atomicMin(&s.L[k], s.icmd[t]);
+  {
+    int4* span4 = reinterpret_cast<int4*>(s.yk);   // (first segment, end segment, command) per interval
+    if (t < N) {
+      uint64_t tag = (uint64_t)s.iw[t] << 48;
+      int32_t s0 = fw_lb(s.E, nu, tag | (uint64_t)s.ia[t]), s1 = fw_lb(s.E, nu, tag | (uint64_t)s.ib[t]);
+      if (N <= FW_LAB_SCAN) span4[t] = make_int4(s0, s1, s.icmd[t], 0);
+      else for (int32_t k = s0; k < s1; ++k) atomicMin(&s.L[k], s.icmd[t]);
+    }
+    if (N <= FW_LAB_SCAN) {
+      // few intervals: each segment takes the min over the intervals covering
+      // it (broadcast loads), instead of one thread walking a long interval
+      __syncthreads();
+      if (t < nu - 1) {
+        int32_t m = kNone;
+#pragma unroll 4
+        for (int i = 0; i < N; ++i) {
+          const int4 q = span4[i];
+          m = (t >= q.x && t < q.y && q.z < m) ? q.z : m;
+        }
+        s.L[t] = m;
+      }
+    }
   }
   __syncthreads();
   FWTS(4);
@@ -1129,7 +1176,8 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     bool keep = false;
     int64_t dlo = 0, dlen = 0;
     if (r < K0) {
-      keep = !P.wd[0].selfpop[s.sl[r]];
+      const int32_t c = s.sl[r];
+      keep = !(ncw0 <= FW_SP_CAP ? s.sp0[c - P.wd[0].c0] : P.wd[0].selfpop[c]);
       dlo = dense_of(s.sa[r]);
       dlen = s.sb[r] - s.sa[r];
     }
@@ -1148,6 +1196,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     uint64_t k = ~0ull;
     if (t < nu && s.isb[t]) k = s.E[t] & FW_POS;
     fw_sort(k, s, fw_pow2(nu));
+    FWTS(8);
     s.xk[t] = k;
     __syncthreads();
     bool f = k != ~0ull && (t == 0 || s.xk[t - 1] != k);
@@ -1163,6 +1212,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
   }
   __syncthreads();
   const int32_t nu2 = s.nu2;
+  FWTS(9);
   // paint each window's class over the elementary segments (all windows in
   // parallel: runs of one window are disjoint), then fold to the mixed radix
   for (int i = t; i < W * nu2; i += blockDim.x) s.wcls[(i / nu2) * 1024 + i % nu2] = 0;
@@ -1173,12 +1223,14 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     for (int32_t k = s0; k < s1; ++k) s.wcls[s.sw[t] * 1024 + k] = c;
   }
   __syncthreads();
+  FWTS(10);
   if (t < nu2 - 1) {
     unsigned __int128 key = 0;
     for (int w = 0; w < W; ++w) key += (unsigned __int128)s.wcls[w * 1024 + t] * s.M[w];
     s.skey[t] = key;
   }
   __syncthreads();
+  FWTS(11);
   // dense rank of the distinct tuples over covered segments
   {
     const int32_t k = t;
@@ -1189,6 +1241,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     const int ns = fw_pow2(nu2 > 1 ? nu2 - 1 : 1);
     if (__syncthreads_or(cov && hi != 0)) fw_sort2(hi, lo, v, s, ns);
     else fw_sortT<false, true>(hi, lo, v, s, ns);
+    FWTS(12);
     const bool valid = t < ns && v < nu2 - 1 && s.skey[v] != 0;
     if (valid) { hi = (uint64_t)(s.skey[v] >> 64); lo = (uint64_t)s.skey[v]; }
     s.xk[t] = hi; s.xk2[t] = lo;
@@ -1200,7 +1253,7 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     if (t == 0) *P.ncls_out = tot;
   }
   __syncthreads();
-  FWTS(8);
+  FWTS(13);
   // ---- covered segments in position order, dense
   {
     const int32_t k = t;
@@ -1214,7 +1267,14 @@ __global__ void __launch_bounds__(1024, 1) k_windows_fused(FusedWinParams P) {
     }
     if (t == 0) *P.nseg_out = tot;
   }
-  FWTS(9);
+  FWTS(15);
+#ifdef MSG_MC_PHASE_TS
+  if (t == 0) {
+    unsigned long long t_;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_));
+    *(volatile unsigned long long*)&g_fw_end = t_;
+  }
+#endif
 }
 
 static void win_kernels_init(Ctx& c) {
@@ -1694,22 +1754,6 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// k-th grid-wide barrier on one monotone counter (zero at launch): the
-// arrival is a gpu-scope release add (it publishes this CTA's writes, which
-// __syncthreads ordered before it), the wait a gpu-scope acquire poll
-__device__ __forceinline__ void grid_barrier(int32_t* bar, int k) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(bar) : "memory");
-    const int32_t target = (k + 1) * (int32_t)gridDim.x;
-    int32_t v;
-    do {
-      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(bar) : "memory");
-    } while (v < target);
-  }
-  __syncthreads();
-}
-
 __device__ __forceinline__ int ms_digit(const SegView& S, int32_t x, int32_t c_lo, int32_t c_hi, int c_d, int shift) {
   if (x >= c_lo && x < c_hi) return c_d;
   return (seg_find(S, x).cls >> shift) & 255;
@@ -1750,10 +1794,12 @@ __device__ __forceinline__ unsigned long long mc_now() {
 #define MCTS_START do {} while (0)
 #endif
 
-__global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
+// The multisplit runs as its own cooperative launch (k_ms_coop) or as a phase
+// of the per-switch cooperative kernel (k_switch_coop); nbar counts the grid
+// barriers used so far on A.bar.
+__device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_raw, int& nbar) {
   MCTS_START;
-  if (threadIdx.x == 0) atomicMin(A.t_first, global_ns());   // device-side launch duration (stats)
-  extern __shared__ __align__(16) unsigned char mc_raw[];
+  if (threadIdx.x == 0) atomicMin(A.t_first, global_ns());   // device-side duration of the multisplit (stats)
   int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(mc_raw);
   int64_t* base = reinterpret_cast<int64_t*>(cnt + MC_WARPS);
   int32_t* red = reinterpret_cast<int32_t*>(base + 256);          // [16][256]
@@ -1785,7 +1831,10 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   };
   if (tid == 0) {
     // pass 0's slice goes to shared memory first -- before the pass count
-    // and the class table are read -- so the copy overlaps those loads
+    // and the class table are read -- so the copy overlaps those loads.
+    // (An earlier phase of the same kernel may have used this shared memory
+    // through the generic proxy.)
+    asm volatile("fence.proxy.async;" ::: "memory");
     for (int k = 0; k < MC_PIECES; ++k)
       asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar + k)), "r"(1) : "memory");
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1819,8 +1868,9 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   }
   int passes = A.passes;
   if (A.ncls_dev) {
-    const bool skip = A.missing_dev && *A.missing_dev == 0 && !A.reorder_always;
-    int64_t nc = skip ? 0 : *A.ncls_dev;
+    // (L2 loads: an earlier phase of the same kernel may have written them)
+    const bool skip = A.missing_dev && __ldcg(A.missing_dev) == 0 && !A.reorder_always;
+    int64_t nc = skip ? 0 : __ldcg(A.ncls_dev);
     passes = 0;
     while (nc > 0) { ++passes; nc >>= 8; }
     if (blockIdx.x == 0 && threadIdx.x == 0) *A.passes_out = passes;
@@ -1832,7 +1882,6 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
     }
   }
   __syncthreads();   // the initialised mbarrier and the class table, before any use
-  int nbar = 0;
   for (int pass = 0; pass < passes; ++pass) {
     const int shift = 8 * pass;
     // pass p reads what pass p-1 wrote (buffers alternate; only pass 0 is offset)
@@ -2130,6 +2179,12 @@ __global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
   if (threadIdx.x == 0) atomicMax(A.t_last, global_ns());
 }
 
+__global__ void __launch_bounds__(MC_THREADS, 1) k_ms_coop(McArgs A) {
+  extern __shared__ __align__(16) unsigned char mc_raw[];
+  int nbar = 0;
+  ms_coop_body(A, mc_raw, nbar);
+}
+
 // generic exclusive scan (int32 in -> int64 out), 3 phases
 constexpr int SCAN_BLOCK = 1024, SCAN_ITEMS = 4, SCAN_CHUNK = SCAN_BLOCK * SCAN_ITEMS;
 
@@ -2227,9 +2282,9 @@ static void ms_init(Ctx& c) {
 // does not fit the on-chip path (the caller falls back).
 // whether the cooperative multisplit can take the current list (the same
 // geometry test ms_coop_launch makes), without launching it
-static bool ms_coop_fits(Ctx& c) {
+static bool ms_coop_fits(Ctx& c, int grid = 0) {
   ms_init(c);
-  const int coop_grid = c.ms_coop_grid;
+  const int coop_grid = grid ? grid : c.ms_coop_grid;
   if (c.len == 0 || coop_grid <= 0 || (c.debug & 8) || (c.fallback & 2)) return c.len == 0;
   const int64_t nA = c.len + 3;
   int64_t E = (nA + coop_grid - 1) / coop_grid;
@@ -2246,15 +2301,16 @@ struct DevPasses {   // the async path: pass count decided on the device
   int64_t* out = nullptr;
 };
 
-static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes, DevPasses dp = DevPasses{}) {
+// The multisplit's arguments for a cooperative grid of `grid` CTAs (false when
+// the list does not fit the on-chip path).  Claims a device-timing slot.
+static bool ms_args(Ctx& c, const SegTab& T, int passes, DevPasses dp, int grid, int32_t* bar, McArgs& A) {
   ms_init(c);
   const int64_t n = c.len;
-  const int coop_grid = c.ms_coop_grid;
-  if (n == 0 || coop_grid <= 0 || (c.debug & 8) || (c.fallback & 2)) return false;
+  if (n == 0 || grid <= 0 || (c.debug & 8) || (c.fallback & 2)) return false;
   const int32_t* src0 = c.order[c.cur].p + c.head;
   const int32_t a = (int32_t)((reinterpret_cast<uintptr_t>(src0) & 15) >> 2);
   const int64_t nA = n + a;
-  int64_t E = (nA + coop_grid - 1) / coop_grid;
+  int64_t E = (nA + grid - 1) / grid;
   E = (E + MC_BLOCK - 1) / MC_BLOCK * MC_BLOCK;
   const int64_t nch = E / MS_CHUNK;
   // shared memory after the fixed part and the chunk records: the slice
@@ -2268,8 +2324,8 @@ static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes, DevPasses dp = D
   if (!c.ms_force_stream) vcap = std::min<int64_t>(vcap, E);
   vcap &= ~int64_t(3);
   if (vcap < 0) return false;
-  if ((int64_t)c.ms_hist.n < 256 * ((int64_t)coop_grid + 2)) {
-    c.ms_hist.exact(256 * ((int64_t)coop_grid + 2));   // rows + two digit-total rows
+  if ((int64_t)c.ms_hist.n < 256 * ((int64_t)grid + 2)) {
+    c.ms_hist.exact(256 * ((int64_t)grid + 2));   // rows + two digit-total rows
     MSG_CUDA(cudaMemsetAsync(c.ms_hist.p, 0, c.ms_hist.n * 4, c.st));
     c.ms_tot_par = 0;
   }
@@ -2284,28 +2340,38 @@ static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes, DevPasses dp = D
   unsigned long long* tf = c.ms_tring.p + c.ms_tslot;
   unsigned long long* tl = c.ms_tring.p + 4096 + c.ms_tslot;
   ++c.ms_tslot;
+  A = McArgs{src0 - a, c.order[c.cur].p, c.order[c.cur ^ 1].p, n, a, T, c.ms_hist.p,
+             c.ms_hist.p + 256 * (int64_t)grid, c.ms_tot_par, bar, E, (int32_t)vcap, (int32_t)nch,
+             passes, tf, tl, (int32_t)(c.ms_launch_id++), (int32_t)tcap, dp.ncls, dp.missing, dp.reorder_always,
+             dp.out, c.ms_force_stream};
+  return true;
+}
+
+static bool ms_coop_launch(Ctx& c, const SegTab& T, int passes, DevPasses dp = DevPasses{}) {
+  ms_init(c);
+  McArgs A;
+  if (!ms_args(c, T, passes, dp, c.ms_coop_grid, next_barrier(c), A)) return false;
   cudaEvent_t e0, e1;
   MSG_CUDA(cudaEventCreate(&e0));
   MSG_CUDA(cudaEventCreate(&e1));
   c.ev_pool.push_back(e0);
   c.ev_pool.push_back(e1);
   MSG_CUDA(cudaEventRecord(e0, c.st));
-  McArgs A{src0 - a, c.order[c.cur].p, c.order[c.cur ^ 1].p, n, a, T, c.ms_hist.p,
-           c.ms_hist.p + 256 * (int64_t)coop_grid, c.ms_tot_par, next_barrier(c), E, (int32_t)vcap, (int32_t)nch,
-           passes, tf, tl, (int32_t)(c.ms_launch_id++), (int32_t)tcap, dp.ncls, dp.missing, dp.reorder_always,
-           dp.out, c.ms_force_stream};
   void* args[] = {&A};
-  MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(coop_grid), dim3(MC_THREADS), args,
-                                       MC_SMEM, c.st));
+  MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_ms_coop), dim3(c.ms_coop_grid), dim3(MC_THREADS),
+                                       args, MC_SMEM, c.st));
   MSG_CHECK_LAUNCH();
   add_launches(1);
   MSG_CUDA(cudaEventRecord(e1, c.st));
   c.busy_ms.push_back({e0, e1});
+  c.ms_events_pending = true;
   return true;
 }
 
 // host bookkeeping once the number of passes a cooperative launch ran is known
 static void ms_coop_done(Ctx& c, int passes) {
+  if (c.ms_events_pending) c.stats.ms_ev_passes += std::max(passes, 0);
+  c.ms_events_pending = false;
   if (passes <= 0) return;
   c.cur ^= passes & 1;
   c.head = 0;
@@ -2358,6 +2424,7 @@ static void multisplit(Ctx& c, const SegTab& T, int passes) {
   MSG_CUDA(cudaEventRecord(e1, c.st));
   c.busy_ms.push_back({e0, e1});
   c.stats.ms_passes += passes;
+  c.stats.ms_ev_passes += passes;
   c.stats.ms_bytes += 8 * n * passes;
 }
 
@@ -2405,7 +2472,7 @@ __device__ __forceinline__ void evict_body(const int32_t* __restrict__ order, in
     for (int k = 0; k < EV_ILP; ++k) {
       const int64_t e = e0 + k * stride + threadIdx.x;
       v[k] = e < n;
-      p[k] = v[k] ? order[e] : 0;
+      p[k] = v[k] ? __ldcg(order + e) : 0;
     }
 #pragma unroll
     for (int k = 0; k < EV_ILP; ++k) f[k] = v[k] ? frame[p[k]] : -1;
@@ -2450,11 +2517,11 @@ __device__ __forceinline__ void install_body(const int32_t* __restrict__ pages, 
     for (int k = 0; k < IN_ILP; ++k) {
       const int64_t j = j0 + k * stride + threadIdx.x;
       v[k] = j < n;
-      p[k] = v[k] ? pages[j] : 0;
+      p[k] = v[k] ? __ldcg(pages + j) : 0;
       int64_t q = fifo_head + j;
       if (q >= C) q -= C;
       if (q >= C) q -= C;
-      f[k] = v[k] ? fifo[q] : -1;
+      f[k] = v[k] ? __ldcg(fifo + q) : -1;
     }
 #pragma unroll
     for (int k = 0; k < IN_ILP; ++k) {
@@ -2490,13 +2557,13 @@ struct ListSel {
   int32_t* cur; int32_t* other; int64_t head; const int64_t* passes_dev;
 };
 __device__ __forceinline__ int32_t* sel_base(const ListSel& L) {
-  const int64_t p = L.passes_dev ? *L.passes_dev : 0;
+  const int64_t p = L.passes_dev ? __ldcg(L.passes_dev) : 0;
   return p > 0 ? ((p & 1) ? L.other : L.cur) : L.cur + L.head;
 }
 // the plan fits (populate <= free frames + evictions, engine.py:338-339);
 // otherwise nothing is applied and the host reports the error
 __device__ __forceinline__ bool plan_fits(const DevState* S, int64_t C, int64_t len0) {
-  return S->populate <= C - len0 + S->evict;
+  return __ldcg(&S->populate) <= C - len0 + __ldcg(&S->evict);
 }
 // S != nullptr: the switch plan's counts (S->evict / S->populate), applied
 // only when the plan fits; S == nullptr (touch installs): n_host evictions
@@ -2516,7 +2583,7 @@ __global__ void k_install_dev(const int32_t* __restrict__ pages, ListSel L, cons
                Epochs{nullptr, nullptr, 0, nullptr}, 0);
 }
 
-// results gathered into the pinned readback buffer (see k_pack / k_apply_coop)
+// results gathered into the pinned readback buffer (see k_pack / apply_body)
 struct PackSeg { const int64_t* src; int32_t words; int32_t dst_word; };
 struct PackArgs { PackSeg seg[6]; int32_t nseg; int64_t* dst; };
 
@@ -2544,21 +2611,26 @@ struct ApplyArgs {
 };
 constexpr int AP_SPLIT = 8;   // blocks' worth of work per command in the touch scan
 
-__global__ void __launch_bounds__(256) k_apply_coop(ApplyArgs A) {
+// The apply: the last phase of the per-switch cooperative kernel
+// (k_switch_coop).  The counts and lists it reads may come from earlier
+// phases of the same kernel, so they are read from L2 (ld.cg), never from a
+// stale L1 line.  red: blockDim / 32 words of shared memory.
+__device__ __forceinline__ void apply_body(const ApplyArgs& A, int& nbar, unsigned long long* red) {
   if (blockIdx.x == 0)
     for (int i = threadIdx.x; i < A.tc_n; i += blockDim.x) A.tc[i] = 0;
   const bool fits = A.S == nullptr || plan_fits(A.S, A.C, A.len0);
-  const int64_t ev = A.S ? (fits ? A.S->evict : 0) : A.ev_host;
+  const int64_t ev = A.S ? (fits ? __ldcg(&A.S->evict) : 0) : A.ev_host;
   int32_t* base = sel_base(A.L);
   evict_body(base, ev, A.bits, A.frame, A.fifo, A.fifo_tail, A.C, nullptr, Epochs{nullptr, nullptr, 0, nullptr});
-  grid_barrier(A.bar, 0);
-  const int64_t np = A.S ? (fits ? A.S->populate : 0) : *A.np_dev;
+  grid_barrier(A.bar, nbar++);
+  SWTS(3);
+  const int64_t np = A.S ? (fits ? __ldcg(&A.S->populate) : 0) : (A.np_dev ? __ldcg(A.np_dev) : 0);
   install_body(A.pages, np, A.bits, A.frame, A.fifo, A.fifo_head, A.C, base + A.len0, nullptr,
                Epochs{nullptr, nullptr, 0, nullptr}, 0);
-  grid_barrier(A.bar, 1);
+  grid_barrier(A.bar, nbar++);
+  SWTS(4);
   // touch scan: (command, split) work items over the blocks; each item strides
   // the command's bitmap words like k_touch_counts' blockIdx.x
-  __shared__ unsigned long long red[8];
   for (int item = blockIdx.x; item < A.tc_n * AP_SPLIT; item += gridDim.x) {
     const int32_t cmd = A.tc_c0 + item / AP_SPLIT, split = item % AP_SPLIT;
     const int64_t i0 = A.act_off[cmd], i1 = A.act_off[cmd + 1];
@@ -2570,7 +2642,7 @@ __global__ void __launch_bounds__(256) k_apply_coop(ApplyArgs A) {
       const int64_t lo = v.d, hi = v.d + (v.b - v.a), w0 = lo >> 5, nw = ((hi + 31) >> 5) - w0;
       int64_t k = (me - skip) % T;
       if (k < 0) k += T;
-      for (; k < nw; k += T) acc += __popc(~A.bits[w0 + k] & unit_mask(lo, hi, w0 + k));
+      for (; k < nw; k += T) acc += __popc(~__ldcg(A.bits + w0 + k) & unit_mask(lo, hi, w0 + k));
       skip += nw;
     }
     acc = __reduce_add_sync(0xffffffffu, (unsigned)acc);
@@ -2584,11 +2656,45 @@ __global__ void __launch_bounds__(256) k_apply_coop(ApplyArgs A) {
     __syncthreads();
   }
   if (A.pack.dst == nullptr) return;
-  grid_barrier(A.bar, 2);
+  grid_barrier(A.bar, nbar++);
+  SWTS(5);
   if (blockIdx.x == 0)
     for (int s = 0; s < A.pack.nseg; ++s)
       for (int i = threadIdx.x; i < A.pack.seg[s].words; i += blockDim.x)
-        A.pack.dst[A.pack.seg[s].dst_word + i] = A.pack.seg[s].src[i];
+        A.pack.dst[A.pack.seg[s].dst_word + i] = __ldcg(A.pack.seg[s].src + i);
+  SWTS(7);
+}
+
+
+// The async switch path's device work after the window kernel as ONE
+// cooperative launch: the units plan (missing = demand - resident, the plan
+// scalars, the populate list; or a faulting command's missing list), the
+// multisplit (pass count read on the device), then evict, install, the touch
+// scan and the result gather -- grid barriers between the phases, all on one
+// barrier counter, one CTA per SM with the multisplit's shared memory.
+struct SwitchArgs {
+  UnitsPlan up;
+  McArgs ms;
+  ApplyArgs ap;
+  int32_t has_up, has_ms;
+};
+
+__global__ void __launch_bounds__(MC_THREADS, 1) k_switch_coop(SwitchArgs A) {
+  extern __shared__ __align__(16) unsigned char sw_raw[];
+  __shared__ unsigned long long red[MC_WARPS];
+  int nbar = 0;
+  SWTS(0);
+  if (A.has_up) {
+    units_plan_body(A.up, sw_raw, nbar);
+    grid_barrier(A.ap.bar, nbar++);
+  }
+  SWTS(1);
+  if (A.has_ms) {
+    ms_coop_body(A.ms, sw_raw, nbar);
+    grid_barrier(A.ap.bar, nbar++);
+  }
+  SWTS(2);
+  apply_body(A.ap, nbar, red);
 }
 
 // MSG_F_EXECUTE: populate position of every page installed by this switch,
@@ -2657,21 +2763,23 @@ static void pack_to_host(Ctx& c, PackArgs& A) {
   add_launches(1);
 }
 
-// the cooperative apply (evict, install, touch scan, result gather), with a
-// grid sized to the work and bounded by co-residency
-static void apply_coop(Ctx& c, ApplyArgs& A, int64_t work_ub) {
-  if (!c.ap_grid) {
+// grid of the per-switch cooperative kernel (one CTA per SM)
+static int sw_grid(Ctx& c) {
+  if (!c.sw_grid) {
+    MSG_CUDA(cudaFuncSetAttribute(k_switch_coop, cudaFuncAttributeMaxDynamicSharedMemorySize, MC_SMEM));
     int per_sm = 0;
-    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_apply_coop, 256, 0));
+    MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_switch_coop, MC_THREADS, MC_SMEM));
     if (!c.nsm) MSG_CUDA(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, c.device));
-    c.ap_grid = std::max(1, per_sm) * std::max(1, c.nsm);
+    c.sw_grid = per_sm * c.nsm;
   }
-  const int64_t want = std::max<int64_t>((work_ub + 4 * 256 - 1) / (4 * 256), (int64_t)A.tc_n * AP_SPLIT);
-  const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(want, c.ap_grid));
-  A.bar = next_barrier(c);
-  if (A.pack.nseg) MSG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&A.pack.dst), c.hbuf.p, 0));
+  return c.sw_grid;
+}
+
+static void switch_launch(Ctx& c, SwitchArgs& A) {
+  if (A.ap.pack.nseg) MSG_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&A.ap.pack.dst), c.hbuf.p, 0));
   void* args[] = {&A};
-  MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_apply_coop), dim3(grid), dim3(256), args, 0, c.st));
+  MSG_CUDA(cudaLaunchCooperativeKernel(reinterpret_cast<void*>(k_switch_coop), dim3(sw_grid(c)), dim3(MC_THREADS),
+                                       args, MC_SMEM, c.st));
   MSG_CHECK_LAUNCH();
   add_launches(1);
 }
@@ -3051,22 +3159,30 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     MSG_CHECK_LAUNCH();
     add_launches(1);
   }
+  // ---- async path: plain replays (no copies, no executed commands, no
+  // debug dumps) run the plan, the multisplit (its pass count decided on the
+  // device) and the apply as one cooperative launch behind the window
+  // kernel, and the host syncs once, at the end
+  const bool async = !(c.cfg.flags & (MSG_F_MIGRATE | MSG_F_VERIFY_TAGS | MSG_F_EXECUTE)) && !c.debug &&
+                     ms_coop_fits(c, sw_grid(c));
   // missing = demand - resident, gating counts, plan scalars, populate list
-  units_plan(c, R, units_cap, ncw ? pref_d : nullptr, ncw, c.C, poplist.p, c.C, total_d);
+  if (!async) units_plan(c, R, units_cap, ncw ? pref_d : nullptr, ncw, c.C, poplist.p, c.C, total_d);
   pc.mark(1);   // plan launch (host)
   int64_t* hb = c.hbuf.p;
-  // ---- async path: plain replays (no copies, no executed commands, no
-  // debug dumps) run phase B straight behind phase A on the device -- the
-  // multisplit decides its pass count and the apply kernels their counts
-  // from device state -- and the host syncs once, at the end
-  if (!(c.cfg.flags & (MSG_F_MIGRATE | MSG_F_VERIFY_TAGS | MSG_F_EXECUTE)) && !c.debug && ms_coop_fits(c)) {
+  if (async) {
     compact_if_needed(c);
     const int64_t len0 = c.len, head0 = c.head, fifo_head0 = c.fifo_head, fifo_len0 = c.fifo_len;
     const int cur0 = c.cur;
     int64_t* passes_d = &c.dstate->aux[2];
-    // (units_plan zeroed the pass-count slot with the plan scalars)
-    if (len0 > 0)
-      ms_coop_launch(c, wp.tab, 0, DevPasses{wp.ncls, &c.dstate->missing, reorder_always ? 1 : 0, passes_d});
+    const int G = sw_grid(c);
+    int32_t* bar = next_barrier(c);
+    SwitchArgs SA{};
+    // (the plan phase zeroes the pass-count slot with the plan scalars)
+    SA.up = units_plan_args(c, R, G, ncw ? pref_d : nullptr, ncw, c.C, poplist.p, c.C, total_d, bar);
+    SA.has_up = 1;
+    SA.has_ms = len0 > 0 &&
+                ms_args(c, wp.tab, 0, DevPasses{wp.ncls, &c.dstate->missing, reorder_always ? 1 : 0, passes_d}, G,
+                        bar, SA.ms);
     pc.mark(3);
     const ListSel L{c.order[cur0].p, c.order[cur0 ^ 1].p, head0, passes_d};
     // evict, install, the slice's touch scan and the result gather: one launch
@@ -3087,7 +3203,9 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
       AA.pack.seg[AA.pack.nseg++] = PackSeg{c.s.tc.p, ncw, nwin + ncw};
     }
     AA.pack.seg[AA.pack.nseg++] = PackSeg{reinterpret_cast<const int64_t*>(c.dstate), kStateWords, nwin + 2 * ncw};
-    apply_coop(c, AA, std::max(len0, std::min<int64_t>(32 * units_cap, c.C)));
+    AA.bar = bar;
+    SA.ap = AA;
+    switch_launch(c, SA);
     pc.mark(4);
     MSG_CUDA(cudaEventRecord(e1, st));
     pc.mark(6);
@@ -3135,6 +3253,12 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     cudaEventDestroy(e0); cudaEventDestroy(e1);
     return;
   }
+  // the reorder is queued behind the plan before the host round trip, its
+  // pass count read on the device (0 on an early exit), so it starts on a
+  // busy stream instead of after the host's launch latency
+  const bool pre_ms = !c.debug && c.len > 0 && ms_coop_fits(c) &&
+                      ms_coop_launch(c, wp.tab, 0, DevPasses{wp.ncls, &c.dstate->missing, reorder_always ? 1 : 0,
+                                                             &c.dstate->aux[2]});
   MSG_CUDA(cudaMemcpyAsync(c.hstate, c.dstate, sizeof(DevState), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(hb, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   MSG_CUDA(cudaMemcpyAsync(hb + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -3142,6 +3266,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   MSG_CUDA(cudaStreamSynchronize(st));
   pc.mark(2);   // first sync (device phase A)
   DevState S = hs(c);
+  if (pre_ms) ms_coop_done(c, (int)S.aux[2]);   // (before any error below: the list is reordered)
   for (int w = 0; w < nwin; ++w) win_pages[w] = hb[w];
   for (int k = 0; k < ncw; ++k) prefix[k] = hb[nwin + 1 + k];
   int64_t ncls = hb[nwin];
@@ -3157,10 +3282,7 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     int64_t pop = S.populate, ev = S.evict;
     out->populate = pop; out->evict = ev; out->truncated = S.truncated;
     if (pop > c.C - c.len + ev) throw Error(MSG_E_CAPACITY, "migration plan overflowed HBM capacity");
-    // (launching the reorder before this host round trip, with the pass
-    // count taken on the device, measured no faster: the gap between the
-    // planner events and the kernel is the cooperative launch itself)
-    multisplit(c, wp.tab, passes_for(ncls));
+    if (!pre_ms) multisplit(c, wp.tab, passes_for(ncls));
     pc.mark(3);   // multisplit launch (host)
     if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     out->free_before = c.C - c.len;
@@ -3241,7 +3363,7 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   const bool refresh = evict > 0 && nwin > 0;
   // the async path gathers its results with one launch at the end
   const bool async = !(c.cfg.flags & (MSG_F_MIGRATE | MSG_F_VERIFY_TAGS | MSG_F_EXECUTE)) && !c.debug &&
-                     ms_coop_fits(c);
+                     ms_coop_fits(c, sw_grid(c));
   RangeSet R{};
   int64_t* hb = c.hbuf.p;
   if (has_iv) {
@@ -3250,15 +3372,23 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     c.s.uscr.resize(512, st);
     c.s.miss.resize(std::max<int64_t>(32 * nu, 1), st);
     R = c.s.ract.set();
-    units_plan(c, R, nu, nullptr, 0, -1, c.s.miss.p, -1, c.s.uscr.p + 400);
-    if (!async) MSG_CUDA(cudaMemcpyAsync(hb, c.s.uscr.p + 400, 8, cudaMemcpyDeviceToHost, st));
+    if (!async) {   // (the async path runs the plan inside its cooperative launch)
+      units_plan(c, R, nu, nullptr, 0, -1, c.s.miss.p, -1, c.s.uscr.p + 400);
+      MSG_CUDA(cudaMemcpyAsync(hb, c.s.uscr.p + 400, 8, cudaMemcpyDeviceToHost, st));
+    }
   }
   WinBuild wb;
   WinPtrs wp{};
+  bool pre_ms = false;   // synchronous path: the refresh reorder queued before the host round trip
   if (refresh) {
     build_windows(c, win, nwin, wb);
     wp = win_ptrs(c, nwin, wb);
     if (!async) {
+      if (!c.debug && c.len > 0 && ms_coop_fits(c)) {
+        MSG_CUDA(cudaMemsetAsync(&c.dstate->aux[2], 0, sizeof(int64_t), st));
+        pre_ms = ms_coop_launch(c, wp.tab, 0, DevPasses{wp.ncls, nullptr, 0, &c.dstate->aux[2]});
+        if (pre_ms) MSG_CUDA(cudaMemcpyAsync(hb + 2 + nwin, &c.dstate->aux[2], 8, cudaMemcpyDeviceToHost, st));
+      }
       MSG_CUDA(cudaMemcpyAsync(hb + 1, wp.pages, nwin * sizeof(int64_t), cudaMemcpyDeviceToHost, st));
       MSG_CUDA(cudaMemcpyAsync(hb + 1 + nwin, wp.ncls, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
     }
@@ -3272,19 +3402,22 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     const int cur0 = c.cur;
     int64_t* passes_d = &c.dstate->aux[2];
     MSG_CUDA(cudaMemsetAsync(passes_d, 0, sizeof(int64_t), st));
-    if (evict > 0 && refresh && len0 > 0) ms_coop_launch(c, wp.tab, 0, DevPasses{wp.ncls, nullptr, 0, passes_d});
+    const int G = sw_grid(c);
+    int32_t* bar = next_barrier(c);
+    SwitchArgs SA{};
+    // the command's missing list (plan phase), the refresh multisplit, then
+    // evict, install, the rescan and the result gather: one launch
+    // (results: n | win pages | ncls slot (unused) | passes | touch counts)
+    if (has_iv) SA.up = units_plan_args(c, R, G, nullptr, 0, -1, c.s.miss.p, -1, c.s.uscr.p + 400, bar);
+    SA.has_up = has_iv ? 1 : 0;
+    SA.has_ms = evict > 0 && refresh && len0 > 0 &&
+                ms_args(c, wp.tab, 0, DevPasses{wp.ncls, nullptr, 0, passes_d}, G, bar, SA.ms);
     const ListSel L{c.order[cur0].p, c.order[cur0 ^ 1].p, head0, passes_d};
     const int64_t ev_done = evict > 0 ? std::min(evict, len0) : 0;
     const int32_t lo = cmd + 1, hi = scan_end;
-    // evict, install, the rescan and the result gather: one launch
-    // (results: n | win pages | ncls slot (unused) | passes | touch counts)
     c.s.tc.resize(std::max(hi - lo, 1), st);
-    if (!has_iv) {
-      c.s.uscr.resize(512, st);
-      MSG_CUDA(cudaMemsetAsync(c.s.uscr.p + 400, 0, sizeof(int64_t), st));
-    }
     ApplyArgs AA{};
-    AA.L = L; AA.S = nullptr; AA.ev_host = ev_done; AA.np_dev = c.s.uscr.p + 400; AA.len0 = len0;
+    AA.L = L; AA.S = nullptr; AA.ev_host = ev_done; AA.np_dev = has_iv ? c.s.uscr.p + 400 : nullptr; AA.len0 = len0;
     AA.bits = c.bits.p; AA.frame = c.frame.p; AA.fifo = c.fifo.p;
     AA.fifo_tail = fifo_head0 + fifo_len0; AA.fifo_head = fifo_head0; AA.C = c.C;
     AA.pages = c.s.miss.p;
@@ -3294,8 +3427,9 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     if (refresh) AA.pack.seg[AA.pack.nseg++] = PackSeg{wp.pages, nwin, 1};
     AA.pack.seg[AA.pack.nseg++] = PackSeg{passes_d, 1, 2 + nwin};
     if (hi > lo) AA.pack.seg[AA.pack.nseg++] = PackSeg{c.s.tc.p, hi - lo, 3 + nwin};
-    const int64_t nu = has_iv ? t.act_units[cmd + 1] - t.act_units[cmd] : 0;
-    apply_coop(c, AA, std::max(ev_done, 32 * nu));
+    AA.bar = bar;
+    SA.ap = AA;
+    switch_launch(c, SA);
     pc.mark(5);
     MSG_CUDA(cudaStreamSynchronize(st));
     pc.mark(6);
@@ -3340,7 +3474,8 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
   int64_t ev_done = 0;
   if (evict > 0) {
     if (refresh) {
-      multisplit(c, wp.tab, passes_for(ncls));
+      if (pre_ms) ms_coop_done(c, (int)hb[2 + nwin]);
+      else multisplit(c, wp.tab, passes_for(ncls));
       out->refreshed = 1;
       if (c.debug & 2) dump_dense(c, c.order[c.cur].p + c.head, c.len, c.dbg[0]);
     }
@@ -3799,10 +3934,17 @@ extern "C" void msg_dbg_mc_cta(unsigned long long* out) {   // 256 x 160 x 8 sta
   cudaDeviceSynchronize();
   cudaMemcpyFromSymbol(out, msg::g_mc_cta, sizeof(msg::g_mc_cta));
 }
-extern "C" void msg_dbg_fw_ts(unsigned long long* out) {   // 10 phase sums + launches
+extern "C" void msg_dbg_fw_ts(unsigned long long* out) {   // 16 phase sums + launches
   cudaDeviceSynchronize();
-  cudaMemcpyFromSymbol(out, msg::g_fw_sum, 10 * 8);
-  cudaMemcpyFromSymbol(out + 10, msg::g_fw_n, 8);
+  cudaMemcpyFromSymbol(out, msg::g_fw_sum, 16 * 8);
+  cudaMemcpyFromSymbol(out + 16, msg::g_fw_n, 8);
+}
+extern "C" void msg_dbg_sw_ts(unsigned long long* out) {   // 8 phase sums + launches
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, msg::g_sw_sum, 8 * 8);
+  cudaMemcpyFromSymbol(out + 8, msg::g_sw_n, 8);
+  cudaMemcpyFromSymbol(out + 9, msg::g_gap_sum, 8);
+  cudaMemcpyFromSymbol(out + 10, msg::g_gap_n, 8);
 }
 extern "C" void msg_dbg_mc_reset() {
   unsigned long long lo[16], hi[16] = {0}, z[16] = {0}, zn = 0;
@@ -3811,8 +3953,13 @@ extern "C" void msg_dbg_mc_reset() {
   cudaMemcpyToSymbol(msg::g_mc_max, hi, 128);
   cudaMemcpyToSymbol(msg::g_mc_sum, z, 128);
   cudaMemcpyToSymbol(msg::g_mc_n, &zn, 8);
-  unsigned long long zf[10] = {0};
+  unsigned long long zf[16] = {0};
   cudaMemcpyToSymbol(msg::g_fw_sum, zf, sizeof(zf));
   cudaMemcpyToSymbol(msg::g_fw_n, &zn, 8);
+  cudaMemcpyToSymbol(msg::g_sw_sum, zf, 8 * 8);
+  cudaMemcpyToSymbol(msg::g_sw_n, &zn, 8);
+  cudaMemcpyToSymbol(msg::g_gap_sum, &zn, 8);
+  cudaMemcpyToSymbol(msg::g_gap_n, &zn, 8);
+  cudaMemcpyToSymbol(msg::g_fw_end, &zn, 8);
 }
 #endif

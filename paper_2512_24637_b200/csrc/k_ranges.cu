@@ -61,170 +61,10 @@ __global__ void __launch_bounds__(1024, 1) k_ranges_from_iv(const Iv* pool, cons
 // unchanged) and writes its pages at their offsets, capped.  Replaces the
 // count / 3-kernel scan / scalars / fill chain (six launches).
 
-struct UnitsPlan {
-  RangeSet R;
-  const uint32_t* bits;
-  int64_t* tag_cnt;      // per-tag totals (ntags), or nullptr
-  int32_t ntags;
-  int64_t cap;           // fill cap (pages), < 0: none
-  int32_t* out;          // fill output, or nullptr
-  DevState* S;           // plan scalars, or nullptr
-  int64_t C, len;        // capacity and resident pages (for the scalars)
-  int64_t* total_out;    // missing pages, or nullptr
-  int32_t* hist;         // [gridDim] CTA totals, then [gridDim][ntags] tag partials
-  int32_t* bar;          // grid barrier counter (zero at launch)
-  int32_t stage;         // the range table fits the dynamic shared memory
-};
-
-constexpr int UP_THREADS = 512;
-constexpr int UP_MAX_TAGS = 8192;
-constexpr int UP_SMEM_RANGES = 4096;   // range tables up to this size are searched in shared memory
-
 __global__ void __launch_bounds__(UP_THREADS, 1) k_units_plan(UnitsPlan P) {
-  __shared__ int64_t ws[32];
-  __shared__ int64_t carry_s;
   extern __shared__ __align__(16) unsigned char up_raw[];
-  int32_t* tagc = reinterpret_cast<int32_t*>(up_raw);                          // ntags
-  int64_t* r_uoff = reinterpret_cast<int64_t*>(up_raw + ((4 * (int64_t)P.ntags + 15) & ~int64_t(15)));
-  int64_t* r_lo = r_uoff + UP_SMEM_RANGES + 1;
-  const int t = threadIdx.x, G = gridDim.x, b = blockIdx.x;
-  const int64_t nr = *P.R.nr;
-  const int64_t nu = nr ? P.R.uoff[nr] : 0;
-  const int64_t U = (nu + G - 1) / G;
-  const int64_t u0 = (int64_t)b * U, u1 = u0 + U < nu ? u0 + U : nu;
-  const bool staged = P.stage && nr <= UP_SMEM_RANGES;
-  for (int i = t; i < P.ntags; i += UP_THREADS) tagc[i] = 0;
-  if (staged)
-    for (int64_t i = t; i <= nr; i += UP_THREADS) {
-      r_uoff[i] = P.R.uoff[i];
-      if (i < nr) r_lo[i] = P.R.lo[i];
-    }
-  __syncthreads();
-  const int64_t* uoff = staged ? r_uoff : P.R.uoff;
-  const int64_t* rlo = staged ? r_lo : P.R.lo;
-  auto unit = [&](int64_t u, int64_t* r_out, int64_t* w_out, uint32_t* m_out) {
-    int64_t a = 0, z = nr;   // largest r with uoff[r] <= u
-    while (z - a > 1) { int64_t mid = (a + z) >> 1; if (uoff[mid] <= u) a = mid; else z = mid; }
-    // a range's units are the bitmap words it overlaps, so its end is the next range's start only
-    // as far as units go; the page extent needs len, read once per unit (cached in L1)
-    int64_t lo = rlo[a], hi = lo + P.R.len[a];
-    int64_t w = (lo >> 5) + (u - uoff[a]);
-    *r_out = a; *w_out = w; *m_out = ~P.bits[w] & unit_mask(lo, hi, w);
-  };
-  // ---- phase 1: counts
-  int64_t acc = 0;
-  for (int64_t base = u0; base < u1; base += UP_THREADS) {
-    int64_t u = base + t, r = -1, w;
-    uint32_t m = 0;
-    if (u < u1) unit(u, &r, &w, &m);
-    int c = __popc(m);
-    acc += c;
-    if (P.tag_cnt) {
-      int tag = (r >= 0 && c) ? P.R.tag[r] : -1;
-      unsigned peers = __match_any_sync(0xffffffffu, tag);
-      int sum = __reduce_add_sync(peers, (unsigned)c);
-      if (tag >= 0 && (int)(t & 31) == __ffs(peers) - 1) atomicAdd(&tagc[tag], sum);
-    }
-  }
-  int64_t tot;
-  block_scan_excl_i64(acc, ws, &tot);
-  int64_t pre_tot = 0, all_tot = tot;
-  if (G == 1) {
-    // one CTA: its totals are the grid's; no histogram round trip, no barrier
-    if (P.tag_cnt) {
-      __syncthreads();
-      for (int i = t; i < P.ntags; i += UP_THREADS) P.tag_cnt[i] = tagc[i];
-    }
-  } else {
-  if (t == 0) __stcg(P.hist + b, (int32_t)tot);
-  __syncthreads();
-  if (P.tag_cnt)
-    for (int i = t; i < P.ntags; i += UP_THREADS) __stcg(P.hist + G + (int64_t)b * P.ntags + i, tagc[i]);
-  // ---- grid barrier
-  __syncthreads();
-  if (t == 0) {   // release arrival / acquire poll at gpu scope (see k_plan.cu grid_barrier)
-    asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(P.bar) : "memory");
-    int32_t v;
-    do {
-      asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(P.bar) : "memory");
-    } while (v < G);
-  }
-  __syncthreads();
-  // ---- phase 2: offsets, totals, scalars, per-tag totals
-  int64_t pre = 0, all = 0;
-  for (int i = t; i < G; i += UP_THREADS) {
-    int64_t v = __ldcg(P.hist + i);
-    all += v;
-    if (i < b) pre += v;
-  }
-  block_scan_excl_i64(pre, ws, &pre_tot);
-  block_scan_excl_i64(all, ws, &all_tot);
-  if (P.tag_cnt) {
-    if (G <= 32) {
-      // few CTAs: one thread per tag sums the G partials (coalesced over tags)
-      for (int i = b * UP_THREADS + t; i < P.ntags; i += G * UP_THREADS) {
-        int64_t sum = 0;
-        for (int c2 = 0; c2 < G; ++c2) sum += __ldcg(P.hist + G + (int64_t)c2 * P.ntags + i);
-        P.tag_cnt[i] = sum;
-      }
-    } else {
-      // many CTAs: CTA b sums tags b, b+G, ... with all its threads (one CTA
-      // row per thread)
-      for (int i = b; i < P.ntags; i += G) {
-        int64_t part = 0;
-        for (int c2 = t; c2 < G; c2 += UP_THREADS) part += __ldcg(P.hist + G + (int64_t)c2 * P.ntags + i);
-        int64_t sum;
-        block_scan_excl_i64(part, ws, &sum);
-        if (t == 0) P.tag_cnt[i] = sum;
-      }
-    }
-  }
-  }   // G > 1
-  if (b == 0 && t == 0) {
-    if (P.total_out) *P.total_out = all_tot;
-    if (P.S) {
-      DevState* S = P.S;
-      S->missing = all_tot;
-      int64_t pop = all_tot < P.C ? all_tot : P.C;
-      S->populate = pop;
-      S->truncated = all_tot - pop;
-      S->free_before = P.C - P.len;
-      int64_t ev = pop - (P.C - P.len);
-      S->evict = ev > 0 ? ev : 0;
-      S->skip = all_tot == 0;
-      S->aux[2] = 0;   // the switch's multisplit pass count, until the multisplit publishes it
-    }
-  }
-  if (!P.out) return;
-  // ---- phase 3: fill in range order, capped.  Offsets per unit (thread per
-  // unit, block scan), then one warp writes a unit's pages with one
-  // coalesced store (lane k writes page 32w+k when missing).
-  __shared__ int64_t uo_s[UP_THREADS];
-  __shared__ int64_t uw_s[UP_THREADS];
-  __shared__ uint32_t um_s[UP_THREADS];
-  const int64_t cap = P.cap < 0 ? INT64_MAX : P.cap;
-  const int lane = t & 31, warp = t >> 5;
-  if (t == 0) carry_s = pre_tot;
-  __syncthreads();
-  for (int64_t base = u0; base < u1; base += UP_THREADS) {
-    int64_t u = base + t, r, w = 0;
-    uint32_t m = 0;
-    if (u < u1) unit(u, &r, &w, &m);
-    int64_t rt;
-    int64_t o = carry_s + block_scan_excl_i64(__popc(m), ws, &rt);
-    uo_s[t] = o; uw_s[t] = w; um_s[t] = m;
-    __syncthreads();
-    for (int k = 0; k < 32; ++k) {
-      const int i = warp * 32 + k;
-      const uint32_t mk = um_s[i];
-      if (!mk) continue;
-      const int64_t ok = uo_s[i] + __popc(mk & ((1u << lane) - 1u));
-      if (((mk >> lane) & 1u) && ok < cap) P.out[ok] = (int32_t)((uw_s[i] << 5) + lane);
-    }
-    __syncthreads();
-    if (t == 0) carry_s += rt;
-    __syncthreads();
-  }
+  int nbar = 0;
+  units_plan_body(P, up_raw, nbar);
 }
 
 // per command of [c0, c1) of a task: missing pages of its actual set against
@@ -269,10 +109,19 @@ void touch_counts_dev(Ctx& c, TaskTab& t, int32_t lo, int32_t hi, int64_t* out) 
   add_launches(1);
 }
 
+UnitsPlan units_plan_args(Ctx& c, const RangeSet& R, int32_t grid, int64_t* tag_cnt, int32_t ntags, int64_t cap,
+                          int32_t* out, int64_t plan_capacity, int64_t* total_out, int32_t* bar) {
+  if (ntags > UP_MAX_TAGS) throw Error(MSG_E_INVAL, "too many commands in one window for the units plan");
+  c.up_hist.resize((int64_t)grid * (1 + std::max(ntags, 0)) + 1, c.st);
+  const int nt = tag_cnt ? ntags : 0;
+  return UnitsPlan{R, c.bits.p, tag_cnt, nt, cap, out, plan_capacity >= 0 ? c.dstate : nullptr,
+                   plan_capacity, c.len, total_out, c.up_hist.p, bar, 1};
+}
+
 void units_plan(Ctx& c, const RangeSet& R, int64_t units_cap, int64_t* tag_cnt, int32_t ntags, int64_t cap,
                 int32_t* out, int64_t plan_capacity, int64_t* total_out) {
   if (c.up_per_sm < 0) {
-    const int max_smem = 4 * UP_MAX_TAGS + 16 * (UP_SMEM_RANGES + 1) + 64;
+    const int max_smem = (int)units_plan_smem(UP_MAX_TAGS, UP_THREADS);
     MSG_CUDA(cudaFuncSetAttribute(k_units_plan, cudaFuncAttributeMaxDynamicSharedMemorySize, max_smem));
     MSG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&c.up_per_sm, k_units_plan, UP_THREADS, max_smem));
     MSG_CUDA(cudaDeviceGetAttribute(&c.nsm, cudaDevAttrMultiProcessorCount, c.device));
@@ -282,7 +131,7 @@ void units_plan(Ctx& c, const RangeSet& R, int64_t units_cap, int64_t* tag_cnt, 
   int G = (int)std::min<int64_t>(std::max<int64_t>((units_cap + 511) / 512, 1), (int64_t)std::max(per_sm, 1) * sms);
   c.up_hist.resize((int64_t)G * (1 + std::max(ntags, 0)) + 1, c.st);
   const int nt = tag_cnt ? ntags : 0;
-  const size_t smem = ((4 * (size_t)nt + 15) & ~size_t(15)) + 16 * ((size_t)UP_SMEM_RANGES + 1);
+  const size_t smem = units_plan_smem(nt, UP_THREADS);
   UnitsPlan P{R, c.bits.p, tag_cnt, nt, cap, out, plan_capacity >= 0 ? c.dstate : nullptr,
               plan_capacity, c.len, total_out, c.up_hist.p, next_barrier(c), 1};
   void* args[] = {&P};

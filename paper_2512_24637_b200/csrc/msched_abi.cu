@@ -425,6 +425,7 @@ int msg_get_stats(msg_ctx* ctx, msg_stats* out) {
     cudaGetLastError();
     s.ms_ms = m;
     s.ms_dev_launches = c.stats.ms_dev_launches;
+    s.ms_ev_passes = c.stats.ms_ev_passes;
     s.ms_dev_ms = c.ms_dev_ms_acc;
     *out = s;
   });

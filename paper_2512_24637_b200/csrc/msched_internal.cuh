@@ -261,6 +261,7 @@ struct Ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_h2d, busy_d2h;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> busy_plan, busy_ms, busy_run;
   msg_stats stats{};
+  bool ms_events_pending = false;   // a standalone multisplit launch awaits its pass count (stats)
   // parity dumps
   int debug = 0;   // 1: plan lists, 2: full list orders
   int fallback = 0;   // MSG_FALLBACK test hook: 1 two-kernel windows, 2 look-back multisplit, 4 demand kernel
@@ -276,7 +277,7 @@ struct Ctx {
   double ms_dev_ms_acc = 0.0;
   // per-device kernel setup (dynamic shared memory attributes are per device)
   bool win_init = false;
-  int ms_grid_cap = 0, ms_coop_grid = 0, up_per_sm = -1, nsm = 0, ap_grid = 0;
+  int ms_grid_cap = 0, ms_coop_grid = 0, up_per_sm = -1, nsm = 0, sw_grid = 0;
   int ms_force_stream = 0;            // MSG_MS_STREAM=1 (tuning / test hook)
   uint32_t ms_epoch = 0;
   int64_t ms_launch_id = 0;           // cooperative multisplit launches (phase-timing build)

@@ -42,7 +42,7 @@ int main(void) {
   S(msg_switch_out) S(msg_touch_out) S(msg_stats)
   O(msg_cmd, dims) O(msg_cmd, dev_addr) O(msg_rule, e) O(msg_expr, slot) O(msg_arg, raw_off)
   O(msg_switch_out, first_missing_pages) O(msg_touch_out, next_missing_pages) O(msg_stats, ms_bytes)
-  O(msg_cfg, flags) O(msg_stats, run_ms) O(msg_stats, ms_dev_ms)
+  O(msg_cfg, flags) O(msg_stats, run_ms) O(msg_stats, ms_dev_ms) O(msg_stats, ms_ev_passes)
   return 0;
 }
 """)
@@ -71,6 +71,7 @@ def test_struct_layouts_match_header(tmp_path):
     assert c["msg_stats"] == ctypes.sizeof(_abi.Stats) and c["msg_stats.ms_bytes"] == _abi.Stats.ms_bytes.offset
     assert c["msg_stats.run_ms"] == _abi.Stats.run_ms.offset
     assert c["msg_stats.ms_dev_ms"] == _abi.Stats.ms_dev_ms.offset
+    assert c["msg_stats.ms_ev_passes"] == _abi.Stats.ms_ev_passes.offset
 
 
 def test_slot_codes_and_rule_lowering():

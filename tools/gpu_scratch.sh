@@ -1,2 +1,10 @@
-timeout 1800 python -m pytest tests -q -m gpu -p no:cacheprovider -x > gpurun_out/r2_pytest_gpu24.txt 2>&1; tail -3 gpurun_out/r2_pytest_gpu24.txt; grep -E "^FAILED|^E " gpurun_out/r2_pytest_gpu24.txt | head
-timeout 300 python tools/prof_replay.py cfg2 3 | tail -1; timeout 300 python tools/prof_replay.py cfg4 2 | tail -1; timeout 300 python tools/prof_replay.py cfg1 3 | tail -1; timeout 300 python tools/prof_replay.py cfg3 3 | tail -1; timeout 300 python tools/prof_replay.py frag 2 | tail -1
+O=gpurun_out/p7; mkdir -p $O
+timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gpu_tests.log 2>&1; tail -4 $O/gpu_tests.log
+timeout 1500 python bench.py --steps 3 --warmup 3 --skip-execute --skip-frag > $O/bench.jsonl 2> $O/bench.err; python - <<'P'
+import json
+d=json.loads(open("gpurun_out/p7/bench.jsonl").read().strip().splitlines()[-1])
+print(d["value"], d["ms_per_step"], json.dumps(d["roofline"])[:600])
+print(json.dumps(d.get("plan_only",{}))[:500])
+print(json.dumps(d.get("cfg2",{}).get("roofline",{}))[:500])
+P
+tail -3 $O/bench.err

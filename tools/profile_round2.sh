@@ -21,16 +21,18 @@ done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_cfg2_migrate.csv \
     python tools/prof_replay.py cfg2 1 --migrate > /dev/null 2>&1
 python tools/launch_summary.py $O/launches_cfg2_migrate.csv > $O/launches_cfg2_migrate_summary.txt
-for k in k_windows_fused k_units_plan k_apply_coop k_ranges_from_iv; do
+for k in k_windows_fused k_switch_coop k_ranges_from_iv; do
   timeout 900 ncu --set full --import-source on --clock-control none -f -k regex:$k -s 30 -c 1 -o $O/ncu_${k}_cfg4 \
       python tools/prof_replay.py cfg4 1 > /dev/null 2>&1
 done
-# several consecutive multisplit launches: a switch that exits early launches one that runs no pass
-timeout 900 ncu --set full --import-source on --clock-control none -f -k regex:k_ms_coop -s 30 -c 6 -o $O/ncu_k_ms_coop_cfg4 \
-    python tools/prof_replay.py cfg4 1 > /dev/null 2>&1
+# the standalone multisplit launches of the migrating (headline) replay; several consecutive ones
+timeout 1800 ncu --set full --import-source on --clock-control none -f -k regex:k_ms_coop -s 30 -c 4 -o $O/ncu_k_ms_coop_cfg4 \
+    python tools/prof_replay.py cfg4 1 --migrate > /dev/null 2>&1
 timeout 900 ncu --set full --import-source on --clock-control none -f -k regex:k_ms_coop -s 40 -c 1 -o $O/ncu_k_ms_coop_cfg2 \
+    python tools/prof_replay.py cfg2 1 --migrate > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -f -k regex:k_switch_coop -s 40 -c 1 -o $O/ncu_k_switch_coop_cfg2 \
     python tools/prof_replay.py cfg2 1 > /dev/null 2>&1
-for k in k_window_combine_wide k_window_runs k_ms_coop; do
+for k in k_window_combine_wide k_window_runs k_switch_coop; do
   timeout 900 ncu --set full --import-source on --clock-control none -f -k regex:$k -s 200 -c 1 -o $O/ncu_${k}_frag \
       python tools/prof_replay.py frag 1 > /dev/null 2>&1
 done

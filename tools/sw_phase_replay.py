@@ -1,5 +1,6 @@
-"""k_windows_fused phase timings over one replay (needs `make phase-ts`; GPU box):
-mean SM cycles from the kernel's first stamp to each phase boundary."""
+"""k_switch_coop phase timings over one replay (needs `make phase-ts`; GPU box):
+mean ns from the kernel's start (block 0) to each phase boundary; every
+boundary but the last is taken after a grid barrier."""
 import ctypes as C
 import sys
 
@@ -22,15 +23,14 @@ lib.msg_dbg_mc_reset()
 sim.reset()
 sim.run()
 sim.ctx.sync()
-out = (C.c_ulonglong * 17)()
-lib.msg_dbg_fw_ts(out)
-n = max(out[16], 1)
-names = {0: "start", 1: "intervals", 2: "endpoints", 3: "labels", 4: "runs", 5: "run order", 6: "demand",
-         7: "class start", 8: "E2 sorted", 9: "E2 compact", 10: "painted", 11: "keys folded", 12: "tuples sorted",
-         13: "ranked", 15: "end"}
-print(f"{cfg}: {out[16]} launches; mean SM cycles (and us at 1965 MHz) since the kernel's first stamp")
+out = (C.c_ulonglong * 11)()
+lib.msg_dbg_sw_ts(out)
+n = max(out[8], 1)
+names = {0: "start", 1: "units plan", 2: "multisplit", 3: "evict", 4: "install", 5: "touch scan", 7: "gather"}
+print(f"{cfg}: {out[8]} launches; mean us since the kernel's start")
 prev = 0.0
 for i, nm in names.items():
-    v = out[i] / n
-    print(f"  {nm:14s} {v:8.0f} cyc {v / 1965:6.2f} us  (+{(v - prev) / 1965:5.2f})")
+    v = out[i] / n / 1e3
+    print(f"  {nm:12s} {v:7.2f}  (+{v - prev:5.2f})")
     prev = v
+print(f"  window kernel end -> switch kernel start: {out[9] / max(out[10], 1) / 1e3:.2f} us (over {out[10]} launches)")
