@@ -212,6 +212,12 @@ int msg_add_commands(msg_ctx *ctx, int32_t task, int32_t ncmd, const msg_cmd *cm
  * Call with runs=NULL to get the count. */
 int msg_read_pages(msg_ctx *ctx, int32_t task, int32_t cmd, int32_t which, int64_t *runs, int64_t cap,
                    int64_t *nruns);
+/* The same for commands [c0, c1) in one device-to-host copy: runs of
+ * command c0 + k are runs[2 * off[k] .. 2 * off[k + 1]) (off: c1 - c0 + 1
+ * entries).  Call with runs=NULL to get the total in *nruns (off is filled
+ * either way; pass off=NULL to skip it). */
+int msg_read_pages_range(msg_ctx *ctx, int32_t task, int32_t c0, int32_t c1, int32_t which, int64_t *runs,
+                         int64_t cap, int64_t *off, int64_t *nruns);
 
 /* One proactive switch.  win[0] is the incoming slice; win_pages_out
  * (nwin entries) receives |window pages| for madvise_cost_s; prefix_out

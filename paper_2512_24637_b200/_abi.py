@@ -23,7 +23,7 @@ F_MIGRATE, F_VERIFY_TAGS, F_LOOSE_DOMAIN, F_EXECUTE = 1, 2, 4, 8
 
 EXPORTS = [
     "msg_create", "msg_destroy", "msg_last_error", "msg_stream", "msg_set_domain", "msg_add_task",
-    "msg_set_rules", "msg_add_commands", "msg_read_pages", "msg_plan_switch", "msg_touch",
+    "msg_set_rules", "msg_add_commands", "msg_read_pages", "msg_read_pages_range", "msg_plan_switch", "msg_touch",
     "msg_um_slice", "msg_release_task", "msg_list_append", "msg_list_madvise", "msg_list_evict_head",
     "msg_list_len", "msg_list_read", "msg_sync", "msg_get_stats", "msg_verify_residency",
     "msg_flush_l2", "msg_list_reorder", "msg_debug", "msg_debug_read", "msg_window_runs", "msg_list_plan", "msg_reset",
@@ -108,6 +108,7 @@ def load():
         "msg_set_rules": ([vp, i32, vp, vp, i32], C.c_int),
         "msg_add_commands": ([vp, i32, i32, vp, vp, vp, i64, vp, vp], C.c_int),
         "msg_read_pages": ([vp, i32, i32, i32, vp, i64, C.POINTER(i64)], C.c_int),
+        "msg_read_pages_range": ([vp, i32, i32, i32, i32, vp, i64, vp, C.POINTER(i64)], C.c_int),
         "msg_plan_switch": ([vp, vp, i32, i32, C.POINTER(SwitchOut), vp, vp, vp], C.c_int),
         "msg_touch": ([vp, i32, i32, i64, vp, i32, i32, i32, C.POINTER(TouchOut), vp], C.c_int),
         "msg_um_slice": ([vp, i32, i32, i32, vp, vp], C.c_int),
@@ -371,6 +372,17 @@ class Context:
         buf = np.zeros(max(2 * n.value, 2), dtype=np.int64)
         self.check(self.lib.msg_read_pages(self.h, idx, cmd, which, _p(buf), n.value, C.byref(n)))
         return [(int(buf[2 * i]), int(buf[2 * i + 1])) for i in range(n.value)]
+
+    def read_pages_range(self, idx, c0, c1, which):
+        """Runs of commands [c0, c1) in one copy: (runs int64[n, 2], off int64[c1 - c0 + 1])."""
+        n = C.c_int64()
+        off = np.zeros(c1 - c0 + 1, dtype=np.int64)
+        self.check(self.lib.msg_read_pages_range(self.h, idx, c0, c1, which, None, 0, _p(off), C.byref(n)))
+        buf = np.zeros(max(2 * n.value, 2), dtype=np.int64)
+        if n.value:
+            self.check(self.lib.msg_read_pages_range(self.h, idx, c0, c1, which, _p(buf), n.value, None,
+                                                     C.byref(n)))
+        return buf[:2 * n.value].reshape(-1, 2), off
 
     def plan_switch(self, windows, reorder_always=False):
         nw = len(windows)

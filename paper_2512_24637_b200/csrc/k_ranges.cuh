@@ -84,7 +84,8 @@ __host__ __device__ constexpr size_t units_plan_smem(int nt, int NT) {
 // threads): block-size generic; its shared memory is the caller's dynamic
 // buffer (units_plan_smem bytes); nbar counts the grid barriers used so far
 // on P.bar.
-__device__ __forceinline__ void units_plan_body(const UnitsPlan& P, unsigned char* up_raw, int& nbar) {
+// Returns the missing total (every CTA computes it).
+__device__ __forceinline__ int64_t units_plan_body(const UnitsPlan& P, unsigned char* up_raw, int& nbar) {
   const int NT = (int)blockDim.x;
   int32_t* tagc = reinterpret_cast<int32_t*>(up_raw);                          // ntags
   int64_t* r_uoff = reinterpret_cast<int64_t*>(up_raw + ((4 * (int64_t)P.ntags + 15) & ~int64_t(15)));
@@ -118,12 +119,17 @@ __device__ __forceinline__ void units_plan_body(const UnitsPlan& P, unsigned cha
     int64_t w = (lo >> 5) + (u - uoff[a]);
     *r_out = a; *w_out = w; *m_out = ~P.bits[w] & unit_mask(lo, hi, w);
   };
-  // ---- phase 1: counts
+  // ---- phase 1: counts.  When the CTA's units fit one pass (one unit per
+  // thread), phase 3 reuses each thread's word and mask instead of recomputing
+  const bool single = u1 - u0 <= NT;
+  int64_t keep_w = 0;
+  uint32_t keep_m = 0;
   int64_t acc = 0;
   for (int64_t base = u0; base < u1; base += NT) {
-    int64_t u = base + t, r = -1, w;
+    int64_t u = base + t, r = -1, w = 0;
     uint32_t m = 0;
     if (u < u1) unit(u, &r, &w, &m);
+    keep_w = w; keep_m = m;
     int c = __popc(m);
     acc += c;
     if (P.tag_cnt) {
@@ -194,7 +200,7 @@ __device__ __forceinline__ void units_plan_body(const UnitsPlan& P, unsigned cha
       S->aux[2] = 0;   // the switch's multisplit pass count, until the multisplit publishes it
     }
   }
-  if (!P.out) return;   // (callers running later phases follow with a grid barrier)
+  if (!P.out) return all_tot;   // (callers running later phases follow with a grid barrier)
   // ---- phase 3: fill in range order, capped.  Offsets per unit (thread per
   // unit, block scan), then one warp writes a unit's pages with one
   // coalesced store (lane k writes page 32w+k when missing).
@@ -205,7 +211,10 @@ __device__ __forceinline__ void units_plan_body(const UnitsPlan& P, unsigned cha
   for (int64_t base = u0; base < u1; base += NT) {
     int64_t u = base + t, r, w = 0;
     uint32_t m = 0;
-    if (u < u1) unit(u, &r, &w, &m);
+    if (u < u1) {
+      if (single) { w = keep_w; m = keep_m; }
+      else unit(u, &r, &w, &m);
+    }
     int64_t rt;
     int64_t o = (*carry_p) + block_scan_excl_i64(__popc(m), ws, &rt);
     uo_s[t] = o; uw_s[t] = w; um_s[t] = m;
@@ -221,6 +230,7 @@ __device__ __forceinline__ void units_plan_body(const UnitsPlan& P, unsigned cha
     if (t == 0) (*carry_p) += rt;
     __syncthreads();
   }
+  return all_tot;
 }
 
 void ranges_from_actual(Ctx& c, TaskTab& t, int32_t c0, int32_t c1, RangeBuf& B);

@@ -271,6 +271,29 @@ int msg_read_pages(msg_ctx* ctx, int32_t task, int32_t cmd, int32_t which, int64
   });
 }
 
+int msg_read_pages_range(msg_ctx* ctx, int32_t task, int32_t c0, int32_t c1, int32_t which, int64_t* runs,
+                         int64_t cap, int64_t* off, int64_t* nruns) {
+  return guard(ctx, [&] {
+    Ctx& c = ctx->c;
+    TaskTab& t = task_of(c, task);
+    if (c0 < 0 || c1 < c0 || c1 > t.ncmd) throw Error(MSG_E_INVAL, "bad command range");
+    if (!nruns) throw Error(MSG_E_INVAL, "null output");
+    const std::vector<int64_t>& o = which ? t.act_off : t.pred_off;
+    const int64_t i0 = o[c0], n = o[c1] - i0;
+    *nruns = n;
+    if (off)
+      for (int32_t k = 0; k <= c1 - c0; ++k) off[k] = o[c0 + k] - i0;
+    if (!runs) return;
+    const int64_t k = std::min(cap, n);
+    if (k <= 0) return;
+    std::vector<Iv> h(k);
+    MSG_CUDA(cudaMemcpyAsync(h.data(), (which ? t.act_pool.p : t.pred_pool.p) + i0, k * sizeof(Iv),
+                             cudaMemcpyDeviceToHost, c.st));
+    MSG_CUDA(cudaStreamSynchronize(c.st));
+    for (int64_t i = 0; i < k; ++i) { runs[2 * i] = h[i].a; runs[2 * i + 1] = h[i].b; }
+  });
+}
+
 // every window names a registered task and a command range inside it
 static void check_windows(Ctx& c, const msg_window* win, int32_t nwin) {
   if (nwin < 0 || (nwin > 0 && !win)) throw Error(MSG_E_INVAL, "bad window list");

@@ -1,10 +1,3 @@
-O=gpurun_out/p7; mkdir -p $O
-timeout 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/gpu_tests.log 2>&1; tail -4 $O/gpu_tests.log
-timeout 1500 python bench.py --steps 3 --warmup 3 --skip-execute --skip-frag > $O/bench.jsonl 2> $O/bench.err; python - <<'P'
-import json
-d=json.loads(open("gpurun_out/p7/bench.jsonl").read().strip().splitlines()[-1])
-print(d["value"], d["ms_per_step"], json.dumps(d["roofline"])[:600])
-print(json.dumps(d.get("plan_only",{}))[:500])
-print(json.dumps(d.get("cfg2",{}).get("roofline",{}))[:500])
-P
-tail -3 $O/bench.err
+O=gpurun_out/p9; mkdir -p $O
+timeout 300 python tools/predict_latency.py > $O/predict_latency.txt 2>&1; cat $O/predict_latency.txt
+timeout 1200 python -m pytest tests/test_gpu_facade.py tests/test_gpu_predictor_edges.py tests/test_gpu_acceptance.py -x -q -p no:cacheprovider > $O/gpu_tests.log 2>&1; tail -4 $O/gpu_tests.log
