@@ -479,9 +479,10 @@ class Simulator:
             c0, c1 = windows[0][1], windows[0][2]
             pop = self._selfpop[entry.task_id]
             prefix, cum = {}, 0
+            pc = prefix_cnt.tolist()
             for c in range(c0, c1):
                 if not pop[c]:
-                    cum += int(prefix_cnt[c - c0])
+                    cum += pc[c - c0]
                 prefix[c] = min(cum, n_pop)
             if rec is not None:
                 rec["prefix"] = [prefix[c] for c in range(c0, c1)]
@@ -514,15 +515,23 @@ class Simulator:
             if self.recorder is not None:
                 self._um_records(task.id, self.ctx.debug_read(3))
         lat, selfpop = self._lat[task.id], self._selfpop[task.id]
-        while task.cursor < len(task.commands) and elapsed < budget:
+        # the switch-time scan names the next missing command: commands before
+        # it cannot fault (the _touch call is skipped for them, same result)
+        fast = self.mode.name in ("proactive", "ideal") and state is not None
+        last_j, last_ready = None, 0.0   # populate_ready is pure: memo by j (the prefix repeats)
+        ncmd = len(task.commands)
+        while task.cursor < ncmd and elapsed < budget:
             cur = task.cursor
             if pending is not None:
                 j = pending["prefix"].get(cur, 0)
-                ready = populate_ready(self.hw, j, pending["free"], pending["n_evict"])
+                if j != last_j:
+                    last_j, last_ready = j, populate_ready(self.hw, j, pending["free"], pending["n_evict"])
+                ready = last_ready
                 if ready > offset:
                     self.metrics.migration_s += ready - offset
                     offset = ready
-            offset += self._touch(task, selfpop[cur], cur, timeline, state, budget - elapsed, um)
+            if not (fast and state["next_missing"] != cur):
+                offset += self._touch(task, selfpop[cur], cur, timeline, state, budget - elapsed, um)
             if self.execute:
                 gate = state["gate"] if state else None
                 self.ctx.run_command(self._idx[task.id], cur, gate.get(cur, 0) if gate else 0, lat[cur])
