@@ -277,6 +277,7 @@ class Simulator:
         self.events: list = []
         self._idx = {t.id: i for i, t in enumerate(self.tasks)}
         self._lat, self._selfpop = {}, {}
+        self._proj_cache = {}
         for t in self.tasks:
             if isinstance(t.commands, CommandColumns):
                 self._lat[t.id] = t.commands.lat.tolist()
@@ -377,7 +378,7 @@ class Simulator:
                 continue
             rank = {tid: i for i, tid in enumerate(self._rr_order)}
             ready.sort(key=lambda t: rank[t.id])
-            timeline = build_timeline(self.policy, ready, latencies=self._lat)
+            timeline = build_timeline(self.policy, ready, latencies=self._lat, project=self._project)
             entry = timeline[0]
             task = self.by_id[entry.task_id]
             self._rr_order.remove(task.id)
@@ -404,15 +405,24 @@ class Simulator:
         if self.record_events:
             self.events.append(SimEvent(self.t, kind, task_id, pages))
 
+    def _project(self, task_id, cursor: int, budget: float) -> int:
+        """project_cursor on a task's latency column, memoised: the timeline
+        and the windows walk the same (cursor, timeslice) slices switch after
+        switch.  The key carries the column's length (feeders append)."""
+        lat = self._lat[task_id]
+        key = (task_id, cursor, budget, len(lat))
+        end = self._proj_cache.get(key)
+        if end is None:
+            if len(self._proj_cache) > 1 << 16:
+                self._proj_cache.clear()
+            end = self._proj_cache[key] = project_cursor(lat, cursor, budget)
+        return end
+
     def _windows(self, timeline) -> list:
         """(task index, cursor, end) per timeline entry: compute_window's
         FP64 walk (memman.py:186-195) on the host, integers to the GPU."""
-        out = []
-        for e in timeline:
-            lat = self._lat[e.task_id]
-            out.append((self._idx[e.task_id], e.resume_command_cursor,
-                        project_cursor(lat, e.resume_command_cursor, e.timeslice_s)))
-        return out
+        return [(self._idx[e.task_id], e.resume_command_cursor,
+                 self._project(e.task_id, e.resume_command_cursor, e.timeslice_s)) for e in timeline]
 
     def _advised(self, windows, win_pages) -> dict:
         """ReorderStats.pages_advised: reversed windows, dict first-insertion

@@ -62,9 +62,11 @@ def runnable_order(policy: Policy, tasks) -> list:
 
 
 def build_timeline(policy: Policy, tasks, horizon_entries: int | None = None,
-                   latencies: dict | None = None) -> Timeline:
+                   latencies: dict | None = None, project=None) -> Timeline:
     """scheduler.py:50-83.  `latencies` (task id -> list of floats) lets the
-    engine pass cached latency columns instead of walking Command objects."""
+    engine pass cached latency columns instead of walking Command objects;
+    `project(task_id, cursor, budget)` (optional) stands in for
+    project_cursor on them (the engine's memoised walk)."""
     live = runnable_order(policy, tasks)
     if not live:
         return ()
@@ -82,6 +84,7 @@ def build_timeline(policy: Policy, tasks, horizon_entries: int | None = None,
             k = 0
             continue
         plan.append(TimelineEntry(t.id, policy.timeslice_s, pos[t.id]))
-        pos[t.id] = project_cursor(lat[t.id], pos[t.id], policy.timeslice_s)
+        pos[t.id] = (project(t.id, pos[t.id], policy.timeslice_s) if project is not None
+                     else project_cursor(lat[t.id], pos[t.id], policy.timeslice_s))
         k += 1
     return tuple(plan)
