@@ -36,6 +36,10 @@ for k in k_window_combine_wide k_window_runs k_switch_coop; do
   timeout 900 ncu --set full --import-source on --clock-control none -f -k regex:$k -s 200 -c 1 -o $O/ncu_${k}_frag \
       python tools/prof_replay.py frag 1 > /dev/null 2>&1
 done
+# device phase stamps (the phase-timing build, tools/bin/libmsched_mcts.so: `make phase-ts` before the call)
+for c in cfg2 cfg4 cfg1; do timeout 300 python tools/sw_phase_replay.py $c; done > $O/switch_kernel_phases.txt 2>&1
+for c in cfg2 cfg4 cfg1; do timeout 300 python tools/fw_phase_replay.py $c; done > $O/window_kernel_phases.txt 2>&1
+for c in cfg1 cfg3 cfg2 cfg4; do echo "== $c"; timeout 300 python tools/prof_replay.py $c 4; done > $O/planonly_all.txt 2>&1
 MSG_HOST_PHASES=1 timeout 300 python tools/prof_replay.py cfg2 3 > $O/host_phases_cfg2.txt 2>&1
 MSG_HOST_PHASES=1 timeout 300 python tools/prof_replay.py cfg4 2 > $O/host_phases_cfg4.txt 2>&1
 timeout 300 python tools/predict_latency.py > $O/predict_latency.txt 2>&1
