@@ -554,7 +554,7 @@ def multisplit_roofline(st, hbm_peak, traffic=None, traffic_src=None):
         dev_timed = {"avg_launch_ms": dms, "achieved": ms_bytes / (dms * 1e6),
                      "frac": ms_bytes / (dms * 1e6) / hbm_peak, "launches_per_step": st["ms_dev_launches"]}
     ev_passes = st.get("ms_ev_passes", st["ms_passes"])
-    if ev_passes:
+    if ev_passes and 2 * ev_passes >= st["ms_passes"]:
         # standalone launches (the synchronous, migrating path): CUDA events around each launch
         ms_kernel_ms = st["ms_ms"] / ev_passes
         timing = "CUDA events on the planner stream around each launch, averaged over the timed steps"

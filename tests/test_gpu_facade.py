@@ -277,3 +277,56 @@ def test_single_command_predictor_api():                      # test_predictor.p
     unk = Command(CommandKind.KERNEL, 1e-6, "unknown")
     p = predictor.predict({}, unk, PAGE)
     assert not p.complete and len(p.pages) == 0
+
+
+def test_single_command_facades_match_reference_predictions():
+    """The per-call facades (one cached task per descriptor / allocation
+    table, commands appended call by call) == the reference's predictions,
+    with calls of different modes and tasks interleaved."""
+    from paper_2512_24637_b200.analyzer import build_descriptors
+
+    cases = list(loader.predictions())
+    tasks = [loader.dec_task(c["task"]) for c in cases]
+    descs = [build_descriptors(t) for t in tasks]
+    n = max(len(c["rows"]) for c in cases)
+    for i in range(n):                     # command i of every task, round robin
+        for case, task, d in zip(cases, tasks, descs):
+            if i >= len(case["rows"]):
+                continue
+            cmd, row = task.commands[i], case["rows"][i]
+            t = predictor.predict(d, cmd, PAGE)
+            a = predictor.predict_allocation(task.allocations, cmd, PAGE)
+            g = predictor.ground_truth_prediction(cmd, PAGE)
+            assert [list(r) for r in t.pages.runs] == row["template"], (case["name"], i)
+            assert t.complete == row["complete"], (case["name"], i)
+            assert [list(r) for r in a.pages.runs] == row["allocation"], (case["name"], i)
+            assert [list(r) for r in g.pages.runs] == row["truth"], (case["name"], i)
+
+
+def test_read_pages_range_equals_per_command_reads():
+    from paper_2512_24637_b200 import _abi
+    from paper_2512_24637_b200.analyzer import build_descriptors
+
+    case = next(iter(loader.predictions()))
+    task = loader.dec_task(case["task"])
+    ctx = _abi.Context(PAGE, 1, predictor=_abi.PRED_TEMPLATE, flags=_abi.F_LOOSE_DOMAIN)
+    try:
+        ctx.set_domain([(0, 1)])
+        ctx.add_task(0, [(a.base_addr, a.size_bytes) for a in task.allocations])
+        names, rules, offs, _ = _abi.lower_rules(build_descriptors(task))
+        ctx.set_rules(0, rules, offs)
+        ctx.add_commands(0, _abi.encode_commands(task.commands, {nm: k for k, nm in enumerate(names)}))
+        n = len(task.commands)
+        for which in (0, 1):
+            for c0, c1 in ((0, n), (1, max(1, n - 1)), (n // 2, n // 2), (0, 1)):
+                runs, off = ctx.read_pages_range(0, c0, c1, which)
+                assert len(off) == c1 - c0 + 1 and off[0] == 0
+                for k in range(c1 - c0):
+                    got = [tuple(r) for r in runs[off[k]:off[k + 1]].tolist()]
+                    assert got == ctx.read_pages(0, c0 + k, which)
+        with pytest.raises(_abi.MsgError):
+            ctx.read_pages_range(0, 1, 0, 0)
+        with pytest.raises(_abi.MsgError):
+            ctx.read_pages_range(0, 0, n + 1, 0)
+    finally:
+        ctx.close()
