@@ -71,3 +71,26 @@ def test_workloads_are_distinct_per_rank(cfg):
     assert d0 == d1
     assert not {t.id for t in t0} & {t.id for t in t1}
     assert max(a.base_addr for t in t0 for a in t.allocations) < min(a.base_addr for t in t1 for a in t.allocations)
+
+
+def _st(**kw):
+    base = {"ms_ms": 0.0, "ms_passes": 0, "ms_bytes": 0, "ms_dev_launches": 0, "ms_dev_ms": 0.0, "ms_ev_passes": 0}
+    base.update(kw)
+    return base
+
+
+def test_multisplit_roofline_timing_sources():
+    # standalone launches (the migrating headline): CUDA events are the primary timing
+    r = bench.multisplit_roofline(_st(ms_ms=0.9, ms_passes=10, ms_bytes=10 * 350e6, ms_dev_launches=10,
+                                      ms_dev_ms=0.7, ms_ev_passes=10), 6550.0)
+    assert r["timing"].startswith("CUDA events") and math.isclose(r["avg_launch_ms"], 0.09)
+    assert math.isclose(r["achieved"], 350e6 / (0.09 * 1e6)) and math.isclose(r["device_timed"]["avg_launch_ms"], 0.07)
+    # the async path: the multisplit is a phase of the per-switch kernel, so the device clock is primary
+    # (a few standalone launches -- e.g. releases -- do not decide it)
+    r = bench.multisplit_roofline(_st(ms_ms=0.05, ms_passes=100, ms_bytes=100 * 33e6, ms_dev_launches=100,
+                                      ms_dev_ms=1.7, ms_ev_passes=3), 6550.0)
+    assert r["timing"].startswith("%globaltimer") and math.isclose(r["avg_launch_ms"], 0.017)
+    assert r["launches_per_step"] == 100 and math.isclose(r["frac"], 33e6 / (0.017 * 1e6) / 6550.0)
+    # nothing ran
+    r = bench.multisplit_roofline(_st(), 6550.0)
+    assert r["achieved"] == 0.0 and r["device_timed"] is None
