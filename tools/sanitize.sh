@@ -27,4 +27,9 @@ run $CS --tool initcheck python -m pytest tests/test_gpu_parity.py tests/test_gp
     -k "(test_gpu_matches and (stream_2.0 or llm_1.5 or edge_tiny or frag)) or madvise or plan_migration or (moves_the_right_bytes and stream_3.0)"
 run $CS --tool racecheck python -m pytest tests/test_gpu_facade.py -x -q -k "multi_window or large_reorder or randomized"
 run $CS --tool synccheck python -m pytest tests/test_gpu_facade.py -x -q -k "multi_window or large_reorder"
+# the async switch path (k_switch_coop: plan, multisplit and apply as phases of one cooperative launch)
+run $CS --tool racecheck python -m pytest tests/test_gpu_engine.py -x -q -k "async"
+run $CS --tool synccheck python -m pytest tests/test_gpu_engine.py -x -q -k "async"
+run $CS --tool initcheck python -m pytest tests/test_gpu_engine.py -x -q -k "async"
+run $CS --tool memcheck python -m pytest tests/test_gpu_engine.py tests/test_gpu_msim_plugin.py -x -q
 cat $O
