@@ -1693,6 +1693,21 @@ constexpr int MC_PIECES = 4;                // TMA pieces of a slice, one mbarri
 constexpr int MC_FIXED = MC_WARPS * 256 * 4 + 256 * 8 + 16 * 256 * 4 + 8 * (8 + MC_PIECES) + 16;
 constexpr int MC_TCAP_MIN = MS_SMEM_SEGS;   // class-table segments always kept on chip
 constexpr int MC_TCAP_MAX = 16384;          // more when the staged slice leaves room (fragmented lists)
+// ms_coop_body's int32 scratch `red` ([16][256] words): phase-2 slots, then
+// the per-entry chunk queue.  A chunk that is not one run in one
+// constant-class interval is queued (up to MC_QCAP per CTA) instead of being
+// classified by the warp that owns it: after phase 1 every warp takes queued
+// chunks round-robin, stores each entry's digit (one byte) and adds the
+// counts to the owner's row, so the slowest warp no longer carries its
+// blocks' per-entry searches alone; phase 3 reads the stored digits.
+constexpr int kRedSlice = 256;    // [256] this slice's digit counts
+constexpr int kRedDl = 512;       // [256] digits present in the slice
+constexpr int kRedQ = 768;        // [MC_QCAP] queued chunks: chunk index << 5 | owner warp
+constexpr int kRedNq = 832;       // queued-chunk count (may pass MC_QCAP: the rest run inline)
+constexpr int kRedNd = 833;       // present-digit count
+constexpr int kRedCol = 1024;     // [4][256] column sums (many-digit slices)
+constexpr int kRedDig = 2048;     // [MC_QCAP][128] stored digits (bytes)
+constexpr int MC_QCAP = 64;
 
 struct McArgs {
   const int32_t* src0;   // pass 0 source, 16-byte aligned: list entry i is src0[i + a]
@@ -1906,6 +1921,7 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
       issue(srcA, m);
     }
     for (int i = lane; i < 256; i += 32) cnt[warp][i] = 0;
+    if (tid == 0) red[kRedNq] = 0;
     __syncthreads();
     if (pass == 0) MCTS(1);
     const int32_t P4 = piece_len(m);
@@ -2021,10 +2037,19 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
           __syncwarp();
           continue;
         }
-        if (lane == 0) info[4 * b + j] = make_int2(0, -1);
 #ifdef MSG_MC_PHASE_TS
         ++wp_slow;
 #endif
+        // per-entry chunk: queued for the whole CTA when there is room
+        int q = 0;
+        if (lane == 0) q = atomicAdd(&red[kRedNq], 1);
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q < MC_QCAP) {
+          if (lane == 0) { info[4 * b + j] = make_int2(q, -2); red[kRedQ + q] = ((coff / MS_CHUNK) << 5) | warp; }
+          __syncwarp();
+          continue;
+        }
+        if (lane == 0) info[4 * b + j] = make_int2(0, -1);
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           int dk = valid(coff + 32 * k + lane) ? lane_digit(x[k]) : 256;
@@ -2035,6 +2060,28 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
       }
     }
     __syncthreads();
+    // ---- phase 1b: the queued per-entry chunks, round-robin over the warps;
+    // counts go to the owner's row (shared atomics: several warps may add to
+    // one row), digits to the byte store phase 3 reads
+    {
+      const int nq = red[kRedNq] < MC_QCAP ? red[kRedNq] : MC_QCAP;
+      uint8_t* const dig = reinterpret_cast<uint8_t*>(red + kRedDig);
+      for (int q = warp; q < nq; q += MC_WARPS) {
+        const int32_t qi = red[kRedQ + q];
+        const int own = qi & 31;
+        const int32_t coff = (qi >> 5) * MS_CHUNK;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int32_t o = coff + 32 * k + lane;
+          const bool vk = valid(o);
+          const int dk = vk ? lane_digit(fetch(o)) : 256;
+          if (vk) dig[q * MS_CHUNK + 32 * k + lane] = (uint8_t)dk;
+          const uint32_t peers = __match_any_sync(0xffffffffu, dk);
+          if (dk < 256 && lane == __ffs(peers) - 1) atomicAdd(&cnt[own][dk], __popc(peers));
+        }
+      }
+      if (nq) __syncthreads();
+    }
 #ifdef MSG_MC_PHASE_TS
     if (pass == 0 && lane == 0 && blockIdx.x < 160) {
       const unsigned long long t1 = mc_now();
@@ -2051,10 +2098,10 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
       for (int w = 0; w < MC_WARPS; ++w) { int32_t t = cnt[w][tid]; cnt[w][tid] = acc; acc += t; }
       __stcg(A.hist + (int64_t)blockIdx.x * 256 + tid, acc);
       if (acc) atomicAdd(tot + tid, acc);
-      red[1024 + tid] = acc;   // this slice's digit counts
+      red[kRedSlice + tid] = acc;   // this slice's digit counts
       red[tid] = 0;            // prefix accumulators
     }
-    if (tid == 0) red[2304] = 0;
+    if (tid == 0) red[kRedNd] = 0;
     if (pass == 0) MCTS(3);
     grid_barrier(A.bar, nbar++);
     if (pass == 0) MCTS(4);
@@ -2063,10 +2110,10 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
     // runs make that a handful), so the CTA reads those columns of the earlier
     // rows -- one round of independent loads -- instead of whole rows.
     {
-      int32_t* dl = red + 2048;   // present digits
-      if (tid < 256 && red[1024 + tid] > 0) dl[atomicAdd(&red[2304], 1)] = tid;
+      int32_t* dl = red + kRedDl;   // present digits
+      if (tid < 256 && red[kRedSlice + tid] > 0) dl[atomicAdd(&red[kRedNd], 1)] = tid;
       __syncthreads();
-      const int nd = red[2304], me = (int)blockIdx.x;
+      const int nd = red[kRedNd], me = (int)blockIdx.x;
       if (nd <= 16) {
         for (int k = tid; k < nd * me; k += MC_THREADS) {
           const int j = k / me, c2 = k - j * me;
@@ -2083,9 +2130,10 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
         int32_t acc = 0;
 #pragma unroll 8
         for (int c2 = r0; c2 < r1; ++c2) acc += __ldcg(A.hist + (int64_t)c2 * 256 + d);
-        red[2560 + q * 256 + d] = acc;
+        red[kRedCol + q * 256 + d] = acc;
         __syncthreads();
-        if (tid < 256) red[tid] = red[2560 + tid] + red[2816 + tid] + red[3072 + tid] + red[3328 + tid];
+        if (tid < 256)
+          red[tid] = red[kRedCol + tid] + red[kRedCol + 256 + tid] + red[kRedCol + 512 + tid] + red[kRedCol + 768 + tid];
       }
     }
     __syncthreads();
@@ -2153,12 +2201,13 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
           __syncwarp();
           continue;
         }
+        const uint8_t* const dq = reinterpret_cast<const uint8_t*>(red + kRedDig) + rx * MS_CHUNK;   // ry == -2
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const int32_t o = coff + 32 * k + lane;
           const bool vk = valid(o);
           const int32_t xv = vk ? fetch(o) : 0;
-          int dk = vk ? lane_digit(xv) : 256;
+          int dk = vk ? (ry == -2 ? (int)dq[32 * k + lane] : lane_digit(xv)) : 256;
           uint32_t peers = __match_any_sync(0xffffffffu, dk);
           int32_t before = dk < 256 ? cnt[warp][dk] : 0;
           __syncwarp();
@@ -3123,8 +3172,11 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   PhaseClock pc(c, 0);
   fold_events(c, c.event_bound);
   cudaStream_t st = c.st;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  MSG_CUDA(cudaEventCreate(&e0)); MSG_CUDA(cudaEventCreate(&e1));
+  // the call's planner-time pair: created once per context (an event create
+  // and destroy per call cost more host time than the pair's two records)
+  for (auto& e : c.ev_call)
+    if (!e) MSG_CUDA(cudaEventCreate(&e));
+  cudaEvent_t e0 = c.ev_call[0], e1 = c.ev_call[1];
   MSG_CUDA(cudaEventRecord(e0, st));
   TaskTab& t0 = *c.tasks[win[0].task];
   int32_t c0 = win[0].c0, c1 = win[0].c1, ncw = c1 - c0;
@@ -3250,7 +3302,6 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     c.stats.plan_ms += ms;
-    cudaEventDestroy(e0); cudaEventDestroy(e1);
     return;
   }
   // the reorder is queued behind the plan before the host round trip, its
@@ -3343,7 +3394,6 @@ void plan_switch(Ctx& c, const msg_window* win, int32_t nwin, bool reorder_alway
   float ms = 0;
   cudaEventElapsedTime(&ms, e0, e1);
   c.stats.plan_ms += ms;
-  cudaEventDestroy(e0); cudaEventDestroy(e1);
 }
 
 void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_window* win, int32_t nwin,

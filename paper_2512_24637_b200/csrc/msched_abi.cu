@@ -43,7 +43,7 @@ Ctx::~Ctx() {
   if (st_run) cudaStreamSynchronize(st_run);
   for (auto* t : tasks) delete t;
   for (auto e : ev_pool) cudaEventDestroy(e);
-  for (auto e : {ev_mig[0], ev_mig[1], ev_h2d_done, ev_plan_done, ev_d2h_prev})
+  for (auto e : {ev_mig[0], ev_mig[1], ev_call[0], ev_call[1], ev_h2d_done, ev_plan_done, ev_d2h_prev})
     if (e) cudaEventDestroy(e);
   if (arena) cudaFree(arena);
   if (pool) cudaFreeHost(pool);

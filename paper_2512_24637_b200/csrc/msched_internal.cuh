@@ -254,6 +254,7 @@ struct Ctx {
   DVec<int32_t> inst_ep, free_ep;     // per frame: last H2D batch / last D2H batch
   std::vector<cudaEvent_t> ev_d2h_of, ev_h2d_of;   // per batch completion events
   cudaEvent_t ev_mig[2] = {nullptr, nullptr};
+  cudaEvent_t ev_call[2] = {nullptr, nullptr};   // plan_switch's planner-time pair (reused every call)
   std::vector<cudaEvent_t> ev_pool;
   // busy times of event pairs already folded away (fold_events)
   double fold_h2d_ms = 0, fold_d2h_ms = 0, fold_ms_ms = 0, fold_run_ms = 0;

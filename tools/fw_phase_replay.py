@@ -1,12 +1,13 @@
 """k_windows_fused phase timings over one replay (needs `make phase-ts`; GPU box):
 mean SM cycles from the kernel's first stamp to each phase boundary."""
 import ctypes as C
+import os
 import sys
 
 sys.path.insert(0, ".")
 from paper_2512_24637_b200 import _abi  # noqa: E402
 
-_abi.LIB_PATH = "tools/bin/libmsched_mcts.so"
+_abi.LIB_PATH = os.environ.get("MSG_LIB", "tools/bin/libmsched_mcts.so")
 import bench  # noqa: E402
 from paper_2512_24637_b200 import engine  # noqa: E402
 from paper_2512_24637_b200.analyzer import build_descriptors  # noqa: E402

@@ -4,13 +4,14 @@ barrier arrival spread, and which CTAs arrive last.
 
   python tools/mc_cta_replay.py cfg2"""
 import ctypes as C
+import os
 import statistics
 import sys
 
 sys.path.insert(0, ".")
 from paper_2512_24637_b200 import _abi  # noqa: E402
 
-_abi.LIB_PATH = "tools/bin/libmsched_mcts.so"
+_abi.LIB_PATH = os.environ.get("MSG_LIB", "tools/bin/libmsched_mcts.so")
 import bench  # noqa: E402
 from paper_2512_24637_b200 import engine  # noqa: E402
 from paper_2512_24637_b200.analyzer import build_descriptors  # noqa: E402

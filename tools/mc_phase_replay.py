@@ -1,8 +1,8 @@
 """k_ms_coop phase timings over one replay (needs `make phase-ts`; GPU box)."""
-import ctypes as C, sys
+import ctypes as C, os, sys
 sys.path.insert(0, ".")
 from paper_2512_24637_b200 import _abi
-_abi.LIB_PATH = "tools/bin/libmsched_mcts.so"   # built by `make phase-ts`
+_abi.LIB_PATH = os.environ.get("MSG_LIB", "tools/bin/libmsched_mcts.so")   # built by `make phase-ts`
 from paper_2512_24637_b200 import engine, scenarios
 from paper_2512_24637_b200.analyzer import build_descriptors
 cfg = sys.argv[1] if len(sys.argv) > 1 else "cfg2"

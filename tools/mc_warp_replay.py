@@ -5,13 +5,14 @@ launches of one replay (needs `make phase-ts`; GPU box).
   python tools/mc_warp_replay.py cfg2"""
 import collections
 import ctypes as C
+import os
 import statistics
 import sys
 
 sys.path.insert(0, ".")
 from paper_2512_24637_b200 import _abi  # noqa: E402
 
-_abi.LIB_PATH = "tools/bin/libmsched_mcts.so"
+_abi.LIB_PATH = os.environ.get("MSG_LIB", "tools/bin/libmsched_mcts.so")
 import bench  # noqa: E402
 from paper_2512_24637_b200 import engine  # noqa: E402
 from paper_2512_24637_b200.analyzer import build_descriptors  # noqa: E402

@@ -2,12 +2,13 @@
 mean ns from the kernel's start (block 0) to each phase boundary; every
 boundary but the last is taken after a grid barrier."""
 import ctypes as C
+import os
 import sys
 
 sys.path.insert(0, ".")
 from paper_2512_24637_b200 import _abi  # noqa: E402
 
-_abi.LIB_PATH = "tools/bin/libmsched_mcts.so"
+_abi.LIB_PATH = os.environ.get("MSG_LIB", "tools/bin/libmsched_mcts.so")
 import bench  # noqa: E402
 from paper_2512_24637_b200 import engine  # noqa: E402
 from paper_2512_24637_b200.analyzer import build_descriptors  # noqa: E402
