@@ -9,6 +9,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import struct
 from fractions import Fraction
 
 import numpy as np
@@ -83,6 +84,7 @@ ARULE_DT = np.dtype([("ptr_arg", "<i4"), ("kind", "<i4"), ("offset", "<i8"), ("n
                      ("slot", "<i8", (3, 3)), ("v0", "<i8", (3,))])
 
 _lib = None
+_WIN_PACK = struct.Struct("<4i").pack_into   # one msg_window
 
 
 def _p(a):
@@ -109,8 +111,8 @@ def load():
         "msg_add_commands": ([vp, i32, i32, vp, vp, vp, i64, vp, vp], C.c_int),
         "msg_read_pages": ([vp, i32, i32, i32, vp, i64, C.POINTER(i64)], C.c_int),
         "msg_read_pages_range": ([vp, i32, i32, i32, i32, vp, i64, vp, C.POINTER(i64)], C.c_int),
-        "msg_plan_switch": ([vp, vp, i32, i32, C.POINTER(SwitchOut), vp, vp, vp], C.c_int),
-        "msg_touch": ([vp, i32, i32, i64, vp, i32, i32, i32, C.POINTER(TouchOut), vp], C.c_int),
+        "msg_plan_switch": ([vp, vp, i32, i32, vp, vp, vp, vp], C.c_int),
+        "msg_touch": ([vp, i32, i32, i64, vp, i32, i32, i32, vp, vp], C.c_int),
         "msg_um_slice": ([vp, i32, i32, i32, vp, vp], C.c_int),
         "msg_release_task": ([vp, vp, vp, i32, C.POINTER(i64)], C.c_int),
         "msg_list_append": ([vp, vp, vp, i32], C.c_int),
@@ -323,6 +325,34 @@ class Context:
         self.capacity = capacity_pages
         self.h2d_bytes = 0   # host->device bytes handed to the ABI (inputs)
         self.d2h_bytes = 0   # device->host result bytes read back
+        # plan_switch / touch marshal through buffers allocated once per
+        # context with their addresses cached (a per-call ctypes array,
+        # numpy allocations and .ctypes conversions cost ~20 us per call)
+        self._sout, self._tout = SwitchOut(), TouchOut()
+        self._sout_p, self._tout_p = C.addressof(self._sout), C.addressof(self._tout)
+        self._win_cap = 0
+        self._i64_cap = 0
+        self._grow_scratch(64, 1024)
+
+    def _grow_scratch(self, nwin, n64):
+        if nwin > self._win_cap:
+            self._win_cap = max(nwin, 2 * self._win_cap)
+            self._warr = (Window * self._win_cap)()
+            self._warr_p = C.addressof(self._warr)
+            self._wview = memoryview(self._warr).cast("B")
+        if n64 > self._i64_cap:
+            self._i64_cap = max(n64, 2 * self._i64_cap)
+            self._i64 = np.zeros(self._i64_cap, dtype=np.int64)
+            self._i64_p = self._i64.ctypes.data
+
+    def _pack_windows(self, windows):
+        nw = len(windows)
+        if nw > self._win_cap:
+            self._grow_scratch(nw, 0)
+        mv = self._wview
+        for i, (t, a, b) in enumerate(windows):
+            _WIN_PACK(mv, 16 * i, t, a, b, 0)
+        return nw
 
     def close(self):
         if getattr(self, "h", None):
@@ -385,29 +415,39 @@ class Context:
         return buf[:2 * n.value].reshape(-1, 2), off
 
     def plan_switch(self, windows, reorder_always=False):
-        nw = len(windows)
-        warr = (Window * nw)(*[Window(t, a, b, 0) for t, a, b in windows])
+        """msg_plan_switch; returns (SwitchOut, per-window pages, per-command
+        gating counts, per-command touch counts), all owned by the caller."""
+        if not windows:
+            raise MsgError(MSG_E_INVAL, "need at least one window")
+        nw = self._pack_windows(windows)
         ncw = windows[0][2] - windows[0][1]
-        win_pages = np.zeros(nw, dtype=np.int64)
-        prefix = np.zeros(max(ncw, 1), dtype=np.int64)
-        touch = np.zeros(max(ncw, 1), dtype=np.int64)
-        out = SwitchOut()
-        self.h2d_bytes += C.sizeof(warr)
-        self.d2h_bytes += C.sizeof(out) + win_pages.nbytes + 2 * 8 * ncw
-        self.check(self.lib.msg_plan_switch(self.h, warr, nw, int(reorder_always), C.byref(out), _p(win_pages),
-                                            _p(prefix), _p(touch)))
-        return out, win_pages, prefix[:ncw], touch[:ncw]
+        n64 = nw + 2 * max(ncw, 1)
+        if n64 > self._i64_cap:
+            self._grow_scratch(0, n64)
+        p = self._i64_p
+        self.h2d_bytes += 16 * nw
+        self.d2h_bytes += C.sizeof(SwitchOut) + 8 * nw + 2 * 8 * ncw
+        rc = self.lib.msg_plan_switch(self.h, self._warr_p, nw, int(reorder_always), self._sout_p, p,
+                                      p + 8 * nw, p + 8 * (nw + max(ncw, 1)))
+        if rc:
+            self.check(rc)
+        buf = self._i64[:n64].copy()
+        o = nw + max(ncw, 1)
+        return SwitchOut.from_buffer_copy(self._sout), buf[:nw], buf[nw:nw + ncw], buf[o:o + ncw]
 
     def touch(self, idx, cmd, evict, windows, scan_end, write_tags):
-        nw = len(windows)
-        warr = (Window * max(nw, 1))(*[Window(t, a, b, 0) for t, a, b in windows])
-        win_pages = np.zeros(max(nw, 1), dtype=np.int64)
-        out = TouchOut()
-        self.h2d_bytes += C.sizeof(warr)
-        self.d2h_bytes += C.sizeof(out) + 8 * nw
-        self.check(self.lib.msg_touch(self.h, idx, cmd, evict, warr if nw else None, nw, scan_end,
-                                      int(write_tags), C.byref(out), _p(win_pages)))
-        return out, win_pages[:nw]
+        """msg_touch; returns (TouchOut, per-window pages of the refresh),
+        owned by the caller."""
+        nw = self._pack_windows(windows)
+        if nw > self._i64_cap:
+            self._grow_scratch(0, nw)
+        self.h2d_bytes += 16 * nw
+        self.d2h_bytes += C.sizeof(TouchOut) + 8 * nw
+        rc = self.lib.msg_touch(self.h, idx, cmd, evict, self._warr_p if nw else None, nw, scan_end,
+                                int(write_tags), self._tout_p, self._i64_p)
+        if rc:
+            self.check(rc)
+        return TouchOut.from_buffer_copy(self._tout), self._i64[:nw].copy()
 
     def run_command(self, idx, cmd, need_pages, latency_s=0.0):
         """Execute a command on the device once `need_pages` of the current

@@ -61,9 +61,28 @@ __shared__ unsigned long long sw_t0;
       if ((i) == 7) atomicAdd(&g_sw_n, 1ull);                                     \
     }                                                                             \
   } while (0)
+// k_window_combine_wide / k_window_runs (block 0) phase stamps: [phase]
+// summed SM cycles since the kernel's first stamp, and launches
+__device__ unsigned long long g_cw_sum[16], g_cw_n, g_wr_sum[16], g_wr_n;
+#define PHTS(arr, cnt, i, last)                                                   \
+  do {                                                                            \
+    __syncthreads();                                                              \
+    if (threadIdx.x == 0 && blockIdx.x == 0) {                                    \
+      const unsigned long long t_ = (unsigned long long)clock64();                \
+      if ((i) == 0) ph_t0 = t_;                                                   \
+      atomicAdd(&arr[i], t_ - ph_t0);                                             \
+      if (last) atomicAdd(&cnt, 1ull);                                            \
+    }                                                                             \
+  } while (0)
+#define CWTS(i) PHTS(g_cw_sum, g_cw_n, i, (i) == 15)
+#define WRTS(i) PHTS(g_wr_sum, g_wr_n, i, (i) == 15)
+#define PHTS_DECL unsigned long long ph_t0 = 0; (void)ph_t0
 #else
 #define FWTS(i) do {} while (0)
 #define SWTS(i) do {} while (0)
+#define CWTS(i) do {} while (0)
+#define WRTS(i) do {} while (0)
+#define PHTS_DECL do {} while (0)
 #endif
 
 static int64_t g_launches = 0;
@@ -188,6 +207,8 @@ constexpr int64_t kWinSmem = 200 * 1024;
 // reserved (same layout).
 __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, int64_t* gkey_u, int64_t* gval,
                               int32_t* glab, WinOut out, int64_t smem_cap) {
+  PHTS_DECL;
+  WRTS(0);
   const WinDesc W = wins[blockIdx.x];
   const Iv* pool = W.pool;
   int64_t n = W.pool_hi - W.pool_lo;
@@ -220,7 +241,9 @@ __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, in
     val[i] = 0;
   }
   __syncthreads();
+  WRTS(1);
   bitonic_kv(key, val, mp);
+  WRTS(2);
   // 2. unique: flag first occurrences, scan to positions (val holds flags)
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) val[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
   __syncthreads();
@@ -236,6 +259,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, in
   int64_t nseg = nu - 1;
   for (int64_t k = threadIdx.x; k < nseg; k += blockDim.x) L[k] = kNone;
   __syncthreads();
+  WRTS(3);
   // 3. label = min covering command (first access)
   for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
     const Iv& v = pool[W.pool_lo + i];
@@ -251,6 +275,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, in
     for (int64_t k = s0; k < s1; ++k) atomicMin(&L[k], cmd);
   }
   __syncthreads();
+  WRTS(4);
   // 4. runs: maximal segment groups with one label (segments abut by construction)
   int64_t* rflag = val;  // reuse: run-start flags -> run ids
   for (int64_t k = threadIdx.x; k < nseg; k += blockDim.x)
@@ -284,7 +309,9 @@ __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, in
     v2[i] = i;
   }
   __syncthreads();
+  WRTS(5);
   bitonic_kv(k2, v2, rp);
+  WRTS(6);
   // gather into final order (use the label area beyond nr as temp for permuted copy)
   int64_t* ta = reinterpret_cast<int64_t*>(key) + rp;   // temp arrays
   int64_t* tb = ta + nr;
@@ -311,6 +338,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, in
     out.pages[W.w] = tot_s;
     out.run_base[W.w] = base;
   }
+  WRTS(15);
 }
 
 // ---------------------------------------------------------------------------
@@ -607,6 +635,8 @@ __device__ bool block_radix_sort(uint64_t* a0, uint64_t* a1, int32_t* av, uint64
 }
 
 __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P, int64_t smem_cap, int32_t* ok_out) {
+  PHTS_DECL;
+  CWTS(0);
   __shared__ int64_t tot_runs_s;
   __shared__ u128 mult_s[64];
   __shared__ int32_t rad_s[64];
@@ -678,11 +708,13 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
         atomicMax(&mx_s, (unsigned long long)v);
       }
       __syncthreads();
+      CWTS(1);
       const uint64_t mn = mn_s;
       for (int i = threadIdx.x; i < m; i += blockDim.x) ea[i] -= mn;
       const int ebits = mx_s > mn ? 64 - __clzll((long long)(mx_s - mn)) : 0;
       __syncthreads();
       const bool ein_b = block_radix_sort<1>(ea, nullptr, nullptr, eb, nullptr, nullptr, m, ebits, cnt, rwarp_s);
+      CWTS(2);
       const uint64_t* es = ein_b ? eb : ea;
       int32_t* fl = reinterpret_cast<int32_t*>(ein_b ? ea : eb);   // the free buffer: unique flags -> positions
       for (int i = threadIdx.x; i < m; i += blockDim.x) fl[i] = (i == 0 || es[i] != es[i - 1]) ? 1 : 0;
@@ -697,6 +729,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       uint64_t* khi = ea + ns;
       for (int k = threadIdx.x; k < ns; k += blockDim.x) { klo[k] = 0; khi[k] = 0; }
       __syncthreads();
+      CWTS(3);
       for (int w = 0; w < W; ++w) {
         const int64_t nr = P.nruns[w];
         const u128 mw = mult_s[w];
@@ -712,6 +745,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
         }
         __syncthreads();
       }
+      CWTS(4);
       // covered segments -> X (key lo, key hi, segment index), in segment order
       int nc = 0;
       for (int base = 0; base < ns; base += blockDim.x) {
@@ -746,7 +780,9 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       uint64_t* ylo = ea;
       uint64_t* yhi = ylo + nc;
       int32_t* yid = reinterpret_cast<int32_t*>(yhi + nc);
+      CWTS(5);
       const bool kin_b = block_radix_sort<2>(xlo, xhi, xid, ylo, yhi, yid, nc, kbits, cnt, rwarp_s);
+      CWTS(6);
       const uint64_t* slo = kin_b ? ylo : xlo;
       const uint64_t* shi = kin_b ? yhi : xhi;
       const int32_t* sid = kin_b ? yid : xid;
@@ -762,6 +798,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
         rcarry += tot;
       }
       __syncthreads();
+      CWTS(7);
       // covered segments in E order -> the class table
       int64_t oc = 0;
       for (int base = 0; base < ns; base += blockDim.x) {
@@ -778,6 +815,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
         oc += tot;
       }
       if (threadIdx.x == 0) { *P.nseg_out = nc; *P.ncls_out = rcarry; }
+      CWTS(15);
       return;
     }
   }
@@ -3450,8 +3488,7 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     compact_if_needed(c);
     const int64_t len0 = c.len, head0 = c.head, fifo_head0 = c.fifo_head, fifo_len0 = c.fifo_len;
     const int cur0 = c.cur;
-    int64_t* passes_d = &c.dstate->aux[2];
-    MSG_CUDA(cudaMemsetAsync(passes_d, 0, sizeof(int64_t), st));
+    int64_t* passes_d = &c.dstate->aux[2];   // published by the multisplit phase (none: read as 0)
     const int G = sw_grid(c);
     int32_t* bar = next_barrier(c);
     SwitchArgs SA{};
@@ -3462,7 +3499,7 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     SA.has_up = has_iv ? 1 : 0;
     SA.has_ms = evict > 0 && refresh && len0 > 0 &&
                 ms_args(c, wp.tab, 0, DevPasses{wp.ncls, nullptr, 0, passes_d}, G, bar, SA.ms);
-    const ListSel L{c.order[cur0].p, c.order[cur0 ^ 1].p, head0, passes_d};
+    const ListSel L{c.order[cur0].p, c.order[cur0 ^ 1].p, head0, SA.has_ms ? passes_d : nullptr};
     const int64_t ev_done = evict > 0 ? std::min(evict, len0) : 0;
     const int32_t lo = cmd + 1, hi = scan_end;
     c.s.tc.resize(std::max(hi - lo, 1), st);
@@ -3475,7 +3512,7 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     AA.tc = reinterpret_cast<unsigned long long*>(c.s.tc.p);
     if (has_iv) AA.pack.seg[AA.pack.nseg++] = PackSeg{c.s.uscr.p + 400, 1, 0};
     if (refresh) AA.pack.seg[AA.pack.nseg++] = PackSeg{wp.pages, nwin, 1};
-    AA.pack.seg[AA.pack.nseg++] = PackSeg{passes_d, 1, 2 + nwin};
+    if (SA.has_ms) AA.pack.seg[AA.pack.nseg++] = PackSeg{passes_d, 1, 2 + nwin};
     if (hi > lo) AA.pack.seg[AA.pack.nseg++] = PackSeg{c.s.tc.p, hi - lo, 3 + nwin};
     AA.bar = bar;
     SA.ap = AA;
@@ -3489,7 +3526,7 @@ void touch_slow(Ctx& c, int32_t task, int32_t cmd, int64_t evict, const msg_wind
     out->missing = n;
     out->refreshed = evict > 0 && refresh ? 1 : 0;
     out->evicted = ev_done;
-    const int64_t passes = hb[2 + nwin];
+    const int64_t passes = SA.has_ms ? hb[2 + nwin] : 0;
     if (passes > 0) {   // ms_coop_done
       c.cur ^= (int)(passes & 1);
       c.head = 0;
@@ -3996,6 +4033,13 @@ extern "C" void msg_dbg_sw_ts(unsigned long long* out) {   // 8 phase sums + lau
   cudaMemcpyFromSymbol(out + 9, msg::g_gap_sum, 8);
   cudaMemcpyFromSymbol(out + 10, msg::g_gap_n, 8);
 }
+extern "C" void msg_dbg_cw_ts(unsigned long long* out) {   // combine_wide 16 sums + n, window_runs 16 sums + n
+  cudaDeviceSynchronize();
+  cudaMemcpyFromSymbol(out, msg::g_cw_sum, 16 * 8);
+  cudaMemcpyFromSymbol(out + 16, msg::g_cw_n, 8);
+  cudaMemcpyFromSymbol(out + 17, msg::g_wr_sum, 16 * 8);
+  cudaMemcpyFromSymbol(out + 33, msg::g_wr_n, 8);
+}
 extern "C" void msg_dbg_mc_reset() {
   unsigned long long lo[16], hi[16] = {0}, z[16] = {0}, zn = 0;
   for (int i = 0; i < 16; ++i) lo[i] = ~0ull;
@@ -4011,5 +4055,9 @@ extern "C" void msg_dbg_mc_reset() {
   cudaMemcpyToSymbol(msg::g_gap_sum, &zn, 8);
   cudaMemcpyToSymbol(msg::g_gap_n, &zn, 8);
   cudaMemcpyToSymbol(msg::g_fw_end, &zn, 8);
+  cudaMemcpyToSymbol(msg::g_cw_sum, zf, sizeof(zf));
+  cudaMemcpyToSymbol(msg::g_cw_n, &zn, 8);
+  cudaMemcpyToSymbol(msg::g_wr_sum, zf, sizeof(zf));
+  cudaMemcpyToSymbol(msg::g_wr_n, &zn, 8);
 }
 #endif
