@@ -202,6 +202,10 @@ struct WinOut {
 extern __shared__ __align__(16) unsigned char dyn_smem[];
 constexpr int64_t kWinSmem = 200 * 1024;
 
+template <int NW>
+__device__ bool block_radix_sort(uint64_t* a0, uint64_t* a1, int32_t* av, uint64_t* b0, uint64_t* b1, int32_t* bv,
+                                 int n, int nbits, int32_t (*cnt)[256], int32_t* warp_s, int sh0);
+
 // Scratch lives in shared memory when the window fits (44 B per padded
 // endpoint: key[4mp] val[mp] label[mp]), else in the global region the host
 // reserved (same layout).
@@ -216,13 +220,17 @@ __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, in
   uint64_t* key = reinterpret_cast<uint64_t*>(gkey_u) + base;
   int64_t* val = gval + base;
   int32_t* L = glab + base;
-  {
-    int64_t mp0 = pow2_at_least(2 * n);
-    if (44 * mp0 <= smem_cap) {
-      key = reinterpret_cast<uint64_t*>(dyn_smem);
-      val = reinterpret_cast<int64_t*>(key + 4 * mp0);
-      L = reinterpret_cast<int32_t*>(val + mp0);
-    }
+  // on-chip windows that leave room for the digit counters sort with the
+  // block radix sort (a few 8-bit passes) instead of the bitonic network
+  const int64_t mp0 = pow2_at_least(2 * n);
+  const bool radix = 44 * mp0 + 32 * 256 * 4 <= smem_cap && mp0 <= (1 << 20);
+  int32_t(*rcnt)[256] = reinterpret_cast<int32_t(*)[256]>(dyn_smem + 44 * mp0);
+  __shared__ int32_t rws[32];
+  __shared__ unsigned long long rmn_s, rmx_s;
+  if (44 * mp0 <= smem_cap) {
+    key = reinterpret_cast<uint64_t*>(dyn_smem);
+    val = reinterpret_cast<int64_t*>(key + 4 * mp0);
+    L = reinterpret_cast<int32_t*>(val + mp0);
   }
   __shared__ int64_t tot_s;
   if (n == 0) {
@@ -242,7 +250,34 @@ __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, in
   }
   __syncthreads();
   WRTS(1);
-  bitonic_kv(key, val, mp);
+  if (radix) {
+    // keys relative to the smallest endpoint: only the spanned bits are sorted
+    unsigned long long vmn = ~0ull, vmx = 0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) {
+      vmn = key[i] < vmn ? key[i] : vmn;
+      vmx = key[i] > vmx ? key[i] : vmx;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, vmn, o), b2 = __shfl_xor_sync(0xffffffffu, vmx, o);
+      vmn = a2 < vmn ? a2 : vmn;
+      vmx = b2 > vmx ? b2 : vmx;
+    }
+    if (threadIdx.x == 0) { rmn_s = ~0ull; rmx_s = 0; }
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) { atomicMin(&rmn_s, vmn); atomicMax(&rmx_s, vmx); }
+    __syncthreads();
+    const unsigned long long mn = rmn_s;
+    const int ebits = rmx_s > mn ? 64 - __clzll((long long)(rmx_s - mn)) : 0;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) key[i] -= mn;
+    __syncthreads();
+    const bool in_b = block_radix_sort<1>(key, nullptr, nullptr, key + mp, nullptr, nullptr, (int)m, ebits, rcnt, rws, 0);
+    const uint64_t* src = in_b ? key + mp : key;
+    for (int64_t i = threadIdx.x; i < m; i += blockDim.x) key[i] = src[i] + mn;
+    __syncthreads();
+  } else {
+    bitonic_kv(key, val, mp);
+  }
   WRTS(2);
   // 2. unique: flag first occurrences, scan to positions (val holds flags)
   for (int64_t i = threadIdx.x; i < m; i += blockDim.x) val[i] = (i == 0 || key[i] != key[i - 1]) ? 1 : 0;
@@ -304,13 +339,25 @@ __global__ void __launch_bounds__(1024, 1) k_window_runs(const WinDesc* wins, in
   int64_t* v2 = val;
   // E lives at key + mp; make sure we do not overwrite it before use: copy runs first
   __syncthreads();
-  for (int64_t i = threadIdx.x; i < rp; i += blockDim.x) {
-    k2[i] = i < nr ? (((uint64_t)(uint32_t)rl[i] << 32) | (uint64_t)i) : ~0ull;
-    v2[i] = i;
-  }
-  __syncthreads();
   WRTS(5);
-  bitonic_kv(k2, v2, rp);
+  if (radix) {
+    // key = (label - c0, run id): labels are commands of [c0, c1)
+    const int ib = nr > 1 ? 64 - __clzll((long long)(nr - 1)) : 0;
+    const int lb = W.c1 - W.c0 > 1 ? 32 - __clz(W.c1 - W.c0 - 1) : 0;
+    for (int64_t i = threadIdx.x; i < nr; i += blockDim.x)
+      k2[i] = ((uint64_t)(uint32_t)(rl[i] - W.c0) << ib) | (uint64_t)i;
+    __syncthreads();
+    const bool in_b = block_radix_sort<1>(k2, nullptr, nullptr, k2 + rp, nullptr, nullptr, (int)nr, ib + lb, rcnt, rws, 0);
+    const uint64_t* src = in_b ? k2 + rp : k2;
+    for (int64_t i = threadIdx.x; i < nr; i += blockDim.x) v2[i] = (int64_t)(src[i] & ((1ull << ib) - 1));
+  } else {
+    for (int64_t i = threadIdx.x; i < rp; i += blockDim.x) {
+      k2[i] = i < nr ? (((uint64_t)(uint32_t)rl[i] << 32) | (uint64_t)i) : ~0ull;
+      v2[i] = i;
+    }
+    __syncthreads();
+    bitonic_kv(k2, v2, rp);
+  }
   WRTS(6);
   // gather into final order (use the label area beyond nr as temp for permuted copy)
   int64_t* ta = reinterpret_cast<int64_t*>(key) + rp;   // temp arrays
@@ -578,13 +625,13 @@ __device__ void bitonic_u64(uint64_t* key, int64_t npow2) {
 // ping-pongs between buffers a and b; returns true when the result is in b.
 template <int NW>
 __device__ bool block_radix_sort(uint64_t* a0, uint64_t* a1, int32_t* av, uint64_t* b0, uint64_t* b1, int32_t* bv,
-                                 int n, int nbits, int32_t (*cnt)[256], int32_t* warp_s) {
+                                 int n, int nbits, int32_t (*cnt)[256], int32_t* warp_s, int sh0) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t lt = (1u << lane) - 1u;
   const int per = ((n + 31) / 32 + 31) & ~31;
   const int lo = w * per, hi = lo + per < n ? lo + per : n;
   bool in_b = false;
-  for (int sh = 0; sh < nbits; sh += 8) {
+  for (int sh = sh0; sh < nbits; sh += 8) {   // key bits [sh0, nbits)
     uint64_t* s0 = in_b ? b0 : a0; uint64_t* s1 = in_b ? b1 : a1; int32_t* sv = in_b ? bv : av;
     uint64_t* d0 = in_b ? a0 : b0; uint64_t* d1 = in_b ? a1 : b1; int32_t* dv = in_b ? av : bv;
     auto digit = [&](int i) -> int {
@@ -641,11 +688,16 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
   __shared__ u128 mult_s[64];
   __shared__ int32_t rad_s[64];
   __shared__ int ok_s;
+  __shared__ int64_t npre_s[65], rbase_s[64];   // per-window run prefix and scratch base (W <= 64)
   const int W = P.nwin;
   if (threadIdx.x < 64) rad_s[threadIdx.x] = 0;
   if (threadIdx.x == 0) {
     int64_t t = 0;
-    for (int w = 0; w < W; ++w) t += P.nruns[w];
+    for (int w = 0; w < W; ++w) {
+      if (w < 64) { npre_s[w] = t; rbase_s[w] = P.run_base[w]; }
+      t += P.nruns[w];
+    }
+    if (W <= 64) npre_s[W] = t;
     tot_runs_s = t;
   }
   __syncthreads();
@@ -655,12 +707,22 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
     return;
   }
   // radix per window: max class + 1
-  for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
-    int64_t g = i, w = 0;
-    while (g >= P.nruns[w]) { g -= P.nruns[w]; ++w; }
-    int64_t r = P.run_base[w] + g;
-    int32_t cls = P.run_cls ? P.run_cls[r] : (int32_t)(P.nruns[w] - g);
-    atomicMax(&rad_s[w], cls);
+  for (int64_t i0 = 0; i0 < M; i0 += blockDim.x) {
+    const int64_t i = i0 + threadIdx.x;
+    int w = -1;
+    int32_t cls = 0;
+    if (i < M) {
+      w = 0;
+      while (i >= npre_s[w + 1]) ++w;   // (shared memory; empty windows are skipped)
+      const int64_t g = i - npre_s[w];
+      const int64_t r = rbase_s[w] + g;
+      cls = P.run_cls ? P.run_cls[r] : (int32_t)(npre_s[w + 1] - npre_s[w] - g);
+    }
+    // one shared atomic per window present in the warp (lanes of a window
+    // are contiguous): 1024 contended atomics on <= 64 words were serialised
+    const uint32_t peers = __match_any_sync(0xffffffffu, w);
+    const int32_t mx = __reduce_max_sync(peers, cls);
+    if (w >= 0 && (int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicMax(&rad_s[w], mx);
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -698,14 +760,26 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(dyn_smem + cnt_off);
       if (threadIdx.x == 0) { mn_s = ~0ull; mx_s = 0; klo_max_s = 0; khi_max_s = 0; }
       __syncthreads();
-      for (int i = threadIdx.x; i < m; i += blockDim.x) {
-        int64_t g = i >> 1, w = 0;
-        while (g >= P.nruns[w]) { g -= P.nruns[w]; ++w; }
-        const int64_t r = P.run_base[w] + g;
-        const uint64_t v = (uint64_t)((i & 1) ? P.run_b[r] : P.run_a[r]);
-        ea[i] = v;
-        atomicMin(&mn_s, (unsigned long long)v);
-        atomicMax(&mx_s, (unsigned long long)v);
+      {
+        unsigned long long vmn = ~0ull, vmx = 0;
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+          const int64_t gi = i >> 1;
+          int w = 0;
+          while (gi >= npre_s[w + 1]) ++w;
+          const int64_t r = rbase_s[w] + (gi - npre_s[w]);
+          const uint64_t v = (uint64_t)((i & 1) ? P.run_b[r] : P.run_a[r]);
+          ea[i] = v;
+          vmn = v < vmn ? v : vmn;
+          vmx = v > vmx ? v : vmx;
+        }
+        // warp-reduced, then one shared atomic per warp (was two per endpoint)
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+          const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, vmn, o), b2 = __shfl_xor_sync(0xffffffffu, vmx, o);
+          vmn = a2 < vmn ? a2 : vmn;
+          vmx = b2 > vmx ? b2 : vmx;
+        }
+        if ((threadIdx.x & 31) == 0) { atomicMin(&mn_s, vmn); atomicMax(&mx_s, vmx); }
       }
       __syncthreads();
       CWTS(1);
@@ -713,7 +787,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       for (int i = threadIdx.x; i < m; i += blockDim.x) ea[i] -= mn;
       const int ebits = mx_s > mn ? 64 - __clzll((long long)(mx_s - mn)) : 0;
       __syncthreads();
-      const bool ein_b = block_radix_sort<1>(ea, nullptr, nullptr, eb, nullptr, nullptr, m, ebits, cnt, rwarp_s);
+      const bool ein_b = block_radix_sort<1>(ea, nullptr, nullptr, eb, nullptr, nullptr, m, ebits, cnt, rwarp_s, 0);
       CWTS(2);
       const uint64_t* es = ein_b ? eb : ea;
       int32_t* fl = reinterpret_cast<int32_t*>(ein_b ? ea : eb);   // the free buffer: unique flags -> positions
@@ -731,10 +805,10 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       __syncthreads();
       CWTS(3);
       for (int w = 0; w < W; ++w) {
-        const int64_t nr = P.nruns[w];
+        const int64_t nr = npre_s[w + 1] - npre_s[w];
         const u128 mw = mult_s[w];
         for (int64_t g = threadIdx.x; g < nr; g += blockDim.x) {
-          const int64_t r = P.run_base[w] + g;
+          const int64_t r = rbase_s[w] + g;
           const int32_t cls = P.run_cls ? P.run_cls[r] : (int32_t)(nr - g);
           const u128 add = mw * (u128)(uint32_t)cls;
           const int64_t s0 = lower_bound_i64(E, nu, P.run_a[r]), s1 = lower_bound_i64(E, nu, P.run_b[r]);
@@ -760,7 +834,103 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       uint64_t* xlo = reinterpret_cast<uint64_t*>(dyn_smem + x_off);
       uint64_t* xhi = xlo + nc;
       int32_t* xid = reinterpret_cast<int32_t*>(xhi + nc);
+      for (int k = threadIdx.x; k < ns; k += blockDim.x) P.E[nu + k] = 0;
+      int64_t rcarry = 0;
+      // ---- grouped path.  In key order the covered segments fall into
+      // groups by (w*, c*): the first window a segment is in and its class
+      // there (every earlier window's digit is 0), w* descending, then c*
+      // ascending; within a group (the segments of one run of window w*) the
+      // later windows decide.  Sorting by that short primary key (a few
+      // radix passes instead of up to sixteen over the 128-bit key) and
+      // insertion-sorting the groups by the full key gives the same order.
+      // Groups are single segments when windows hold scattered pages; a
+      // group of more than 32 segments falls back to the full-key sort.
+      bool ranked = false;
+      {
+        constexpr int IDB = 20;   // segment index bits of a packed key
+        int wb = 0;
+        while ((1 << wb) < W) ++wb;
+        int32_t cmax = 0;
+        for (int w = 0; w < W; ++w) cmax = rad_s[w] > cmax ? rad_s[w] : cmax;
+        int cb = 0;
+        while ((1ll << cb) <= (int64_t)cmax) ++cb;
+        __shared__ int big_s;
+        if (IDB + wb + cb <= 64 && ns < (1 << IDB)) {
+          uint64_t* pk = xlo;   // packed (primary << IDB | segment), in segment order
+          uint64_t* pk2 = xhi;  // the sort's second buffer
+          int64_t carry2 = 0;
+          for (int base = 0; base < ns; base += blockDim.x) {
+            const int k = base + threadIdx.x;
+            const bool cov = k < ns && (klo[k] | khi[k]) != 0;
+            int32_t tot;
+            const int32_t ex = block_excl_scan<int32_t>(cov ? 1 : 0, rwarp_s, &tot);
+            if (cov) {
+              const u128 key = ((u128)khi[k]) << 64 | klo[k];
+              int ws = 0;   // smallest w with mult[w] <= key (mult falls with w)
+              while (ws + 1 < W && mult_s[ws] > key) ++ws;
+              // c* = key / mult[w*]: a double-precision estimate (within one of
+              // the quotient, which is < 2^20), corrected exactly -- a 128-bit
+              // division per segment was the phase's cost
+              const u128 mw = mult_s[ws];
+              const double kd = (double)khi[k] * 18446744073709551616.0 + (double)klo[k];
+              const double md = (double)(uint64_t)(mw >> 64) * 18446744073709551616.0 + (double)(uint64_t)mw;
+              uint64_t cs = (uint64_t)(kd / md);
+              while (cs > 0 && (u128)cs * mw > key) --cs;
+              while ((u128)(cs + 1) * mw <= key) ++cs;
+              pk[carry2 + ex] = ((((uint64_t)(W - 1 - ws)) << cb | cs) << IDB) | (uint64_t)k;
+            }
+            carry2 += tot;
+          }
+          if (threadIdx.x == 0) big_s = 0;
+          __syncthreads();
+          CWTS(5);
+          const bool in_b = block_radix_sort<1>(pk, nullptr, nullptr, pk2, nullptr, nullptr, nc, IDB + wb + cb, cnt,
+                                                rwarp_s, IDB);
+          uint64_t* ps = in_b ? pk2 : pk;
+          constexpr uint64_t kSeg = (1ull << IDB) - 1;
+          auto kless = [&](uint64_t u, uint64_t v) {
+            const int a = (int)(u & kSeg), b = (int)(v & kSeg);
+            return khi[a] < khi[b] || (khi[a] == khi[b] && klo[a] < klo[b]);
+          };
+          for (int i = threadIdx.x; i < nc; i += blockDim.x) {
+            const uint64_t pi = ps[i] >> IDB;
+            if (i > 0 && (ps[i - 1] >> IDB) == pi) continue;   // not a group start
+            int j = i + 1;
+            while (j < nc && (ps[j] >> IDB) == pi && j - i <= 32) ++j;
+            if (j - i > 32) { big_s = 1; continue; }
+            for (int a = i + 1; a < j; ++a) {   // (group members share the primary bits others read)
+              const uint64_t v = ps[a];
+              int b = a;
+              while (b > i && kless(v, ps[b - 1])) { ps[b] = ps[b - 1]; --b; }
+              ps[b] = v;
+            }
+          }
+          __syncthreads();
+          CWTS(6);
+          if (!big_s) {
+            for (int base = 0; base < nc; base += blockDim.x) {
+              const int i = base + threadIdx.x;
+              bool first = false;
+              if (i < nc) {
+                const int a = (int)(ps[i] & kSeg);
+                first = i == 0;
+                if (!first) {
+                  const int b = (int)(ps[i - 1] & kSeg);
+                  first = klo[a] != klo[b] || khi[a] != khi[b];
+                }
+              }
+              int32_t tot;
+              const int32_t ex = block_excl_scan<int32_t>(first ? 1 : 0, rwarp_s, &tot);
+              if (i < nc) P.E[nu + (int64_t)(ps[i] & kSeg)] = rcarry + ex + (first ? 1 : 0);
+              rcarry += tot;
+            }
+            ranked = true;
+          }
+        }
+      }
+      if (!ranked) {
       int64_t carry = 0;
+      unsigned long long hmax = 0, lmax = 0;
       for (int base = 0; base < ns; base += blockDim.x) {
         const int k = base + threadIdx.x;
         const bool cov = k < ns && (klo[k] | khi[k]) != 0;
@@ -769,26 +939,29 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
         if (cov) {
           const int o = (int)(carry + ex);
           xlo[o] = klo[k]; xhi[o] = khi[k]; xid[o] = k;
-          atomicMax(&khi_max_s, (unsigned long long)khi[k]);
-          atomicMax(&klo_max_s, (unsigned long long)klo[k]);
+          hmax = khi[k] > hmax ? khi[k] : hmax;
+          lmax = klo[k] > lmax ? klo[k] : lmax;
         }
         carry += tot;
       }
+#pragma unroll
+      for (int o = 16; o; o >>= 1) {
+        const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, hmax, o), b2 = __shfl_xor_sync(0xffffffffu, lmax, o);
+        hmax = a2 > hmax ? a2 : hmax;
+        lmax = b2 > lmax ? b2 : lmax;
+      }
+      if ((threadIdx.x & 31) == 0) { atomicMax(&khi_max_s, hmax); atomicMax(&klo_max_s, lmax); }
       __syncthreads();
       const int kbits = khi_max_s ? 128 - __clzll((long long)khi_max_s) : (klo_max_s ? 64 - __clzll((long long)klo_max_s) : 0);
       // the sort's second buffer in R0 (the per-segment keys are dead)
       uint64_t* ylo = ea;
       uint64_t* yhi = ylo + nc;
       int32_t* yid = reinterpret_cast<int32_t*>(yhi + nc);
-      CWTS(5);
-      const bool kin_b = block_radix_sort<2>(xlo, xhi, xid, ylo, yhi, yid, nc, kbits, cnt, rwarp_s);
-      CWTS(6);
+      const bool kin_b = block_radix_sort<2>(xlo, xhi, xid, ylo, yhi, yid, nc, kbits, cnt, rwarp_s, 0);
       const uint64_t* slo = kin_b ? ylo : xlo;
       const uint64_t* shi = kin_b ? yhi : xhi;
       const int32_t* sid = kin_b ? yid : xid;
       // dense rank of the distinct keys; class per segment (0 = uncovered) in P.E[nu + k]
-      for (int k = threadIdx.x; k < ns; k += blockDim.x) P.E[nu + k] = 0;
-      int64_t rcarry = 0;
       for (int base = 0; base < nc; base += blockDim.x) {
         const int i = base + threadIdx.x;
         const bool first = i < nc && (i == 0 || slo[i] != slo[i - 1] || shi[i] != shi[i - 1]);
@@ -797,6 +970,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
         if (i < nc) P.E[nu + sid[i]] = rcarry + ex + (first ? 1 : 0);
         rcarry += tot;
       }
+      }   // !ranked
       __syncthreads();
       CWTS(7);
       // covered segments in E order -> the class table

@@ -221,6 +221,32 @@ def test_large_reorder_matches_closed_form(path):
         assert ev.pages_in_order() == cur, it
 
 
+@pytest.mark.parametrize("gap", [150, 60], ids=["one_group_of_35", "groups_of_three"])
+def test_class_table_groups_match_closed_form(gap):
+    """The wide class table sorts covered segments by (first window present,
+    its class there) and orders each such group by the full class tuple; a
+    window-1 run cut by many scattered window-0 pages makes one large group
+    (> 32 segments: the full-key sort takes over) or, with later windows
+    splitting it further, many small ones."""
+    rng = random.Random(gap)
+    D = 20000
+    ev = memman.EvictionList(domain_pages=D)
+    runs = port.norm_runs([(a, a + rng.randint(1, 40)) for a in range(0, 12000, 50)] + [(0, 6000)])
+    order = list(runs)
+    rng.shuffle(order)
+    ev.append_tail(order)
+    cur = [p for a, b in order for p in range(a, b)]
+    for it in range(2):
+        if gap > 100:   # one window-1 run cut into 35 segments of one tuple by window-0 pages
+            wins = [[(p, p + 1) for p in range(100 + it, 5100, gap)], [(0, 5200)], [(7000, 7100)], [(8000, 8001)]]
+        else:           # 100 window-1 runs, each cut by window 3 into three segments of two tuples
+            wins = [[(p, p + 1) for p in range(5500 + it, 6000, gap)], [(a, a + 40) for a in range(0, 5000, 50)],
+                    [(7000, 7100)], [(a + 10 + it, a + 17) for a in range(0, 5000, 50)]]
+        memman.reorder_for_opt(ev, (), {}, [memman.Window("t", wr, wr, PageSet(wr), 0) for wr in wins])
+        cur = _closed_form_reorder(cur, wins)
+        assert ev.pages_in_order() == cur, it
+
+
 @pytest.mark.parametrize("path", [0, 8], ids=["coop", "onesweep"])
 def test_randomized_list_ops_match_oracle(path):
     rng = random.Random(7)

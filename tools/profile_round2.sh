@@ -40,6 +40,9 @@ done
 for c in cfg2 cfg4 cfg1; do timeout 300 python tools/sw_phase_replay.py $c; done > $O/switch_kernel_phases.txt 2>&1
 for c in cfg2 cfg4 cfg1; do timeout 300 python tools/fw_phase_replay.py $c; done > $O/window_kernel_phases.txt 2>&1
 for c in cfg1 cfg3 cfg2 cfg4; do echo "== $c"; timeout 300 python tools/prof_replay.py $c 4; done > $O/planonly_all.txt 2>&1
+timeout 600 python tools/ms_devtime.py cfg1 cfg3 cfg2 cfg4 frag --reps 4 > $O/planonly_devtime.jsonl 2>&1
+timeout 300 python tools/cw_phase_replay.py frag > $O/frag_window_phases.txt 2>&1
+for c in cfg2 cfg4; do timeout 300 python tools/mc_cta_replay.py $c | tail -3; done > $O/multisplit_cta_phases.txt 2>&1
 MSG_HOST_PHASES=1 timeout 300 python tools/prof_replay.py cfg2 3 > $O/host_phases_cfg2.txt 2>&1
 MSG_HOST_PHASES=1 timeout 300 python tools/prof_replay.py cfg4 2 > $O/host_phases_cfg4.txt 2>&1
 timeout 300 python tools/predict_latency.py > $O/predict_latency.txt 2>&1
