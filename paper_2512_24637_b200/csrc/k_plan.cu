@@ -759,7 +759,23 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       int64_t* E = reinterpret_cast<int64_t*>(dyn_smem + e_off);
       int32_t(*cnt)[256] = reinterpret_cast<int32_t(*)[256]>(dyn_smem + cnt_off);
       if (threadIdx.x == 0) { mn_s = ~0ull; mx_s = 0; klo_max_s = 0; khi_max_s = 0; }
+      // endpoints as dense page ids when the span table fits the X region
+      // (unused until the painting is done): the dense map is monotone and
+      // only closes the gaps between spans, which no run covers, so the
+      // covered segments are the same and the keys span fewer bits (one radix
+      // pass less at the fragmented configuration: 30 -> 22 bits)
+      const bool dmode = P.nspans <= 1024 && x_off + 16ll * P.nspans <= smem_cap;
+      int64_t* sfirst = reinterpret_cast<int64_t*>(dyn_smem + x_off);
+      int64_t* sdense = sfirst + P.nspans;
+      if (dmode)
+        for (int i = threadIdx.x; i < P.nspans; i += blockDim.x) { sfirst[i] = P.span_first[i]; sdense[i] = P.span_dense[i]; }
       __syncthreads();
+      auto to_dense = [&](int64_t a) -> int64_t {
+        if (!dmode) return a;
+        int lo = 0, hi = P.nspans;
+        while (lo < hi) { const int mid = (lo + hi) >> 1; if (sfirst[mid] <= a) lo = mid + 1; else hi = mid; }
+        return sdense[lo - 1] + (a - sfirst[lo - 1]);
+      };
       {
         unsigned long long vmn = ~0ull, vmx = 0;
         for (int i = threadIdx.x; i < m; i += blockDim.x) {
@@ -767,7 +783,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
           int w = 0;
           while (gi >= npre_s[w + 1]) ++w;
           const int64_t r = rbase_s[w] + (gi - npre_s[w]);
-          const uint64_t v = (uint64_t)((i & 1) ? P.run_b[r] : P.run_a[r]);
+          const uint64_t v = (uint64_t)to_dense((i & 1) ? P.run_b[r] : P.run_a[r]);
           ea[i] = v;
           vmn = v < vmn ? v : vmn;
           vmx = v > vmx ? v : vmx;
@@ -804,21 +820,26 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       for (int k = threadIdx.x; k < ns; k += blockDim.x) { klo[k] = 0; khi[k] = 0; }
       __syncthreads();
       CWTS(3);
-      for (int w = 0; w < W; ++w) {
-        const int64_t nr = npre_s[w + 1] - npre_s[w];
-        const u128 mw = mult_s[w];
-        for (int64_t g = threadIdx.x; g < nr; g += blockDim.x) {
-          const int64_t r = rbase_s[w] + g;
-          const int32_t cls = P.run_cls ? P.run_cls[r] : (int32_t)(nr - g);
-          const u128 add = mw * (u128)(uint32_t)cls;
-          const int64_t s0 = lower_bound_i64(E, nu, P.run_a[r]), s1 = lower_bound_i64(E, nu, P.run_b[r]);
-          for (int64_t k = s0; k < s1; ++k) {
-            const u128 v = (((u128)khi[k]) << 64 | klo[k]) + add;
-            klo[k] = (uint64_t)v; khi[k] = (uint64_t)(v >> 64);
-          }
+      // every window's runs at once (was one window per barrier round): a
+      // segment several windows cover sums their contributions with 64-bit
+      // shared atomics, each low-word add's carry added to the high word, so
+      // the 128-bit total does not depend on the order
+      for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+        int w = 0;
+        while (i >= npre_s[w + 1]) ++w;
+        const int64_t g = i - npre_s[w], nr = npre_s[w + 1] - npre_s[w];
+        const int64_t r = rbase_s[w] + g;
+        const int32_t cls = P.run_cls ? P.run_cls[r] : (int32_t)(nr - g);
+        const u128 add = mult_s[w] * (u128)(uint32_t)cls;
+        const unsigned long long alo = (uint64_t)add, ahi = (uint64_t)(add >> 64);
+        const int64_t s0 = lower_bound_i64(E, nu, to_dense(P.run_a[r])), s1 = lower_bound_i64(E, nu, to_dense(P.run_b[r]));
+        for (int64_t k = s0; k < s1; ++k) {
+          const unsigned long long old = atomicAdd(reinterpret_cast<unsigned long long*>(klo + k), alo);
+          const unsigned long long c = old + alo < old ? 1ull : 0ull;
+          if (ahi | c) atomicAdd(reinterpret_cast<unsigned long long*>(khi + k), ahi + c);
         }
-        __syncthreads();
       }
+      __syncthreads();
       CWTS(4);
       // covered segments -> X (key lo, key hi, segment index), in segment order
       int nc = 0;
@@ -982,7 +1003,7 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
         const int32_t ex = block_excl_scan<int32_t>(cls > 0 ? 1 : 0, rwarp_s, &tot);
         if (cls > 0) {
           const int64_t ci = oc + ex;
-          P.seg_lo[ci] = dense_at(P, E[k]);
+          P.seg_lo[ci] = dmode ? E[k] : dense_at(P, E[k]);
           P.seg_hi[ci] = P.seg_lo[ci] + (E[k + 1] - E[k]);
           P.seg_cls[ci] = (int32_t)cls;
         }
