@@ -640,12 +640,11 @@ __device__ bool block_radix_sort(uint64_t* a0, uint64_t* a1, int32_t* av, uint64
     };
     for (int j = lane; j < 256; j += 32) cnt[w][j] = 0;
     __syncwarp();
+    // counts need no order: one shared atomic per element on the warp's own
+    // row (__match_any_sync here cost 9x more: tools/radix_probe.cu)
     for (int i0 = lo; i0 < hi; i0 += 32) {
       const int i = i0 + lane;
-      const int d = i < hi ? digit(i) : 256;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
-      if (d < 256 && lane == __ffs(peers) - 1) cnt[w][d] += __popc(peers);
-      __syncwarp();
+      if (i < hi) atomicAdd(&cnt[w][digit(i)], 1);
     }
     __syncthreads();
     // exclusive offsets in (digit, warp) order: thread t owns digit t/4, warps 8(t%4) .. +8
@@ -663,7 +662,14 @@ __device__ bool block_radix_sort(uint64_t* a0, uint64_t* a1, int32_t* av, uint64
     for (int i0 = lo; i0 < hi; i0 += 32) {
       const int i = i0 + lane;
       const int d = i < hi ? digit(i) : 256;
-      const uint32_t peers = __match_any_sync(0xffffffffu, d);
+      // lanes holding the same digit, built from nine ballots (the stable
+      // rank is the count of such lanes below this one)
+      uint32_t peers = 0xffffffffu;
+#pragma unroll
+      for (int bt = 0; bt < 9; ++bt) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> bt) & 1);
+        peers &= ((d >> bt) & 1) ? bal : ~bal;
+      }
       const int32_t before = d < 256 ? cnt[w][d] : 0;
       __syncwarp();
       if (d < 256) {
