@@ -2315,8 +2315,7 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
           const bool vk = valid(o);
           const int dk = vk ? lane_digit(fetch(o)) : 256;
           if (vk) dig[q * MS_CHUNK + 32 * k + lane] = (uint8_t)dk;
-          const uint32_t peers = __match_any_sync(0xffffffffu, dk);
-          if (dk < 256 && lane == __ffs(peers) - 1) atomicAdd(&cnt[own][dk], __popc(peers));
+          if (dk < 256) atomicAdd(&cnt[own][dk], 1);   // (counts need no lane match)
         }
       }
       if (nq) __syncthreads();
