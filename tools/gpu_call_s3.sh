@@ -1,6 +1,7 @@
 set -u
-O=gpurun_out/s3m
+O=gpurun_out/final
 mkdir -p $O
-for lib in tools/bin/libmsched_prev.so paper_2512_24637_b200/libmsched_b200.so; do echo "== $lib"; MSG_LIB=$lib timeout 600 python tools/ms_devtime.py frag cfg2 cfg3 --reps 3; done > $O/walls.txt 2>&1
-cat $O/walls.txt
-timeout 600 python -m pytest tests/test_gpu_facade.py tests/test_gpu_parity.py -q -x -p no:cacheprovider > $O/focus.log 2>&1; tail -2 $O/focus.log
+timeout 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > $O/gpu_tests.log 2>&1; tail -2 $O/gpu_tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.build(); g.smoke(); print('smoke ok')" > $O/smoke.log 2>&1; tail -1 $O/smoke.log
+timeout 2400 python bench.py > $O/bench.jsonl 2> $O/bench.err; tail -c 300 $O/bench.jsonl
+timeout 600 python tools/ms_devtime.py cfg1 cfg3 cfg2 cfg4 frag --reps 4 > $O/planonly_devtime.jsonl 2>&1
