@@ -919,13 +919,18 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
             const int a = (int)(u & kSeg), b = (int)(v & kSeg);
             return khi[a] < khi[b] || (khi[a] == khi[b] && klo[a] < klo[b]);
           };
+          // group starts first (the free payload slots of X hold the flags), so
+          // a group's thread reads and writes only its own group's entries
+          int32_t* gstart = xid;
+          for (int i = threadIdx.x; i < nc; i += blockDim.x)
+            gstart[i] = i == 0 || (ps[i - 1] >> IDB) != (ps[i] >> IDB);
+          __syncthreads();
           for (int i = threadIdx.x; i < nc; i += blockDim.x) {
-            const uint64_t pi = ps[i] >> IDB;
-            if (i > 0 && (ps[i - 1] >> IDB) == pi) continue;   // not a group start
+            if (!gstart[i]) continue;
             int j = i + 1;
-            while (j < nc && (ps[j] >> IDB) == pi && j - i <= 32) ++j;
-            if (j - i > 32) { big_s = 1; continue; }
-            for (int a = i + 1; a < j; ++a) {   // (group members share the primary bits others read)
+            while (j < nc && !gstart[j] && j - i <= 32) ++j;
+            if (j - i > 32) { atomicOr(&big_s, 1); continue; }
+            for (int a = i + 1; a < j; ++a) {
               const uint64_t v = ps[a];
               int b = a;
               while (b > i && kless(v, ps[b - 1])) { ps[b] = ps[b - 1]; --b; }

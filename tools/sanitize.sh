@@ -32,4 +32,10 @@ run $CS --tool racecheck python -m pytest tests/test_gpu_engine.py -x -q -k "asy
 run $CS --tool synccheck python -m pytest tests/test_gpu_engine.py -x -q -k "async"
 run $CS --tool initcheck python -m pytest tests/test_gpu_engine.py -x -q -k "async"
 run $CS --tool memcheck python -m pytest tests/test_gpu_engine.py tests/test_gpu_msim_plugin.py -x -q
+# late round 2: the queued per-entry chunks of the multisplit, the grouped class-table keys, the radix-sorted
+# window runs (general kernels forced by MSG_FALLBACK on the fragmented goldens)
+run $CS --tool racecheck python -m pytest tests/test_gpu_facade.py -x -q -k "class_table_groups or multi_window"
+MSG_FALLBACK=windows,demand run $CS --tool racecheck python -m pytest tests/test_gpu_parity.py -x -q -k "general_kernels and frag"
+MSG_FALLBACK=windows,demand run $CS --tool memcheck python -m pytest tests/test_gpu_parity.py tests/test_gpu_facade.py -x -q -k "frag or class_table_groups or large_reorder"
+run $CS --tool synccheck python -m pytest tests/test_gpu_facade.py -x -q -k "class_table_groups"
 cat $O
