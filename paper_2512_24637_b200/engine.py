@@ -230,6 +230,9 @@ class Simulator:
         self.hw, self.policy, self.mode, self.feeder = hw, policy, mode, feeder
         self.page = hw.page_size_bytes
         self.capacity = hw.hbm_capacity_pages
+        # per-page copy costs of the pipelined-swap model, computed once
+        # (populate_ready runs for every new gating prefix of a slice)
+        self._cost_e, self._cost_p = evict_page_cost_s(hw), populate_page_cost_s(hw)
         self._source = list(tasks)
         self.record_events = record_events
         self.recorder = recorder
@@ -530,12 +533,14 @@ class Simulator:
         fast = self.mode.name in ("proactive", "ideal") and state is not None
         last_j, last_ready = None, 0.0   # populate_ready is pure: memo by j (the prefix repeats)
         ncmd = len(task.commands)
+        if pending is not None:
+            prefix, p_free, p_nev = pending["prefix"], pending["free"], pending["n_evict"]
         while task.cursor < ncmd and elapsed < budget:
             cur = task.cursor
             if pending is not None:
-                j = pending["prefix"].get(cur, 0)
+                j = prefix.get(cur, 0)
                 if j != last_j:
-                    last_j, last_ready = j, populate_ready(self.hw, j, pending["free"], pending["n_evict"])
+                    last_j, last_ready = j, self._populate_ready(j, p_free, p_nev)
                 ready = last_ready
                 if ready > offset:
                     self.metrics.migration_s += ready - offset
@@ -553,6 +558,22 @@ class Simulator:
             offset = pending["evict_done"]
         self.t = slice_start + offset
         self.metrics.exec_s += elapsed
+
+    def _populate_ready(self, j: int, free_pages: int, n_evict: int) -> float:
+        """populate_ready (engine.py:139-158) with the per-page costs cached:
+        the same candidates and the same FP64 expressions, so the same float."""
+        if j <= 0:
+            return 0.0
+        e, p = self._cost_e, self._cost_p
+        f = free_pages if free_pages > 0 else 0
+        cap = n_evict + f
+        best = 0.0
+        for i in (1, f + 1 if f + 1 < j else j, j):   # every candidate is >= 1 here
+            lag = (i if i < cap else cap) - f
+            v = (lag if lag > 0 else 0) * e + (j - i + 1) * p
+            if v > best:
+                best = v
+        return best
 
     def _um_records(self, task_id, flat):
         i = 0
