@@ -431,9 +431,9 @@ class Simulator:
         """ReorderStats.pages_advised: reversed windows, dict first-insertion
         order (memman.py:238-241)."""
         adv: dict = {}
-        for (ti, _, _), n in zip(reversed(windows), reversed(list(win_pages))):
+        for (ti, _, _), n in zip(reversed(windows), reversed(win_pages.tolist())):
             tid = self.tasks[ti].id
-            adv[tid] = adv.get(tid, 0) + int(n)
+            adv[tid] = adv.get(tid, 0) + n
         return adv
 
     def _madvise_cost(self, adv: dict) -> float:

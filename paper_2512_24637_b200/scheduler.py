@@ -40,6 +40,19 @@ class Policy:
             raise ValueError(f"unknown policy kind {self.kind!r}")
 
 
+def _entry(task_id: str, timeslice_s: float, cursor: int) -> TimelineEntry:
+    """TimelineEntry(task_id, timeslice_s, cursor) without the frozen
+    dataclass's per-field object.__setattr__ calls (the same object: equal,
+    same hash and repr); build_timeline makes one per horizon entry every
+    context switch."""
+    e = object.__new__(TimelineEntry)
+    d = e.__dict__
+    d["task_id"] = task_id
+    d["timeslice_s"] = timeslice_s
+    d["resume_command_cursor"] = cursor
+    return e
+
+
 def project_cursor(latencies: Sequence[float], cursor: int, budget: float) -> int:
     """Cursor after one slice: every command that starts inside the slice
     runs to completion (scheduler.py:86-97, memman.py:186-195)."""
@@ -83,7 +96,7 @@ def build_timeline(policy: Policy, tasks, horizon_entries: int | None = None,
             rr = [x for x in rr if pos[x.id] < len(lat[x.id])]
             k = 0
             continue
-        plan.append(TimelineEntry(t.id, policy.timeslice_s, pos[t.id]))
+        plan.append(_entry(t.id, policy.timeslice_s, pos[t.id]))
         pos[t.id] = (project(t.id, pos[t.id], policy.timeslice_s) if project is not None
                      else project_cursor(lat[t.id], pos[t.id], policy.timeslice_s))
         k += 1
