@@ -1,5 +1,5 @@
 set -u
-O=gpurun_out/s3o
+O=gpurun_out/s3p
 mkdir -p $O
 timeout 1200 python -m pytest tests -m gpu -q -x -p no:cacheprovider > $O/gpu_tests.log 2>&1; tail -2 $O/gpu_tests.log
 timeout 600 python tools/ms_devtime.py cfg1 cfg3 cfg2 cfg4 frag --reps 4 > $O/planonly_devtime.jsonl 2>&1
