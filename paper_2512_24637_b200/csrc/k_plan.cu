@@ -697,14 +697,18 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
   __shared__ int64_t npre_s[65], rbase_s[64];   // per-window run prefix and scratch base (W <= 64)
   const int W = P.nwin;
   if (threadIdx.x < 64) rad_s[threadIdx.x] = 0;
+  // per-window counts and bases loaded by one thread each (one thread walking
+  // them was a chain of dependent global round trips), then prefixed
+  if (threadIdx.x < W && threadIdx.x < 64) {
+    npre_s[threadIdx.x + 1] = P.nruns[threadIdx.x];
+    rbase_s[threadIdx.x] = P.run_base[threadIdx.x];
+  }
+  __syncthreads();
   if (threadIdx.x == 0) {
-    int64_t t = 0;
-    for (int w = 0; w < W; ++w) {
-      if (w < 64) { npre_s[w] = t; rbase_s[w] = P.run_base[w]; }
-      t += P.nruns[w];
-    }
-    if (W <= 64) npre_s[W] = t;
-    tot_runs_s = t;
+    const int Wc = W < 64 ? W : 64;   // (W > 64 exits below, before the total is used)
+    npre_s[0] = 0;
+    for (int w = 0; w < Wc; ++w) npre_s[w + 1] += npre_s[w];
+    tot_runs_s = npre_s[Wc];
   }
   __syncthreads();
   const int64_t M = tot_runs_s;
@@ -734,11 +738,14 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
   if (threadIdx.x == 0) {
     ok_s = W <= 64;
     u128 m = 1;
-    const u128 lim = ((u128)1) << 127;
     for (int w = W - 1; w >= 0 && ok_s; --w) {
       mult_s[w] = m;
-      const u128 rad = (u128)(uint32_t)rad_s[w] + 1;
-      if (m > lim / rad) ok_s = 0;
+      // m * rad <= 2^127 (the radices fit), decided from the 64-bit halves of
+      // the product instead of a 128-bit division
+      const uint64_t rad = (uint64_t)(uint32_t)rad_s[w] + 1;
+      const u128 lo = (u128)(uint64_t)m * rad;
+      const u128 hi = (m >> 64) * rad + (lo >> 64);   // product >> 64 (< 2^97)
+      if (hi > ((u128)1 << 63) || (hi == ((u128)1 << 63) && (uint64_t)lo != 0)) ok_s = 0;
       else m *= rad;
     }
     *ok_out = ok_s;
@@ -784,7 +791,8 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       };
       {
         unsigned long long vmn = ~0ull, vmx = 0;
-        for (int i = threadIdx.x; i < m; i += blockDim.x) {
+#pragma unroll 4
+        for (int i = threadIdx.x; i < m; i += blockDim.x) {   // (unrolled: the endpoint loads overlap)
           const int64_t gi = i >> 1;
           int w = 0;
           while (gi >= npre_s[w + 1]) ++w;
