@@ -855,12 +855,17 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       }
       __syncthreads();
       CWTS(4);
-      // covered segments -> X (key lo, key hi, segment index), in segment order
-      int nc = 0;
-      for (int base = 0; base < ns; base += blockDim.x) {
-        const int k = base + threadIdx.x;
-        nc += __syncthreads_count(k < ns && (klo[k] | khi[k]) != 0);
-      }
+      // covered segments -> X (key lo, key hi, segment index), in segment order.
+      // Each thread owns a contiguous run of segments: one count and one
+      // block scan give every thread its output offset (was a barrier-bound
+      // scan round per 1024 segments)
+      const int per_t = (ns + (int)blockDim.x - 1) / (int)blockDim.x;
+      const int k0 = (int)threadIdx.x * per_t, k1 = k0 + per_t < ns ? k0 + per_t : ns;
+      int mine = 0;
+      for (int k = k0; k < k1; ++k) mine += (klo[k] | khi[k]) != 0;
+      int32_t nc_tot;
+      const int32_t my_off = block_excl_scan<int32_t>(mine, rwarp_s, &nc_tot);
+      const int nc = nc_tot;
       if (20ll * nc > 16 * m0 || x_off + 20ll * nc > smem_cap) {
         // the covered set does not fit on chip: the tuple-comparison kernel takes it
         if (threadIdx.x == 0) *ok_out = 0;
@@ -893,28 +898,22 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
         if (IDB + wb + cb <= 64 && ns < (1 << IDB)) {
           uint64_t* pk = xlo;   // packed (primary << IDB | segment), in segment order
           uint64_t* pk2 = xhi;  // the sort's second buffer
-          int64_t carry2 = 0;
-          for (int base = 0; base < ns; base += blockDim.x) {
-            const int k = base + threadIdx.x;
-            const bool cov = k < ns && (klo[k] | khi[k]) != 0;
-            int32_t tot;
-            const int32_t ex = block_excl_scan<int32_t>(cov ? 1 : 0, rwarp_s, &tot);
-            if (cov) {
-              const u128 key = ((u128)khi[k]) << 64 | klo[k];
-              int ws = 0;   // smallest w with mult[w] <= key (mult falls with w)
-              while (ws + 1 < W && mult_s[ws] > key) ++ws;
-              // c* = key / mult[w*]: a double-precision estimate (within one of
-              // the quotient, which is < 2^20), corrected exactly -- a 128-bit
-              // division per segment was the phase's cost
-              const u128 mw = mult_s[ws];
-              const double kd = (double)khi[k] * 18446744073709551616.0 + (double)klo[k];
-              const double md = (double)(uint64_t)(mw >> 64) * 18446744073709551616.0 + (double)(uint64_t)mw;
-              uint64_t cs = (uint64_t)(kd / md);
-              while (cs > 0 && (u128)cs * mw > key) --cs;
-              while ((u128)(cs + 1) * mw <= key) ++cs;
-              pk[carry2 + ex] = ((((uint64_t)(W - 1 - ws)) << cb | cs) << IDB) | (uint64_t)k;
-            }
-            carry2 += tot;
+          int o = my_off;
+          for (int k = k0; k < k1; ++k) {
+            if ((klo[k] | khi[k]) == 0) continue;
+            const u128 key = ((u128)khi[k]) << 64 | klo[k];
+            int ws = 0;   // smallest w with mult[w] <= key (mult falls with w)
+            while (ws + 1 < W && mult_s[ws] > key) ++ws;
+            // c* = key / mult[w*]: a double-precision estimate (within one of
+            // the quotient, which is < 2^20), corrected exactly -- a 128-bit
+            // division per segment was the phase's cost
+            const u128 mw = mult_s[ws];
+            const double kd = (double)khi[k] * 18446744073709551616.0 + (double)klo[k];
+            const double md = (double)(uint64_t)(mw >> 64) * 18446744073709551616.0 + (double)(uint64_t)mw;
+            uint64_t cs = (uint64_t)(kd / md);
+            while (cs > 0 && (u128)cs * mw > key) --cs;
+            while ((u128)(cs + 1) * mw <= key) ++cs;
+            pk[o++] = ((((uint64_t)(W - 1 - ws)) << cb | cs) << IDB) | (uint64_t)k;
           }
           if (threadIdx.x == 0) big_s = 0;
           __syncthreads();
