@@ -820,12 +820,20 @@ __global__ void __launch_bounds__(1024, 1) k_window_combine_wide(CombineParams P
       const bool ein_b = block_radix_sort<1>(ea, nullptr, nullptr, eb, nullptr, nullptr, m, ebits, cnt, rwarp_s, 0);
       CWTS(2);
       const uint64_t* es = ein_b ? eb : ea;
-      int32_t* fl = reinterpret_cast<int32_t*>(ein_b ? ea : eb);   // the free buffer: unique flags -> positions
-      for (int i = threadIdx.x; i < m; i += blockDim.x) fl[i] = (i == 0 || es[i] != es[i - 1]) ? 1 : 0;
-      __syncthreads();
-      const int nu = block_scan_array<int32_t>(fl, m);
-      for (int i = threadIdx.x; i < m; i += blockDim.x)
-        if (i == 0 || es[i] != es[i - 1]) E[fl[i]] = (int64_t)(es[i] + mn);
+      // unique endpoints -> E: each thread owns a contiguous run of the sorted
+      // endpoints, one block scan of the per-thread unique counts
+      int nu;
+      {
+        const int per_e = (m + (int)blockDim.x - 1) / (int)blockDim.x;
+        const int i0 = (int)threadIdx.x * per_e, i1 = i0 + per_e < m ? i0 + per_e : m;
+        int mine = 0;
+        for (int i = i0; i < i1; ++i) mine += (i == 0 || es[i] != es[i - 1]);
+        int32_t tot;
+        int o = block_excl_scan<int32_t>(mine, rwarp_s, &tot);
+        for (int i = i0; i < i1; ++i)
+          if (i == 0 || es[i] != es[i - 1]) E[o++] = (int64_t)(es[i] + mn);
+        nu = tot;
+      }
       __syncthreads();
       const int ns = nu - 1;
       // per-segment 128-bit keys in R0 (the endpoint buffers are dead)
