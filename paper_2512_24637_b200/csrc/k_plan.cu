@@ -2947,8 +2947,8 @@ __device__ __forceinline__ void apply_body(const ApplyArgs& A, int& nbar, unsign
     for (int64_t i = i0; i < i1; ++i) {
       const Iv v = A.act_pool[i];
       const int64_t lo = v.d, hi = v.d + (v.b - v.a), w0 = lo >> 5, nw = ((hi + 31) >> 5) - w0;
-      int64_t k = (me - skip) % T;
-      if (k < 0) k += T;
+      // (me - skip) mod T; T = AP_SPLIT * 1024 is a power of two: a mask instead of a 64-bit remainder per interval
+      int64_t k = (T & (T - 1)) == 0 ? ((me - skip) & (T - 1)) : (((me - skip) % T) + T) % T;
       for (; k < nw; k += T) acc += __popc(~__ldcg(A.bits + w0 + k) & unit_mask(lo, hi, w0 + k));
       skip += nw;
     }

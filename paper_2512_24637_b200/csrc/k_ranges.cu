@@ -85,8 +85,7 @@ __global__ void __launch_bounds__(256) k_touch_counts(const Iv* __restrict__ poo
   for (int64_t i = i0; i < i1; ++i) {
     const Iv v = pool[i];
     const int64_t lo = v.d, hi = v.d + (v.b - v.a), w0 = lo >> 5, nw = ((hi + 31) >> 5) - w0;
-    int64_t k = (me - skip) % T;
-    if (k < 0) k += T;
+    int64_t k = (T & (T - 1)) == 0 ? ((me - skip) & (T - 1)) : (((me - skip) % T) + T) % T;   // (me - skip) mod T
     for (; k < nw; k += T) acc += __popc(~bits[w0 + k] & unit_mask(lo, hi, w0 + k));
     skip += nw;
   }
