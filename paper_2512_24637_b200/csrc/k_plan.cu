@@ -2123,10 +2123,16 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
   // round trip instead of two (entries past the count are never searched).
   SegView S;
   {
+    // (the first kEager entries are loaded before the count arrives; the rest,
+    // up to the count, after it: loading the whole allocated capacity staged 4x
+    // the table for fragmented windows)
+    constexpr int64_t kEager = 2048;
     const int64_t nn = *A.T.n;
+    int64_t eager = 0;
     if (A.T.cap > 0) {
-      const int64_t lim = A.T.cap < A.tcap ? A.T.cap : A.tcap;
-      for (int64_t i = tid; i < lim; i += MC_THREADS) {
+      eager = A.T.cap < A.tcap ? A.T.cap : A.tcap;
+      eager = eager < kEager ? eager : kEager;
+      for (int64_t i = tid; i < eager; i += MC_THREADS) {
         lo32[i] = (int32_t)A.T.lo[i]; hi32[i] = (int32_t)A.T.hi[i]; cls32[i] = A.T.cls[i];
       }
     }
@@ -2135,8 +2141,8 @@ __device__ __forceinline__ void ms_coop_body(const McArgs& A, unsigned char* mc_
     S.small = nn <= A.tcap;
     S.lo = A.T.lo; S.hi = A.T.hi; S.cls = A.T.cls;
     S.lo32 = lo32; S.hi32 = hi32; S.cls32 = cls32;
-    if (S.small && A.T.cap <= 0)
-      for (int64_t i = tid; i < nn; i += MC_THREADS) {
+    if (S.small)
+      for (int64_t i = eager + tid; i < nn; i += MC_THREADS) {
         lo32[i] = (int32_t)A.T.lo[i]; hi32[i] = (int32_t)A.T.hi[i]; cls32[i] = A.T.cls[i];
       }
   }
