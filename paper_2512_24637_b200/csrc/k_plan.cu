@@ -647,16 +647,34 @@ __device__ bool block_radix_sort(uint64_t* a0, uint64_t* a1, int32_t* av, uint64
       if (i < hi) atomicAdd(&cnt[w][digit(i)], 1);
     }
     __syncthreads();
-    // exclusive offsets in (digit, warp) order: thread t owns digit t/4, warps 8(t%4) .. +8
+    // exclusive offsets in (digit, warp) order: thread d < 256 walks digit d's
+    // column over the 32 warp rows (consecutive digits: conflict-free), the
+    // 256 digit totals are scanned by warps 0-7, and the digit bases are added
+    // back down the columns -- two barriers instead of a 1024-wide block scan
+    // (the scan was the fixed cost of a pass: tools/radix_probe.cu)
     {
-      const int d = threadIdx.x >> 2, wq = (threadIdx.x & 3) * 8;
-      int32_t sum = 0;
+      const int t = threadIdx.x, ln = t & 31, wid = t >> 5;
+      int32_t excl = 0;
+      if (t < 256) {
+        int32_t tot = 0;
+#pragma unroll 8
+        for (int ww = 0; ww < 32; ++ww) { const int32_t c = cnt[ww][t]; cnt[ww][t] = tot; tot += c; }
+        int32_t x = tot;
 #pragma unroll
-      for (int j = 0; j < 8; ++j) sum += cnt[wq + j][d];
-      int32_t tot;
-      int32_t run = block_excl_scan<int32_t>(sum, warp_s, &tot);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) { const int32_t c = cnt[wq + j][d]; cnt[wq + j][d] = run; run += c; }
+        for (int o = 1; o < 32; o <<= 1) {
+          const int32_t y = __shfl_up_sync(0xffffffffu, x, o);
+          if (ln >= o) x += y;
+        }
+        if (ln == 31) warp_s[wid] = x;
+        excl = x - tot;
+      }
+      __syncthreads();
+      if (t < 256) {
+        int32_t base = excl;
+        for (int k = 0; k < wid; ++k) base += warp_s[k];
+#pragma unroll 8
+        for (int ww = 0; ww < 32; ++ww) cnt[ww][t] += base;
+      }
     }
     __syncthreads();
     for (int i0 = lo; i0 < hi; i0 += 32) {

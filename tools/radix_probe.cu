@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(1024, 1) k_probe(const uint64_t* keys, int n, 
     }
     __syncthreads();
     const unsigned long long c1 = clock64();
-    {
+    if (MODE < 3) {
       const int d = threadIdx.x >> 2, wq = (threadIdx.x & 3) * 8;
       int32_t sum = 0;
 #pragma unroll
@@ -91,13 +91,33 @@ __global__ void __launch_bounds__(1024, 1) k_probe(const uint64_t* keys, int n, 
       int32_t run = block_excl_scan<int32_t>(sum, warp_s, &tot);
 #pragma unroll
       for (int j = 0; j < 8; ++j) { const int32_t c = cnt[wq + j][d]; cnt[wq + j][d] = run; run += c; }
+    } else {   // column walk + 256-wide scan (the kernel's scan)
+      const int t = threadIdx.x, ln = t & 31, wid = t >> 5;
+      int32_t excl = 0;
+      if (t < 256) {
+        int32_t tot = 0;
+#pragma unroll 8
+        for (int ww = 0; ww < 32; ++ww) { const int32_t c = cnt[ww][t]; cnt[ww][t] = tot; tot += c; }
+        int32_t x = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) { const int32_t y = __shfl_up_sync(0xffffffffu, x, o); if (ln >= o) x += y; }
+        if (ln == 31) warp_s[wid] = x;
+        excl = x - tot;
+      }
+      __syncthreads();
+      if (t < 256) {
+        int32_t base = excl;
+        for (int k = 0; k < wid; ++k) base += warp_s[k];
+#pragma unroll 8
+        for (int ww = 0; ww < 32; ++ww) cnt[ww][t] += base;
+      }
     }
     __syncthreads();
     const unsigned long long c2 = clock64();
     for (int i0 = lo; i0 < hi; i0 += 32) {
       const int i = i0 + lane;
       const int d = i < hi ? (int)((s0[i] >> sh) & 255) : 256;
-      const uint32_t peers = MODE == 2 ? match9(d) : __match_any_sync(0xffffffffu, d);
+      const uint32_t peers = MODE >= 2 ? match9(d) : __match_any_sync(0xffffffffu, d);
       const int32_t before = d < 256 ? cnt[w][d] : 0;
       __syncwarp();
       if (d < 256) {
@@ -130,8 +150,9 @@ int main() {
   cudaFuncSetAttribute(k_probe<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_probe<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   cudaFuncSetAttribute(k_probe<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_probe<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   for (int n : {640, 5120}) {
-    for (int mode = 0; mode < 3; ++mode) {
+    for (int mode = 0; mode < 4; ++mode) {
       unsigned long long z[4] = {0, 0, 0, 0};
       cudaMemcpyToSymbol(g_ph, z, sizeof(z));
       cudaEvent_t a, b;
@@ -140,7 +161,8 @@ int main() {
       for (int r = 0; r < 100; ++r) {
         if (mode == 0) k_probe<0><<<1, 1024, smem>>>(dk, n, 22, dout);
         else if (mode == 1) k_probe<1><<<1, 1024, smem>>>(dk, n, 22, dout);
-        else k_probe<2><<<1, 1024, smem>>>(dk, n, 22, dout);
+        else if (mode == 2) k_probe<2><<<1, 1024, smem>>>(dk, n, 22, dout);
+        else k_probe<3><<<1, 1024, smem>>>(dk, n, 22, dout);
       }
       cudaEventRecord(b);
       cudaEventSynchronize(b);
@@ -153,7 +175,7 @@ int main() {
       bool sorted = true;
       for (int i = 1; i < n; ++i) sorted &= res[i - 1] <= res[i];
       printf("n %5d %-22s kernel %.2f us; per sort (3 passes): count %.2f us, scan %.2f us, scatter %.2f us; sorted %d (%s)\n",
-             n, mode == 2 ? "atomics + ballot ranks" : mode ? "count by smem atomics" : "count by match_any", ms * 1e3 / 100,
+             n, mode == 3 ? "+ column-walk scan" : mode == 2 ? "atomics + ballot ranks" : mode ? "count by smem atomics" : "count by match_any", ms * 1e3 / 100,
              o[0] / (double)o[3] / 1965.0, o[1] / (double)o[3] / 1965.0, o[2] / (double)o[3] / 1965.0, (int)sorted,
              cudaGetErrorString(cudaGetLastError()));
     }
